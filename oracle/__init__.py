@@ -1,0 +1,122 @@
+"""ctypes shim over ``oracle/liboracle.so`` -- the sequential CPU Polylla oracle.
+
+TEST INFRASTRUCTURE ONLY.  Only ``tests/``, ``__graft_entry__.smoke()`` and the
+``cpu_baseline`` / ``--impl reference`` legs of ``bench.py`` may import this package.
+The product package ``paper_2403_14723_b200`` never imports it, and the oracle shares
+no code with the CUDA path (see the header of ``polylla_oracle.c``).
+
+Parity pins (what the oracle is checked against, independently of itself) live in
+``tests/test_oracle_pins.py``: hand-worked fixtures (Fig. 5, SPEC.md
+examples), closed forms for Alg. 13 grids, brute-force Lepp terminal-edge regions
+(Defs. 1-2), and invariants.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+_LIB = None
+
+STATUS = {
+    0: "OK", -1: "INVALID_ARGUMENT", -2: "DANGLING_INDEX", -3: "DEGENERATE_TRI",
+    -4: "NON_MANIFOLD_EDGE", -5: "NON_MANIFOLD_VERTEX", -6: "INDEX_OVERFLOW",
+    -8: "WALK_BOUND", -9: "UNSEEDED_LOOP", -12: "NOMEM",
+}
+
+PHASES = ("Build", "LM", "LF", "LS", "Trav", "Rep", "Extract", "Total")
+
+
+class OracleError(RuntimeError):
+    def __init__(self, code):
+        super().__init__(f"oracle status {code} ({STATUS.get(code, '?')})")
+        self.code = code
+
+
+class _IO(ctypes.Structure):
+    _fields_ = [
+        ("T", ctypes.c_int64), ("V", ctypes.c_int64),
+        ("xy", ctypes.c_void_p), ("tri", ctypes.c_void_p),
+        ("origin", ctypes.c_void_p), ("twin", ctypes.c_void_p),
+        ("next", ctypes.c_void_p), ("prev", ctypes.c_void_p),
+        ("next_pre", ctypes.c_void_p),
+        ("lcode", ctypes.c_void_p), ("longest", ctypes.c_void_p),
+        ("frontier0", ctypes.c_void_p), ("frontier1", ctypes.c_void_p),
+        ("seeds0", ctypes.c_void_p), ("seeds", ctypes.c_void_p),
+        ("offsets", ctypes.c_void_p), ("loops", ctypes.c_void_p),
+        ("tips", ctypes.c_void_p),
+        ("counts", ctypes.c_int64 * 10), ("times", ctypes.c_double * 8),
+    ]
+
+
+def _lib():
+    global _LIB
+    if _LIB is None:
+        path = os.path.join(_HERE, "liboracle.so")
+        if not os.path.exists(path):
+            raise RuntimeError(f"{path} missing: run __graft_entry__.build()")
+        lib = ctypes.CDLL(path)
+        lib.oracle_run.restype = ctypes.c_int
+        lib.oracle_run.argtypes = [ctypes.POINTER(_IO)]
+        lib.oracle_build.restype = ctypes.c_int
+        lib.oracle_build.argtypes = [ctypes.c_int64, ctypes.c_void_p, ctypes.c_int64, ctypes.c_void_p,
+                                     ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p,
+                                     ctypes.c_void_p]
+        _LIB = lib
+    return _LIB
+
+
+def build(xy: np.ndarray, tri: np.ndarray):
+    """Half-edge build only: returns dict origin/twin/next/prev, H, B, flips."""
+    xy = np.ascontiguousarray(xy, dtype=np.float64)
+    tri = np.ascontiguousarray(tri, dtype=np.int32)
+    V, T = xy.shape[0], tri.shape[0]
+    cap = max(6 * T, 1)
+    origin = np.empty(cap, np.int32); twin = np.empty(cap, np.int32)
+    nxt = np.empty(cap, np.int32); prv = np.empty(cap, np.int32)
+    hb = np.zeros(3, np.int64)
+    rc = _lib().oracle_build(V, xy.ctypes.data, T, tri.ctypes.data, origin.ctypes.data, twin.ctypes.data,
+                             nxt.ctypes.data, prv.ctypes.data, hb.ctypes.data)
+    if rc:
+        raise OracleError(rc)
+    H = int(hb[0])
+    return dict(origin=origin[:H], twin=twin[:H], next=nxt[:H], prev=prv[:H], H=H, B=int(hb[1]),
+                flips=int(hb[2]))
+
+
+def run(xy: np.ndarray, tri: np.ndarray):
+    """Full sequential Polylla (Alg. 1).  Returns a dict of numpy arrays + counts + times."""
+    xy = np.ascontiguousarray(xy, dtype=np.float64)
+    tri = np.ascontiguousarray(tri, dtype=np.int32)
+    V, T = xy.shape[0], tri.shape[0]
+    H = 6 * max(T, 1)
+    a = dict(
+        origin=np.empty(H, np.int32), twin=np.empty(H, np.int32), next=np.empty(H, np.int32),
+        prev=np.empty(H, np.int32), next_pre=np.empty(H, np.int32),
+        lcode=np.empty(max(T, 1), np.uint8), longest=np.empty(H, np.uint8),
+        frontier0=np.empty(H, np.uint8), frontier1=np.empty(H, np.uint8),
+        seeds0=np.empty(H, np.int32), seeds=np.empty(max(T, 1), np.int32),
+        offsets=np.empty(max(T, 1) + 1, np.int32), loops=np.empty(3 * max(T, 1), np.int32),
+        tips=np.empty(max(V, 1), np.int32),
+    )
+    io = _IO()
+    io.T, io.V = T, V
+    io.xy, io.tri = xy.ctypes.data, tri.ctypes.data
+    for k, v in a.items():
+        setattr(io, k, v.ctypes.data)
+    rc = _lib().oracle_run(ctypes.byref(io))
+    if rc:
+        raise OracleError(rc)
+    c = list(io.counts)
+    H, B, flips, n_seeds0, P, L, n_tips, n_mid = c[:8]
+    out = dict(
+        H=H, B=B, T=T, V=V, flips=flips, P=P, L=L, n_tips=n_tips, n_mid=n_mid, n_seeds0=n_seeds0,
+        origin=a["origin"][:H], twin=a["twin"][:H], next=a["next"][:H], prev=a["prev"][:H],
+        next_pre=a["next_pre"][:H], lcode=a["lcode"][:T], longest=a["longest"][:H],
+        frontier0=a["frontier0"][:H], frontier1=a["frontier1"][:H], seeds0=a["seeds0"][:n_seeds0],
+        seeds=a["seeds"][:P], offsets=a["offsets"][:P + 1], loops=a["loops"][:L], tips=a["tips"][:n_tips],
+        times=dict(zip(PHASES, list(io.times))),
+    )
+    return out
