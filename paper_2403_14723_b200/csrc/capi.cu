@@ -1,0 +1,341 @@
+// capi.cu -- the C ABI of libpolylla.so (include/polylla.h): argument validation,
+// workspace carving, call-order state, kernel orchestration.  No compute here: every
+// step of the conversion runs in the kernels of build.cu / label.cu / generate.cu /
+// extract.cu.
+#include <cstdlib>
+#include <cstring>
+
+#include "internal.cuh"
+
+namespace polylla {
+
+static size_t align_up(size_t x) { return (x + 255) & ~size_t(255); }
+
+static int64_t hash_cap_max_for(int64_t T) {
+  int64_t c = 1024;
+  while (c < 2 * 3 * T && c < (int64_t(1) << 31)) c <<= 1;
+  return c;
+}
+
+struct Layout {
+  size_t off[32];
+  size_t total;
+};
+
+// region order; sizes in bytes
+static Layout layout(int64_t V, int64_t T) {
+  const int64_t Hmax = 6 * T;
+  const int64_t nw = (3 * T + 31) / 32;
+  const int64_t nb = (nw + 2047) / 2048 + 1;
+  const int64_t cap = hash_cap_max_for(T);
+  const size_t sz[] = {
+      (size_t)Hmax * 4,       // 0 origin
+      (size_t)Hmax * 4,       // 1 twin
+      (size_t)Hmax * 4,       // 2 next
+      (size_t)T,              // 3 lcode
+      (size_t)nw * 4,         // 4 F0
+      (size_t)nw * 4,         // 5 F1
+      (size_t)nw * 4,         // 6 S
+      (size_t)nw * 4,         // 7 C
+      (size_t)nw * 4,         // 8 Bd
+      (size_t)(3 * T) * 4,    // 9 len
+      (size_t)(3 * T) * 8,    // 10 left_key
+      (size_t)(3 * T) * 4,    // 11 left_e
+      (size_t)cap * 4,        // 12 ehash
+      (size_t)cap * 4,        // 13 vkey
+      (size_t)cap * 4,        // 14 vval
+      (size_t)V * 4,          // 15 tips
+      (size_t)(2 * V) * 4,    // 16 aff
+      (size_t)(2 * V) * 4,    // 17 mids
+      (size_t)nb * 8,         // 18 scan_a
+      (size_t)nb * 8,         // 19 scan_b
+      (size_t)nb * 8,         // 20 scan_c
+      (size_t)T * 4,          // 21 seeds
+      (size_t)(T + 1) * 4,    // 22 offsets
+      (size_t)(3 * T) * 4,    // 23 loops staging
+      (size_t)(2 * V) * 8,    // 24 xy staging
+      (size_t)(3 * T) * 4,    // 25 tri staging
+      sizeof(DevCounters),    // 26 counters
+  };
+  Layout L{};
+  size_t o = 0;
+  for (size_t i = 0; i < sizeof(sz) / sizeof(sz[0]); ++i) {
+    L.off[i] = o;
+    o += align_up(sz[i]);
+  }
+  L.total = o;
+  return L;
+}
+
+size_t workspace_bytes(int64_t V, int64_t T) { return layout(V, T).total; }
+
+bool carve(Ctx* c, void* ws, size_t bytes) {
+  const Layout L = layout(c->V, c->T);
+  if (bytes < L.total || (reinterpret_cast<uintptr_t>(ws) & 255)) return false;
+  char* b = static_cast<char*>(ws);
+  c->Hmax = 6 * c->T;
+  c->origin = reinterpret_cast<int32_t*>(b + L.off[0]);
+  c->twin = reinterpret_cast<int32_t*>(b + L.off[1]);
+  c->next = reinterpret_cast<int32_t*>(b + L.off[2]);
+  c->lcode = reinterpret_cast<uint8_t*>(b + L.off[3]);
+  c->F0 = reinterpret_cast<uint32_t*>(b + L.off[4]);
+  c->F1 = reinterpret_cast<uint32_t*>(b + L.off[5]);
+  c->S = reinterpret_cast<uint32_t*>(b + L.off[6]);
+  c->C = reinterpret_cast<uint32_t*>(b + L.off[7]);
+  c->Bd = reinterpret_cast<uint32_t*>(b + L.off[8]);
+  c->len = reinterpret_cast<int32_t*>(b + L.off[9]);
+  c->left_key = reinterpret_cast<unsigned long long*>(b + L.off[10]);
+  c->left_e = reinterpret_cast<int32_t*>(b + L.off[11]);
+  c->ehash = reinterpret_cast<uint32_t*>(b + L.off[12]);
+  c->vkey = reinterpret_cast<uint32_t*>(b + L.off[13]);
+  c->vval = reinterpret_cast<int32_t*>(b + L.off[14]);
+  c->hash_cap_max = hash_cap_max_for(c->T);
+  c->tips = reinterpret_cast<int32_t*>(b + L.off[15]);
+  c->aff = reinterpret_cast<int32_t*>(b + L.off[16]);
+  c->mids = reinterpret_cast<int32_t*>(b + L.off[17]);
+  c->scan_a = reinterpret_cast<long long*>(b + L.off[18]);
+  c->scan_b = reinterpret_cast<long long*>(b + L.off[19]);
+  c->scan_c = reinterpret_cast<long long*>(b + L.off[20]);
+  c->seeds = reinterpret_cast<int32_t*>(b + L.off[21]);
+  c->offsets = reinterpret_cast<int32_t*>(b + L.off[22]);
+  c->loops = reinterpret_cast<int32_t*>(b + L.off[23]);
+  c->xy_stage = reinterpret_cast<double*>(b + L.off[24]);
+  c->tri_stage = reinterpret_cast<int32_t*>(b + L.off[25]);
+  c->ctr = reinterpret_cast<DevCounters*>(b + L.off[26]);
+  c->n_words = (3 * c->T + 31) / 32;
+  return true;
+}
+
+static polylla_status map_status(uint32_t st) {
+  if (!st) return POLYLLA_OK;
+  if (st & ST_DANGLING) return POLYLLA_E_DANGLING_INDEX;
+  if (st & ST_DEGENERATE) return POLYLLA_E_DEGENERATE_TRI;
+  if (st & ST_NONMANIFOLD_EDGE) return POLYLLA_E_NON_MANIFOLD_EDGE;
+  if (st & ST_NONMANIFOLD_VERTEX) return POLYLLA_E_NON_MANIFOLD_VERTEX;
+  if (st & ST_OVERFLOW) return POLYLLA_E_INDEX_OVERFLOW;
+  if (st & ST_WALK) return POLYLLA_E_WALK_BOUND;
+  if (st & ST_UNSEEDED) return POLYLLA_E_UNSEEDED_LOOP;
+  if (st & ST_CAPACITY) return POLYLLA_E_CAPACITY;
+  return POLYLLA_E_WORKSPACE;
+}
+
+}  // namespace polylla
+
+using namespace polylla;
+
+struct polylla_ctx {
+  Ctx c;
+};
+
+static inline cudaStream_t S(polylla_stream s) { return reinterpret_cast<cudaStream_t>(s); }
+
+extern "C" {
+
+POLYLLA_API size_t polylla_workspace_bytes(int64_t n_vertices, int64_t n_triangles) {
+  if (n_vertices < 0 || n_triangles < 0) return 0;
+  return workspace_bytes(n_vertices, n_triangles);
+}
+
+POLYLLA_API polylla_status polylla_build_halfedges(const double* xy, int64_t V, const int32_t* tri, int64_t T,
+                                                   void* workspace, size_t workspace_bytes_, polylla_stream stream,
+                                                   polylla_ctx** ctx_out) {
+  if (!ctx_out) return POLYLLA_E_INVALID_ARGUMENT;
+  *ctx_out = nullptr;
+  if (!xy || !tri || !workspace || V < 3 || T < 1) return POLYLLA_E_INVALID_ARGUMENT;
+  if ((reinterpret_cast<uintptr_t>(xy) & 15) || (reinterpret_cast<uintptr_t>(tri) & 3))
+    return POLYLLA_E_INVALID_ARGUMENT;
+  if (3 * T > 0x7fffffffLL || V > 0x7fffffffLL) return POLYLLA_E_INDEX_OVERFLOW;
+  polylla_ctx* p = static_cast<polylla_ctx*>(std::calloc(1, sizeof(polylla_ctx)));
+  if (!p) return POLYLLA_E_INVALID_ARGUMENT;
+  Ctx* c = &p->c;
+  c->xy = xy;
+  c->tri = tri;
+  c->V = V;
+  c->T = T;
+  if (!carve(c, workspace, workspace_bytes_)) {
+    std::free(p);
+    return POLYLLA_E_WORKSPACE;
+  }
+  const int n = launch_build(c, S(stream));
+  if (n < 0) {
+    std::free(p);
+    return POLYLLA_E_CUDA;
+  }
+  c->launches += n;
+  c->stage = 1;
+  *ctx_out = p;
+  return POLYLLA_OK;
+}
+
+POLYLLA_API polylla_status polylla_label(polylla_ctx* p, polylla_stream stream) {
+  if (!p) return POLYLLA_E_INVALID_ARGUMENT;
+  if (p->c.stage != 1) return POLYLLA_E_CALL_ORDER;
+  const int n = launch_label(&p->c, S(stream));
+  if (n < 0) return POLYLLA_E_CUDA;
+  p->c.launches += n;
+  p->c.stage = 2;
+  return POLYLLA_OK;
+}
+
+POLYLLA_API polylla_status polylla_generate(polylla_ctx* p, polylla_stream stream) {
+  if (!p) return POLYLLA_E_INVALID_ARGUMENT;
+  if (p->c.stage != 2) return POLYLLA_E_CALL_ORDER;
+  const int n = launch_generate(&p->c, S(stream));
+  if (n < 0) return POLYLLA_E_CUDA;
+  p->c.launches += n;
+  p->c.stage = 3;
+  return POLYLLA_OK;
+}
+
+POLYLLA_API polylla_status polylla_get_counts(polylla_ctx* p, polylla_stream stream, polylla_counts* out) {
+  if (!p || !out) return POLYLLA_E_INVALID_ARGUMENT;
+  Ctx* c = &p->c;
+  if (c->stage < 1) return POLYLLA_E_CALL_ORDER;
+  DevCounters h{};
+  if (cudaMemcpyAsync(&h, c->ctr, sizeof(h), cudaMemcpyDeviceToHost, S(stream)) != cudaSuccess ||
+      cudaStreamSynchronize(S(stream)) != cudaSuccess)
+    return POLYLLA_E_CUDA;
+  polylla_counts r{};
+  r.n_vertices = c->V;
+  r.n_triangles = c->T;
+  r.n_border = h.n_border;
+  r.n_halfedges = 3 * c->T + h.n_border;
+  r.n_polygons = c->stage >= 3 ? h.P : 0;
+  r.n_loop_entries = c->stage >= 3 ? h.L : 0;
+  r.n_tips = h.n_tips;
+  r.n_flips = h.n_flips;
+  r.n_leftover = h.n_left;
+  r.status = (int32_t)map_status(h.status);
+  c->host_counts = r;
+  if (c->stage == 3) c->stage = 4;
+  *out = r;
+  return (polylla_status)r.status;
+}
+
+POLYLLA_API polylla_status polylla_get_polygons(polylla_ctx* p, int32_t* offsets, int64_t offsets_cap, int32_t* loops,
+                                                int64_t loops_cap, int32_t* origin, int32_t* twin, int32_t* next,
+                                                int32_t* prev, polylla_stream stream) {
+  if (!p) return POLYLLA_E_INVALID_ARGUMENT;
+  Ctx* c = &p->c;
+  if (c->stage < 3) return POLYLLA_E_CALL_ORDER;
+  if ((origin || twin || next) && c->stage < 4) return POLYLLA_E_CALL_ORDER;  // H needs get_counts
+  if (offsets && loops) {
+    const int n = launch_extract(c, offsets, offsets_cap, loops, loops_cap, prev, S(stream));
+    if (n < 0) return POLYLLA_E_CUDA;
+    c->launches += n;
+  } else if (offsets || loops) {
+    return POLYLLA_E_INVALID_ARGUMENT;
+  } else if (prev) {
+    const int n = launch_extract(c, nullptr, -1, nullptr, -1, prev, S(stream));
+    if (n < 0) return POLYLLA_E_CUDA;
+    c->launches += n;
+  }
+  const size_t hb = (size_t)c->host_counts.n_halfedges * 4;
+  if (origin && cudaMemcpyAsync(origin, c->origin, hb, cudaMemcpyDefault, S(stream)) != cudaSuccess)
+    return POLYLLA_E_CUDA;
+  if (twin && cudaMemcpyAsync(twin, c->twin, hb, cudaMemcpyDefault, S(stream)) != cudaSuccess)
+    return POLYLLA_E_CUDA;
+  if (next && cudaMemcpyAsync(next, c->next, hb, cudaMemcpyDefault, S(stream)) != cudaSuccess)
+    return POLYLLA_E_CUDA;
+  return POLYLLA_OK;
+}
+
+POLYLLA_API polylla_status polylla_get_views(polylla_ctx* p, polylla_views* v) {
+  if (!p || !v) return POLYLLA_E_INVALID_ARGUMENT;
+  if (p->c.stage < 1) return POLYLLA_E_CALL_ORDER;
+  const Ctx* c = &p->c;
+  v->origin = c->origin;
+  v->twin = c->twin;
+  v->next = c->next;
+  v->lcode = c->lcode;
+  v->frontier0 = c->F0;
+  v->frontier1 = c->F1;
+  v->seed_bits = c->S;
+  v->seeds = c->seeds;
+  v->tips = c->tips;
+  return POLYLLA_OK;
+}
+
+POLYLLA_API polylla_status polylla_set_debug(polylla_ctx* p, int32_t* next_pre) {
+  if (!p) return POLYLLA_E_INVALID_ARGUMENT;
+  p->c.next_pre = next_pre;
+  return POLYLLA_OK;
+}
+
+POLYLLA_API polylla_status polylla_run_host(const double* xy_host, int64_t V, const int32_t* tri_host, int64_t T,
+                                            void* workspace, size_t workspace_bytes_, int32_t* offsets_host,
+                                            int64_t offsets_cap, int32_t* loops_host, int64_t loops_cap,
+                                            int32_t* origin_host, int32_t* twin_host, int32_t* next_host,
+                                            int64_t halfedge_cap, polylla_counts* counts, polylla_stream stream) {
+  if (!xy_host || !tri_host || !workspace || !offsets_host || !loops_host || !counts || V < 3 || T < 1)
+    return POLYLLA_E_INVALID_ARGUMENT;
+  if (3 * T > 0x7fffffffLL || V > 0x7fffffffLL) return POLYLLA_E_INDEX_OVERFLOW;
+  Ctx probe{};
+  probe.V = V;
+  probe.T = T;
+  if (!carve(&probe, workspace, workspace_bytes_)) return POLYLLA_E_WORKSPACE;
+  cudaStream_t s = S(stream);
+  if (cudaMemcpyAsync(probe.xy_stage, xy_host, (size_t)V * 16, cudaMemcpyHostToDevice, s) != cudaSuccess ||
+      cudaMemcpyAsync(probe.tri_stage, tri_host, (size_t)T * 12, cudaMemcpyHostToDevice, s) != cudaSuccess)
+    return POLYLLA_E_CUDA;
+  polylla_ctx* p = nullptr;
+  polylla_status st = polylla_build_halfedges(probe.xy_stage, V, probe.tri_stage, T, workspace, workspace_bytes_,
+                                              stream, &p);
+  if (st != POLYLLA_OK) return st;
+  if ((st = polylla_label(p, stream)) != POLYLLA_OK || (st = polylla_generate(p, stream)) != POLYLLA_OK) {
+    polylla_destroy(p);
+    return st;
+  }
+  st = polylla_get_counts(p, stream, counts);
+  if (st != POLYLLA_OK) {
+    polylla_destroy(p);
+    return st;
+  }
+  Ctx* c = &p->c;
+  const int64_t P = counts->n_polygons, L = counts->n_loop_entries, H = counts->n_halfedges;
+  if (offsets_cap < P + 1 || loops_cap < L || ((origin_host || twin_host || next_host) && halfedge_cap < H)) {
+    polylla_destroy(p);
+    return POLYLLA_E_CAPACITY;
+  }
+  // extraction into the workspace staging, then exact-size D2H copies
+  // (the offsets are already final in the workspace; only the loops are extracted)
+  polylla_status out = POLYLLA_OK;
+  if (launch_extract(c, nullptr, T + 1, c->loops, 3 * T, nullptr, s) < 0) out = POLYLLA_E_CUDA;
+  if (cudaMemcpyAsync(offsets_host, c->offsets, (size_t)(P + 1) * 4, cudaMemcpyDeviceToHost, s) != cudaSuccess ||
+      cudaMemcpyAsync(loops_host, c->loops, (size_t)L * 4, cudaMemcpyDeviceToHost, s) != cudaSuccess)
+    out = POLYLLA_E_CUDA;
+  if (origin_host && cudaMemcpyAsync(origin_host, c->origin, (size_t)H * 4, cudaMemcpyDeviceToHost, s) != cudaSuccess)
+    out = POLYLLA_E_CUDA;
+  if (twin_host && cudaMemcpyAsync(twin_host, c->twin, (size_t)H * 4, cudaMemcpyDeviceToHost, s) != cudaSuccess)
+    out = POLYLLA_E_CUDA;
+  if (next_host && cudaMemcpyAsync(next_host, c->next, (size_t)H * 4, cudaMemcpyDeviceToHost, s) != cudaSuccess)
+    out = POLYLLA_E_CUDA;
+  if (cudaStreamSynchronize(s) != cudaSuccess) out = POLYLLA_E_CUDA;
+  polylla_destroy(p);
+  return out;
+}
+
+POLYLLA_API void polylla_destroy(polylla_ctx* p) { std::free(p); }
+
+POLYLLA_API int64_t polylla_launch_count(const polylla_ctx* p) { return p ? p->c.launches : 0; }
+
+POLYLLA_API const char* polylla_status_string(polylla_status s) {
+  switch (s) {
+    case POLYLLA_OK: return "ok";
+    case POLYLLA_E_INVALID_ARGUMENT: return "invalid argument";
+    case POLYLLA_E_DANGLING_INDEX: return "dangling vertex index";
+    case POLYLLA_E_DEGENERATE_TRI: return "degenerate triangle";
+    case POLYLLA_E_NON_MANIFOLD_EDGE: return "non-manifold edge";
+    case POLYLLA_E_NON_MANIFOLD_VERTEX: return "non-manifold boundary vertex";
+    case POLYLLA_E_INDEX_OVERFLOW: return "half-edge index overflow";
+    case POLYLLA_E_WORKSPACE: return "workspace too small or misaligned";
+    case POLYLLA_E_WALK_BOUND: return "walk bound exceeded";
+    case POLYLLA_E_UNSEEDED_LOOP: return "frontier loop without a seed";
+    case POLYLLA_E_CALL_ORDER: return "call order";
+    case POLYLLA_E_CUDA: return "CUDA error";
+    case POLYLLA_E_CAPACITY: return "output capacity too small";
+  }
+  return "unknown";
+}
+
+}  // extern "C"

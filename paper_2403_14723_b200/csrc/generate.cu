@@ -1,0 +1,183 @@
+// generate.cu -- repair, seed landing, canonical seeds, compaction
+// ("Label extra seed and frontier edges" (Alg. 10), "Search frontier
+// edges for each seed edge" (Alg. 12), "Overwrite seeds", "Scan and compact").
+//
+//   k_repair_mid     one thread per barrier tip (found by the label pass as next == twin):
+//                    d = degree(v); m = sweep_out^k(e0), k = floor((d-1)/2) (R5) from the
+//                    tip's outgoing frontier half-edge e0; F1[m] = F1[twin m] = 1; both
+//                    halves become seeds (mids list).  Topology only -> snapshot (R6).
+//   k_repair_rewire  one thread per touched vertex w (the tip v and the far end u of m):
+//                    recompute next[p] for every incoming frontier half-edge p of w with
+//                    the F1 bits (the only next values repair can change).
+//   k_seed_walk      one thread per seed (S bits + mids): rotate to the first frontier
+//                    half-edge (Alg. 12), walk the polygon through next, keep the minimum
+//                    id as the canonical seed and its loop length (Overwrite seeds,
+//                    PAPER.md L816).  Duplicate walks of one polygon write the same values.
+//   canon scan       ascending canonical seeds -> seeds[P]; exclusive scan of lengths ->
+//                    offsets[P+1]; checks sum(len) == #interior F1 half-edges (R12).
+#include "internal.cuh"
+#include "scan.cuh"
+
+namespace polylla {
+
+__device__ __forceinline__ bool f1_of(const uint32_t* __restrict__ F1, int64_t T3, int32_t x) {
+  return x >= T3 || bit_of(F1, x);
+}
+
+__global__ void k_repair_mid(int64_t T, const int32_t* __restrict__ twin, uint32_t* F1, const int32_t* __restrict__ tips,
+                             int32_t* __restrict__ mids, int32_t* __restrict__ aff, DevCounters* ctr) {
+  if (ctr->status) return;
+  const int64_t T3 = 3 * T;
+  const int32_t n = ctr->n_tips;
+  for (int32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    const int32_t e = tips[i];
+    const int32_t e0 = twin[e];  // the tip's only outgoing frontier half-edge
+    int32_t x = e0, d = 0;
+    bool ok = true;
+    do {  // degree(v): rotation closure about v (an interior vertex)
+      const int32_t tx = twin[x];
+      if (tx >= T3 || ++d > kWalkBound) { ok = false; break; }
+      x = next_in(tx);
+    } while (x != e0);
+    if (!ok) { raise_status(ctr, ST_WALK); continue; }
+    int32_t m = e0;
+    for (int k = 0; k < (d - 1) / 2; ++k) m = next_in(twin[m]);  // CWvertexEdge steps (R1, R5)
+    const int32_t tm = twin[m];
+    atomicOr(&F1[m >> 5], 1u << (m & 31));
+    atomicOr(&F1[tm >> 5], 1u << (tm & 31));
+    mids[2 * i] = m;
+    mids[2 * i + 1] = tm;
+    aff[2 * i] = e0;     // outgoing from v
+    aff[2 * i + 1] = tm; // outgoing from u = target(m)
+  }
+}
+
+__global__ void k_repair_rewire(int64_t T, const int32_t* __restrict__ twin, const uint32_t* __restrict__ F1,
+                                const int32_t* __restrict__ aff, int32_t* next, DevCounters* ctr) {
+  if (ctr->status) return;
+  const int64_t T3 = 3 * T;
+  const int32_t n = 2 * ctr->n_tips;
+  for (int32_t j = blockIdx.x * blockDim.x + threadIdx.x; j < n; j += gridDim.x * blockDim.x) {
+    const int32_t o = aff[j];
+    int32_t y = o;
+    int guard = 0;
+    do {
+      if (y < T3) {
+        const int32_t p = prev_in(y);  // incoming to w in y's triangle; next_in(p) = y
+        if (f1_of(F1, T3, p)) {
+          int32_t x = y;
+          int steps = 0;
+          while (!f1_of(F1, T3, x) && ++steps < kWalkBound) x = next_in(twin[x]);
+          next[p] = x;
+        }
+      }
+      const int32_t ty = twin[y];
+      y = ty >= T3 ? next[ty] : next_in(ty);  // full rotation about w (border chain at the hull)
+      if (++guard > kWalkBound) { raise_status(ctr, ST_WALK); break; }
+    } while (y != o);
+  }
+}
+
+constexpr int kSeedThreads = 256;
+constexpr int kSeedWarps = kSeedThreads / 32;
+
+__device__ __forceinline__ void process_seed(int32_t s, int64_t T3, int64_t H, const int32_t* __restrict__ twin,
+                                             const int32_t* __restrict__ next, const uint32_t* __restrict__ F1,
+                                             uint32_t* C, int32_t* len, DevCounters* ctr) {
+  int32_t x = s;
+  int steps = 0;
+  while (!f1_of(F1, T3, x)) {  // Alg. 12: rotate (sweep_out) to a frontier half-edge
+    x = next_in(twin[x]);
+    if (++steps > kWalkBound || x == s) { raise_status(ctr, ST_WALK); return; }
+  }
+  int32_t mn = x, y = x;
+  int64_t n = 0;
+  do {  // Overwrite seeds: walk the polygon, keep the minimum index
+    mn = min(mn, y);
+    y = next[y];
+    if (++n > H) { raise_status(ctr, ST_WALK); return; }
+  } while (y != x);
+  atomicOr(&C[mn >> 5], 1u << (mn & 31));
+  len[mn] = (int32_t)n;
+}
+
+__global__ void __launch_bounds__(kSeedThreads)
+    k_seed_walk(int64_t T, int64_t n_words, const int32_t* __restrict__ twin, const int32_t* __restrict__ next,
+                const uint32_t* __restrict__ F1, const uint32_t* __restrict__ S, const int32_t* __restrict__ mids,
+                uint32_t* C, int32_t* len, DevCounters* ctr) {
+  __shared__ int32_t queue[kSeedWarps][32 * 32];
+  if (ctr->status) return;
+  const int64_t T3 = 3 * T;
+  const int64_t H = T3 + ctr->n_border;
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  int32_t* q = queue[wid];
+  const int64_t groups = (n_words + 31) / 32;
+  for (int64_t g = (int64_t)blockIdx.x * kSeedWarps + wid; g < groups; g += (int64_t)gridDim.x * kSeedWarps) {
+    const int64_t w = g * 32 + lane;
+    uint32_t bits = w < n_words ? S[w] : 0u;
+    const int cnt = __popc(bits);
+    int incl = cnt;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int v = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += v;
+    }
+    const int total = __shfl_sync(0xffffffffu, incl, 31);
+    int pos = incl - cnt;
+    while (bits) {
+      const int b = __ffs(bits) - 1;
+      bits &= bits - 1;
+      q[pos++] = (int32_t)(w * 32 + b);
+    }
+    __syncwarp();
+    for (int i = lane; i < total; i += 32) process_seed(q[i], T3, H, twin, next, F1, C, len, ctr);
+    __syncwarp();
+  }
+  // the repair's new seeds (both halves of every middle edge)
+  const int32_t nm = 2 * ctr->n_tips;
+  for (int32_t j = blockIdx.x * kSeedThreads + threadIdx.x; j < nm; j += gridDim.x * kSeedThreads)
+    process_seed(mids[j], T3, H, twin, next, F1, C, len, ctr);
+}
+
+struct CanonOp {
+  const uint32_t* C;
+  const uint32_t* F1;
+  const int32_t* len;
+  int32_t* seeds;
+  int32_t* offsets;
+  DevCounters* ctr;
+  __device__ bool skip() const { return ctr->status != 0; }
+  __device__ uint32_t word(int64_t w) const { return C[w]; }
+  __device__ long long aux(int32_t e) const { return len[e]; }
+  __device__ long long extra(int64_t w) const { return __popc(F1[w]); }
+  __device__ void finish(long long P, long long L, long long nf1) const {
+    ctr->P = (int32_t)P;
+    ctr->L = (int32_t)L;
+    ctr->n_f1 = (int32_t)nf1;
+    if (L != nf1) raise_status(ctr, ST_UNSEEDED);  // R12: a frontier loop without a seed
+    offsets[P] = (int32_t)L;
+  }
+  __device__ void emit(int32_t e, long long rank, long long pre) const {
+    seeds[rank] = e;
+    offsets[rank] = (int32_t)pre;
+  }
+};
+
+int launch_generate(Ctx* c, cudaStream_t s) {
+  int n = 0;
+  const int grid = 148 * 4;
+  if (c->next_pre) cudaMemcpyAsync(c->next_pre, c->next, (size_t)c->Hmax * 4, cudaMemcpyDeviceToDevice, s);
+  k_repair_mid<<<grid, 128, 0, s>>>(c->T, c->twin, c->F1, c->tips, c->mids, c->aff, c->ctr);
+  k_repair_rewire<<<grid, 128, 0, s>>>(c->T, c->twin, c->F1, c->aff, c->next, c->ctr);
+  cudaMemsetAsync(c->C, 0, (size_t)c->n_words * 4, s);
+  k_seed_walk<<<148 * 8, kSeedThreads, 0, s>>>(c->T, c->n_words, c->twin, c->next, c->F1, c->S, c->mids, c->C,
+                                               c->len, c->ctr);
+  n += 3;
+  CanonOp op{c->C, c->F1, c->len, c->seeds, c->offsets, c->ctr};
+  const int r = launch_scan(op, c->n_words, c->scan_a, c->scan_b, c->scan_c, s);
+  if (r < 0) return -1;
+  n += r;
+  return cudaGetLastError() == cudaSuccess ? n : -1;
+}
+
+}  // namespace polylla

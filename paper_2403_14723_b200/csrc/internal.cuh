@@ -1,0 +1,122 @@
+// internal.cuh -- shared declarations of the libpolylla.so kernels (CUDA, sm_100a).
+//
+// Data layout in HBM (all inside the caller's workspace, see carve() in capi.cu):
+//   origin/twin/next : int32 SoA [H_max], H_max = 6T (worst case B = 3T)
+//   lcode            : uint8 [T]   k* of each triangle (longest half-edge 3f+k*)
+//   F0, F1, S, C, Bd : uint32 bit-vectors over the interior half-edges [0, 3T)
+//                      (frontier before/after repair, seed, canonical seed, unmatched)
+//   len              : int32 [3T]  loop length, written only at canonical seeds
+//   leftover keys/ids, global edge hash, border-vertex hash, tips, mids, scan sums,
+//   seeds/offsets/loops staging, input staging (run_host).
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#include "polylla.h"
+
+namespace polylla {
+
+// ------------------------------------------------------------------ status bits
+enum : uint32_t {
+  ST_DANGLING = 1u << 0,
+  ST_DEGENERATE = 1u << 1,
+  ST_NONMANIFOLD_EDGE = 1u << 2,
+  ST_NONMANIFOLD_VERTEX = 1u << 3,
+  ST_WALK = 1u << 4,
+  ST_UNSEEDED = 1u << 5,
+  ST_CAPACITY = 1u << 6,
+  ST_OVERFLOW = 1u << 7,
+  ST_INTERNAL = 1u << 8,
+};
+
+// device-side counters (zeroed at the start of every build)
+struct DevCounters {
+  uint32_t status;
+  int32_t n_left;    // leftover half-edges (twin not in the build tile)
+  int32_t n_border;  // B
+  int32_t n_tips;
+  int32_t n_flips;
+  int32_t P;         // polygons
+  int32_t L;         // loop entries
+  int32_t n_f1;      // #interior F1 half-edges
+  uint32_t hash_cap; // capacity (pow2 <= 2^31) of the leftover hash for this run
+  int32_t pad[7];
+};
+
+struct Ctx {
+  // inputs
+  const double* xy;
+  const int32_t* tri;
+  int64_t V, T;
+  int64_t Hmax;  // 6T
+  // workspace views
+  int32_t *origin, *twin, *next;
+  uint8_t* lcode;
+  uint32_t *F0, *F1, *S, *C, *Bd;
+  int32_t* len;
+  unsigned long long* left_key;
+  int32_t* left_e;
+  uint32_t* ehash;  // leftover-edge hash slots [hash_cap_max] (capacity chosen on device)
+  uint32_t* vkey;   // border-vertex hash: key = vertex id [hash_cap_max]
+  int32_t* vval;    //                      val = border half-edge id
+  int64_t hash_cap_max;
+  int32_t* tips;    // [V]
+  int32_t* aff;     // [2V] affected (outgoing half-edge) per tip side
+  int32_t* mids;    // [2V]
+  long long* scan_a;  // per-block sums (count)
+  long long* scan_b;  // per-block sums (aux)
+  long long* scan_c;  // per-block sums (F1 popcount)
+  int32_t* seeds;     // [T]
+  int32_t* offsets;   // [T+1]
+  int32_t* loops;     // [3T]  (run_host staging)
+  double* xy_stage;   // [2V]  (run_host staging)
+  int32_t* tri_stage; // [3T]
+  DevCounters* ctr;
+  int32_t* next_pre;  // optional debug copy
+  // host state
+  int stage;          // 1 built, 2 labelled, 3 generated, 4 counted
+  int64_t launches;
+  polylla_counts host_counts;
+  int64_t n_words;    // ceil(3T/32)
+  int64_t scan_blocks;
+};
+
+// workspace
+size_t workspace_bytes(int64_t V, int64_t T);
+bool carve(Ctx* c, void* ws, size_t bytes);
+
+// launchers (each returns the number of kernel launches issued, < 0 on CUDA error)
+int launch_build(Ctx* c, cudaStream_t s);
+int launch_label(Ctx* c, cudaStream_t s);
+int launch_generate(Ctx* c, cudaStream_t s);
+int launch_extract(Ctx* c, int32_t* offsets, int64_t offsets_cap, int32_t* loops, int64_t loops_cap,
+                   int32_t* prev, cudaStream_t s);
+
+// ------------------------------------------------------------------ device helpers
+__device__ __forceinline__ int32_t next_in(int32_t e) {  // 3f + (k+1)%3
+  const int32_t k = e % 3;
+  return k == 2 ? e - 2 : e + 1;
+}
+__device__ __forceinline__ int32_t prev_in(int32_t e) {  // 3f + (k+2)%3
+  const int32_t k = e % 3;
+  return k == 0 ? e + 2 : e - 1;
+}
+__device__ __forceinline__ bool bit_of(const uint32_t* w, int32_t e) { return (w[e >> 5] >> (e & 31)) & 1u; }
+
+__device__ __forceinline__ void raise_status(DevCounters* c, uint32_t bits) { atomicOr(&c->status, bits); }
+
+__device__ __forceinline__ uint32_t mix32(uint32_t a, uint32_t b) {
+  uint32_t h = a * 0x9E3779B1u ^ (b + 0x7F4A7C15u + (a << 6) + (a >> 2));
+  h ^= h >> 16;
+  h *= 0x85EBCA6Bu;
+  h ^= h >> 13;
+  h *= 0xC2B2AE35u;
+  h ^= h >> 16;
+  return h;
+}
+
+constexpr uint32_t kEmpty = 0xFFFFFFFFu;   // empty hash slot
+constexpr uint32_t kPaired = 0x80000000u;  // flag in hash slots (slot values < 2^31 - 1)
+constexpr int kWalkBound = 1 << 16;      // rotation bound (vertex degree)
+
+}  // namespace polylla

@@ -1,0 +1,275 @@
+"""Thin Python binding of ``libpolylla.so`` (include/polylla.h), same names as the C ABI.
+
+Argument marshalling only: every step of the conversion runs in the CUDA kernels of
+the library.  PyTorch supplies device memory (the workspace and output tensors) and
+streams.  There is no CPU fallback: importing works anywhere, but every call loads the
+shared library and fails loudly if it is missing or no GPU is present.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libpolylla.so")
+
+STATUS = {
+    0: "OK", -1: "INVALID_ARGUMENT", -2: "DANGLING_INDEX", -3: "DEGENERATE_TRI",
+    -4: "NON_MANIFOLD_EDGE", -5: "NON_MANIFOLD_VERTEX", -6: "INDEX_OVERFLOW", -7: "WORKSPACE",
+    -8: "WALK_BOUND", -9: "UNSEEDED_LOOP", -10: "CALL_ORDER", -11: "CUDA", -12: "CAPACITY",
+}
+
+# every symbol include/polylla.h declares (checked by tests/test_abi.py)
+EXPORTS = (
+    "polylla_workspace_bytes", "polylla_build_halfedges", "polylla_label", "polylla_generate",
+    "polylla_get_counts", "polylla_get_polygons", "polylla_get_views", "polylla_set_debug",
+    "polylla_run_host", "polylla_destroy", "polylla_status_string", "polylla_launch_count",
+)
+
+
+class PolyllaError(RuntimeError):
+    def __init__(self, code: int, where: str = ""):
+        super().__init__(f"{where}: polylla status {code} ({STATUS.get(code, '?')})")
+        self.code = code
+
+
+class Counts(ctypes.Structure):
+    _fields_ = [(n, ctypes.c_int64) for n in (
+        "n_vertices", "n_triangles", "n_halfedges", "n_border", "n_polygons", "n_loop_entries",
+        "n_tips", "n_flips", "n_leftover")] + [("status", ctypes.c_int32), ("reserved", ctypes.c_int32)]
+
+    def as_dict(self):
+        return {k: int(getattr(self, k)) for k, _ in self._fields_ if k != "reserved"}
+
+
+class Views(ctypes.Structure):
+    _fields_ = [(n, ctypes.c_void_p) for n in (
+        "origin", "twin", "next", "lcode", "frontier0", "frontier1", "seed_bits", "seeds", "tips")]
+
+
+_LIB = None
+
+
+def lib():
+    global _LIB
+    if _LIB is None:
+        if not os.path.exists(LIB_PATH):
+            raise RuntimeError(f"{LIB_PATH} is missing: build it with __graft_entry__.build()")
+        L = ctypes.CDLL(LIB_PATH)
+        vp, i64, i32p = ctypes.c_void_p, ctypes.c_int64, ctypes.c_void_p
+        L.polylla_workspace_bytes.restype = ctypes.c_size_t
+        L.polylla_workspace_bytes.argtypes = [i64, i64]
+        L.polylla_build_halfedges.restype = ctypes.c_int
+        L.polylla_build_halfedges.argtypes = [vp, i64, vp, i64, vp, ctypes.c_size_t, vp, ctypes.POINTER(vp)]
+        for n in ("polylla_label", "polylla_generate"):
+            getattr(L, n).restype = ctypes.c_int
+            getattr(L, n).argtypes = [vp, vp]
+        L.polylla_get_counts.restype = ctypes.c_int
+        L.polylla_get_counts.argtypes = [vp, vp, ctypes.POINTER(Counts)]
+        L.polylla_get_polygons.restype = ctypes.c_int
+        L.polylla_get_polygons.argtypes = [vp, i32p, i64, i32p, i64, i32p, i32p, i32p, i32p, vp]
+        L.polylla_get_views.restype = ctypes.c_int
+        L.polylla_get_views.argtypes = [vp, ctypes.POINTER(Views)]
+        L.polylla_set_debug.restype = ctypes.c_int
+        L.polylla_set_debug.argtypes = [vp, vp]
+        L.polylla_run_host.restype = ctypes.c_int
+        L.polylla_run_host.argtypes = [vp, i64, vp, i64, vp, ctypes.c_size_t, vp, i64, vp, i64, vp, vp, vp, i64,
+                                       ctypes.POINTER(Counts), vp]
+        L.polylla_destroy.restype = None
+        L.polylla_destroy.argtypes = [vp]
+        L.polylla_status_string.restype = ctypes.c_char_p
+        L.polylla_status_string.argtypes = [ctypes.c_int]
+        L.polylla_launch_count.restype = ctypes.c_int64
+        L.polylla_launch_count.argtypes = [vp]
+        _LIB = L
+    return _LIB
+
+
+def _stream(stream):
+    if stream is None:
+        return ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
+    if isinstance(stream, torch.cuda.Stream):
+        return ctypes.c_void_p(stream.cuda_stream)
+    return ctypes.c_void_p(int(stream))
+
+
+def _ptr(t):
+    return None if t is None else ctypes.c_void_p(t.data_ptr())
+
+
+def _check(rc, where):
+    if rc != 0:
+        raise PolyllaError(rc, where)
+
+
+@dataclass
+class Context:
+    """A polylla_ctx plus the torch tensors it views (kept alive here)."""
+    handle: ctypes.c_void_p
+    xy: torch.Tensor
+    tri: torch.Tensor
+    workspace: torch.Tensor
+
+    def __del__(self):
+        destroy(self)
+
+
+def workspace_bytes(n_vertices: int, n_triangles: int) -> int:
+    return int(lib().polylla_workspace_bytes(n_vertices, n_triangles))
+
+
+def alloc_workspace(n_vertices: int, n_triangles: int, device="cuda") -> torch.Tensor:
+    return torch.empty(workspace_bytes(n_vertices, n_triangles), dtype=torch.uint8, device=device)
+
+
+def build_halfedges(xy: torch.Tensor, tri: torch.Tensor, workspace: torch.Tensor, stream=None) -> Context:
+    if not (xy.is_cuda and tri.is_cuda and workspace.is_cuda):
+        raise ValueError("xy, tri and workspace must be CUDA tensors")
+    if xy.dtype != torch.float64 or tri.dtype != torch.int32 or not xy.is_contiguous() or not tri.is_contiguous():
+        raise ValueError("xy must be contiguous float64 [V,2], tri contiguous int32 [T,3]")
+    h = ctypes.c_void_p()
+    rc = lib().polylla_build_halfedges(_ptr(xy), xy.shape[0], _ptr(tri), tri.shape[0], _ptr(workspace),
+                                       workspace.numel(), _stream(stream), ctypes.byref(h))
+    _check(rc, "polylla_build_halfedges")
+    return Context(h, xy, tri, workspace)
+
+
+def label(ctx: Context, stream=None) -> None:
+    _check(lib().polylla_label(ctx.handle, _stream(stream)), "polylla_label")
+
+
+def generate(ctx: Context, stream=None) -> None:
+    _check(lib().polylla_generate(ctx.handle, _stream(stream)), "polylla_generate")
+
+
+def get_counts(ctx: Context, stream=None, check=True) -> dict:
+    c = Counts()
+    rc = lib().polylla_get_counts(ctx.handle, _stream(stream), ctypes.byref(c))
+    if check:
+        _check(rc, "polylla_get_counts")
+    return c.as_dict()
+
+
+def get_polygons(ctx: Context, offsets, loops, origin=None, twin=None, next=None, prev=None, stream=None):
+    rc = lib().polylla_get_polygons(
+        ctx.handle, _ptr(offsets), -1 if offsets is None else offsets.numel(), _ptr(loops),
+        -1 if loops is None else loops.numel(), _ptr(origin), _ptr(twin), _ptr(next), _ptr(prev), _stream(stream))
+    _check(rc, "polylla_get_polygons")
+
+
+def set_debug(ctx: Context, next_pre: torch.Tensor | None) -> None:
+    _check(lib().polylla_set_debug(ctx.handle, _ptr(next_pre)), "polylla_set_debug")
+
+
+def get_views(ctx: Context) -> dict:
+    """Raw device pointers into the workspace, returned as torch tensor slices of it."""
+    v = Views()
+    _check(lib().polylla_get_views(ctx.handle, ctypes.byref(v)), "polylla_get_views")
+    base = ctx.workspace.data_ptr()
+    return {k: int(getattr(v, k)) - base for k, _ in Views._fields_}
+
+
+def view_tensor(ctx: Context, offset: int, n: int, dtype) -> torch.Tensor:
+    esz = torch.empty((), dtype=dtype).element_size()
+    return ctx.workspace[offset:offset + n * esz].view(dtype)
+
+
+def launch_count(ctx: Context) -> int:
+    return int(lib().polylla_launch_count(ctx.handle))
+
+
+def destroy(ctx: Context) -> None:
+    if ctx.handle is not None and ctx.handle.value:
+        lib().polylla_destroy(ctx.handle)
+        ctx.handle = ctypes.c_void_p()
+
+
+def status_string(code: int) -> str:
+    return lib().polylla_status_string(code).decode()
+
+
+# ----------------------------------------------------------------------- conveniences
+
+def run(xy: torch.Tensor, tri: torch.Tensor, stream=None, arrays=True, prev=False, debug=False) -> dict:
+    """build -> label -> generate -> get_counts -> get_polygons on device tensors.
+    Returns a dict of torch tensors (offsets, loops, seeds, [origin, twin, next, prev],
+    [lcode, frontier0, frontier1, seed_bits, next_pre]) plus the counts."""
+    V, T = xy.shape[0], tri.shape[0]
+    ws = alloc_workspace(V, T, xy.device)
+    ctx = build_halfedges(xy, tri, ws, stream)
+    next_pre = None
+    if debug:
+        next_pre = torch.empty(6 * T, dtype=torch.int32, device=xy.device)
+        set_debug(ctx, next_pre)
+    label(ctx, stream)
+    generate(ctx, stream)
+    counts = get_counts(ctx, stream)
+    P, L, H = counts["n_polygons"], counts["n_loop_entries"], counts["n_halfedges"]
+    dev = xy.device
+    out = dict(counts)
+    out.update(P=P, L=L, H=H)
+    out["offsets"] = torch.empty(P + 1, dtype=torch.int32, device=dev)
+    out["loops"] = torch.empty(max(L, 1), dtype=torch.int32, device=dev)
+    kw = {}
+    if arrays:
+        for k in ("origin", "twin", "next"):
+            out[k] = kw[k] = torch.empty(H, dtype=torch.int32, device=dev)
+    if prev:
+        out["prev"] = kw["prev"] = torch.empty(H, dtype=torch.int32, device=dev)
+    get_polygons(ctx, out["offsets"], out["loops"], stream=stream, **kw)
+    c2 = get_counts(ctx, stream)  # synchronises; surfaces a capacity error
+    out["loops"] = out["loops"][:L]
+    v = get_views(ctx)
+    nw = (3 * T + 31) // 32
+    out["seeds"] = view_tensor(ctx, v["seeds"], P, torch.int32).clone()
+    if debug:
+        out["lcode"] = view_tensor(ctx, v["lcode"], T, torch.uint8).clone()
+        for k in ("frontier0", "frontier1", "seed_bits"):
+            out[k] = view_tensor(ctx, v[k], nw, torch.int32).clone()
+        out["tips"] = view_tensor(ctx, v["tips"], counts["n_tips"], torch.int32).clone()
+        out["next_pre"] = next_pre[:H].clone()
+    out["launches"] = launch_count(ctx)
+    assert c2["status"] == 0
+    destroy(ctx)
+    return out
+
+
+def run_host(xy: np.ndarray, tri: np.ndarray, workspace: torch.Tensor | None = None, arrays=True, stream=None,
+             pinned: dict | None = None) -> dict:
+    """End to end from host numpy arrays through polylla_run_host (H2D, kernels, D2H)."""
+    xy = np.ascontiguousarray(xy, dtype=np.float64)
+    tri = np.ascontiguousarray(tri, dtype=np.int32)
+    V, T = xy.shape[0], tri.shape[0]
+    if workspace is None:
+        workspace = alloc_workspace(V, T)
+    if pinned is None:
+        pinned = alloc_host_outputs(T, arrays)
+    c = Counts()
+    a = {k: (None if pinned.get(k) is None else ctypes.c_void_p(pinned[k].data_ptr()))
+         for k in ("offsets", "loops", "origin", "twin", "next")}
+    rc = lib().polylla_run_host(
+        ctypes.c_void_p(xy.ctypes.data), V, ctypes.c_void_p(tri.ctypes.data), T, _ptr(workspace),
+        workspace.numel(), a["offsets"], pinned["offsets"].numel(), a["loops"], pinned["loops"].numel(),
+        a["origin"], a["twin"], a["next"], 6 * T, ctypes.byref(c), _stream(stream))
+    _check(rc, "polylla_run_host")
+    d = c.as_dict()
+    P, L, H = d["n_polygons"], d["n_loop_entries"], d["n_halfedges"]
+    out = dict(d)
+    out.update(P=P, L=L, H=H, offsets=pinned["offsets"][:P + 1], loops=pinned["loops"][:L])
+    if arrays:
+        for k in ("origin", "twin", "next"):
+            out[k] = pinned[k][:H]
+    return out
+
+
+def alloc_host_outputs(T: int, arrays=True, pin=True) -> dict:
+    mk = (lambda n: torch.empty(n, dtype=torch.int32, pin_memory=pin))
+    d = dict(offsets=mk(T + 1), loops=mk(3 * T))
+    if arrays:
+        for k in ("origin", "twin", "next"):
+            d[k] = mk(6 * T)
+    return d
