@@ -178,6 +178,16 @@ POLYLLA_API polylla_status polylla_run_host(const double* xy_host, int64_t n_ver
                                             polylla_stream stream);
 
 POLYLLA_API void polylla_destroy(polylla_ctx* ctx);
+
+/* Optional per-kernel timing (process-wide, host-only state): when enabled, CUDA
+ * events are recorded on the launching stream around each kernel group
+ * (k_build_tile, k_left_match, k_border_scan, k_border_next, k_label_rewire,
+ * k_repair, k_seed_walk, k_canon_scan, k_extract).  polylla_profile_read
+ * synchronises on the recorded events, writes up to `cap` (name, total ms, launch
+ * count) triples accumulated since the last read/enable, clears them and returns
+ * the number written (< 0 on a CUDA error).  Names are valid until the next read. */
+POLYLLA_API void polylla_profile_enable(int on);
+POLYLLA_API int polylla_profile_read(const char** names, double* total_ms, int64_t* count, int cap);
 POLYLLA_API const char* polylla_status_string(polylla_status s);
 
 /* Number of kernel launches issued by the calls since the ctx was built (for the

@@ -283,21 +283,26 @@ int launch_build(Ctx* c, cudaStream_t s) {
     cudaFuncSetAttribute(k_build_tile, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kBuildSmem);
     attr = true;
   }
+  prof_mark(s, "k_build_tile");
   k_build_tile<<<(unsigned)tiles, kBuildThreads, kBuildSmem, s>>>(reinterpret_cast<const double2*>(c->xy), c->tri, c->V,
                                                           c->T, c->origin, c->twin, c->lcode, c->left_key,
                                                           c->left_e, c->ctr);
   ++n;
   const int grid = 148 * 8;
+  prof_mark(s, "k_left_match");
   k_hash_clear<<<grid, 256, 0, s>>>(c->ctr, c->ehash, c->vkey, c->hash_cap_max);
   k_left_insert<<<grid, 256, 0, s>>>(c->ctr, c->left_key, c->left_e, c->origin, c->twin, c->ehash);
   k_left_unmatched<<<grid, 256, 0, s>>>(c->ctr, c->left_e, c->twin, c->Bd);
   n += 3;
+  prof_mark(s, "k_border_scan");
   BorderOp op{c->Bd, c->origin, c->twin, c->vkey, c->vval, c->ctr, 3 * c->T};
   const int r = launch_scan(op, c->n_words, c->scan_a, c->scan_b, c->scan_c, s);
   if (r < 0) return -1;
   n += r;
+  prof_mark(s, "k_border_next");
   k_border_next<<<grid, 256, 0, s>>>(c->ctr, 3 * c->T, c->origin, c->twin, c->vkey, c->vval, c->next);
   ++n;
+  prof_end(s);
   return cudaGetLastError() == cudaSuccess ? n : -1;
 }
 

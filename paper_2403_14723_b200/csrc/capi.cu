@@ -4,6 +4,9 @@
 // extract.cu.
 #include <cstdlib>
 #include <cstring>
+#include <map>
+#include <string>
+#include <vector>
 
 #include "internal.cuh"
 
@@ -117,6 +120,44 @@ static polylla_status map_status(uint32_t st) {
   if (st & ST_UNSEEDED) return POLYLLA_E_UNSEEDED_LOOP;
   if (st & ST_CAPACITY) return POLYLLA_E_CAPACITY;
   return POLYLLA_E_WORKSPACE;
+}
+
+// ------------------------------------------------------------------ profiling
+struct ProfEntry {
+  const char* name;
+  cudaEvent_t a, b;
+};
+static bool g_prof = false;
+static std::vector<cudaEvent_t> g_pool;
+static size_t g_pool_used = 0;
+static std::vector<ProfEntry> g_entries;
+static const char* g_open = nullptr;
+static cudaEvent_t g_open_ev;
+
+static cudaEvent_t prof_event() {
+  if (g_pool_used == g_pool.size()) {
+    cudaEvent_t e;
+    cudaEventCreate(&e);
+    g_pool.push_back(e);
+  }
+  return g_pool[g_pool_used++];
+}
+
+void prof_mark(cudaStream_t s, const char* name) {
+  if (!g_prof) return;
+  cudaEvent_t e = prof_event();
+  cudaEventRecord(e, s);
+  if (g_open) g_entries.push_back({g_open, g_open_ev, e});
+  g_open = name;
+  g_open_ev = e;
+}
+
+void prof_end(cudaStream_t s) {
+  if (!g_prof || !g_open) return;
+  cudaEvent_t e = prof_event();
+  cudaEventRecord(e, s);
+  g_entries.push_back({g_open, g_open_ev, e});
+  g_open = nullptr;
 }
 
 }  // namespace polylla
@@ -316,6 +357,45 @@ POLYLLA_API polylla_status polylla_run_host(const double* xy_host, int64_t V, co
 }
 
 POLYLLA_API void polylla_destroy(polylla_ctx* p) { std::free(p); }
+
+POLYLLA_API void polylla_profile_enable(int on) {
+  g_prof = on != 0;
+  g_entries.clear();
+  g_pool_used = 0;
+  g_open = nullptr;
+}
+
+POLYLLA_API int polylla_profile_read(const char** names, double* total_ms, int64_t* count, int cap) {
+  std::map<std::string, std::pair<double, int64_t>> acc;
+  std::vector<std::string> order;
+  for (const ProfEntry& e : g_entries) {
+    if (cudaEventSynchronize(e.b) != cudaSuccess) return -1;
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, e.a, e.b);
+    auto it = acc.find(e.name);
+    if (it == acc.end()) {
+      order.push_back(e.name);
+      acc[e.name] = {ms, 1};
+    } else {
+      it->second.first += ms;
+      it->second.second += 1;
+    }
+  }
+  int n = 0;
+  static std::vector<std::string> keep;  // stable storage for the returned names
+  keep = order;
+  for (const std::string& k : keep) {
+    if (n >= cap) break;
+    names[n] = k.c_str();
+    total_ms[n] = acc[k].first;
+    count[n] = acc[k].second;
+    ++n;
+  }
+  g_entries.clear();
+  g_pool_used = 0;
+  g_open = nullptr;
+  return n;
+}
 
 POLYLLA_API int64_t polylla_launch_count(const polylla_ctx* p) { return p ? p->c.launches : 0; }
 

@@ -46,12 +46,14 @@ __global__ void k_prev(int64_t T, const int32_t* __restrict__ next, const uint32
 int launch_extract(Ctx* c, int32_t* offsets, int64_t offsets_cap, int32_t* loops, int64_t loops_cap,
                    int32_t* prev, cudaStream_t s) {
   int n = 0;
+  prof_mark(s, "k_extract");
   if (loops) k_extract<<<148 * 8, 256, 0, s>>>(c->seeds, c->offsets, c->origin, c->next, offsets, offsets_cap, loops, loops_cap,
                                     c->ctr), ++n;
   if (prev) {
     k_prev<<<148 * 16, 256, 0, s>>>(c->T, c->next, c->F1, prev, c->ctr);
     ++n;
   }
+  prof_end(s);
   return cudaGetLastError() == cudaSuccess ? n : -1;
 }
 

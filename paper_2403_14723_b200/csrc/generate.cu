@@ -167,16 +167,20 @@ int launch_generate(Ctx* c, cudaStream_t s) {
   int n = 0;
   const int grid = 148 * 4;
   if (c->next_pre) cudaMemcpyAsync(c->next_pre, c->next, (size_t)c->Hmax * 4, cudaMemcpyDeviceToDevice, s);
+  prof_mark(s, "k_repair");
   k_repair_mid<<<grid, 128, 0, s>>>(c->T, c->twin, c->F1, c->tips, c->mids, c->aff, c->ctr);
   k_repair_rewire<<<grid, 128, 0, s>>>(c->T, c->twin, c->F1, c->aff, c->next, c->ctr);
+  prof_mark(s, "k_seed_walk");
   cudaMemsetAsync(c->C, 0, (size_t)c->n_words * 4, s);
   k_seed_walk<<<148 * 8, kSeedThreads, 0, s>>>(c->T, c->n_words, c->twin, c->next, c->F1, c->S, c->mids, c->C,
                                                c->len, c->ctr);
   n += 3;
+  prof_mark(s, "k_canon_scan");
   CanonOp op{c->C, c->F1, c->len, c->seeds, c->offsets, c->ctr};
   const int r = launch_scan(op, c->n_words, c->scan_a, c->scan_b, c->scan_c, s);
   if (r < 0) return -1;
   n += r;
+  prof_end(s);
   return cudaGetLastError() == cudaSuccess ? n : -1;
 }
 

@@ -81,6 +81,10 @@ struct Ctx {
   int64_t scan_blocks;
 };
 
+// optional per-kernel timing (polylla_profile_*): events recorded around launches
+void prof_mark(cudaStream_t s, const char* name);  // start of kernel `name` (ends at the next mark)
+void prof_end(cudaStream_t s);
+
 // workspace
 size_t workspace_bytes(int64_t V, int64_t T);
 bool carve(Ctx* c, void* ws, size_t bytes);

@@ -77,8 +77,10 @@ __global__ void __launch_bounds__(kLabelThreads)
 
 int launch_label(Ctx* c, cudaStream_t s) {
   const int64_t blocks = (3 * c->T + kLabelThreads - 1) / kLabelThreads;
+  prof_mark(s, "k_label_rewire");
   k_label_rewire<<<(unsigned)blocks, kLabelThreads, 0, s>>>(c->T, c->twin, c->lcode, c->next, c->F0, c->F1, c->S,
                                                            c->tips, c->ctr);
+  prof_end(s);
   return cudaGetLastError() == cudaSuccess ? 1 : -1;
 }
 

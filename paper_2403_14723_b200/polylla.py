@@ -28,6 +28,7 @@ EXPORTS = (
     "polylla_workspace_bytes", "polylla_build_halfedges", "polylla_label", "polylla_generate",
     "polylla_get_counts", "polylla_get_polygons", "polylla_get_views", "polylla_set_debug",
     "polylla_run_host", "polylla_destroy", "polylla_status_string", "polylla_launch_count",
+    "polylla_profile_enable", "polylla_profile_read",
 )
 
 
@@ -85,6 +86,11 @@ def lib():
         L.polylla_status_string.argtypes = [ctypes.c_int]
         L.polylla_launch_count.restype = ctypes.c_int64
         L.polylla_launch_count.argtypes = [vp]
+        L.polylla_profile_enable.restype = None
+        L.polylla_profile_enable.argtypes = [ctypes.c_int]
+        L.polylla_profile_read.restype = ctypes.c_int
+        L.polylla_profile_read.argtypes = [ctypes.POINTER(ctypes.c_char_p), ctypes.POINTER(ctypes.c_double),
+                                           ctypes.POINTER(ctypes.c_int64), ctypes.c_int]
         _LIB = L
     return _LIB
 
@@ -186,6 +192,22 @@ def destroy(ctx: Context) -> None:
     if ctx.handle is not None and ctx.handle.value:
         lib().polylla_destroy(ctx.handle)
         ctx.handle = ctypes.c_void_p()
+
+
+def profile_enable(on: bool = True) -> None:
+    lib().polylla_profile_enable(1 if on else 0)
+
+
+def profile_read() -> dict:
+    """{kernel group: (total ms, launches)} since the last read (synchronises)."""
+    cap = 64
+    names = (ctypes.c_char_p * cap)()
+    ms = (ctypes.c_double * cap)()
+    cnt = (ctypes.c_int64 * cap)()
+    n = lib().polylla_profile_read(names, ms, cnt, cap)
+    if n < 0:
+        raise PolyllaError(-11, "polylla_profile_read")
+    return {names[i].decode(): (ms[i], int(cnt[i])) for i in range(n)}
 
 
 def status_string(code: int) -> str:
