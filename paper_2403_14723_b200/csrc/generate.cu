@@ -165,11 +165,10 @@ struct CanonOp {
 
 int launch_generate(Ctx* c, cudaStream_t s) {
   int n = 0;
-  const int grid = 148 * 4;
   if (c->next_pre) cudaMemcpyAsync(c->next_pre, c->next, (size_t)c->Hmax * 4, cudaMemcpyDeviceToDevice, s);
   prof_mark(s, "k_repair");
-  k_repair_mid<<<grid, 128, 0, s>>>(c->T, c->twin, c->F1, c->tips, c->mids, c->aff, c->ctr);
-  k_repair_rewire<<<grid, 128, 0, s>>>(c->T, c->twin, c->F1, c->aff, c->next, c->ctr);
+  k_repair_mid<<<148 * 16, 128, 0, s>>>(c->T, c->twin, c->F1, c->tips, c->mids, c->aff, c->ctr);
+  k_repair_rewire<<<148 * 32, 128, 0, s>>>(c->T, c->twin, c->F1, c->aff, c->next, c->ctr);
   prof_mark(s, "k_seed_walk");
   cudaMemsetAsync(c->C, 0, (size_t)c->n_words * 4, s);
   k_seed_walk<<<148 * 8, kSeedThreads, 0, s>>>(c->T, c->n_words, c->twin, c->next, c->F1, c->S, c->mids, c->C,

@@ -40,7 +40,8 @@ struct DevCounters {
   int32_t L;         // loop entries
   int32_t n_f1;      // #interior F1 half-edges
   uint32_t hash_cap; // capacity (pow2 <= 2^31) of the leftover hash for this run
-  int32_t pad[7];
+  int32_t n_def;     // half-edges deferred by k_tile to the label fixup
+  int32_t pad[6];
 };
 
 struct Ctx {
@@ -56,6 +57,7 @@ struct Ctx {
   int32_t* len;
   unsigned long long* left_key;
   int32_t* left_e;
+  int32_t* def_e;   // [3T] half-edges deferred by k_tile
   uint32_t* ehash;  // leftover-edge hash slots [hash_cap_max] (capacity chosen on device)
   uint32_t* vkey;   // border-vertex hash: key = vertex id [hash_cap_max]
   int32_t* vval;    //                      val = border half-edge id
