@@ -23,15 +23,47 @@
 namespace polylla {
 
 constexpr int kTileTris = 2048;
-constexpr int kTileHE = 3 * kTileTris;   // 6144 half-edges = 192 bit-vector words
-constexpr int kTileSlots = 8192;         // pow2 hash slots, >= 2.4x the unique keys of a tile
-constexpr int kTileThreads = 512;
-constexpr int kTileWalk = 64;            // longer in-tile rotations are deferred to the fixup
-// shared memory: tri_s int32[kTileHE] | tw_s int16[kTileHE] | slot uint16[kTileSlots] | lc_s u8[kTileTris]
-constexpr size_t kTileSmem = kTileHE * 4 + kTileHE * 2 + kTileSlots * 2 + kTileTris;  // 55,296 B -> 3-4 CTAs/SM
-constexpr uint16_t kEmpty16 = 0xFFFFu, kPaired16 = 0x8000u;
+constexpr int kTileHE = 3 * kTileTris;   // 6144 half-edges = 192 bit-vector words (e order)
+constexpr int kTileQ = 4 * kTileTris;    // quad slots q = 4t + k (slot 3 unused) -> 256 words
+constexpr int kTileSlots = 8192;         // pow2 hash slots (load ~0.38: only the lo->hi halves insert)
+constexpr int kTileThreads = 768;
+constexpr int kTileWords = kTileHE / 32; // 192
+// shared memory (bytes):
+//   tri_s int32[kTileHE] 24576
+//   tw_s  int16[kTileQ]  16384   twin as a quad index, -1 = outside the tile
+//   slot  u32[kTileSlots] 32768  (dead after P2: reused for succ u16[kTileQ] | Lm, Dm, Tm, SDm u32[192] | scan scratch)
+//   lc_s  u8[kTileTris]   2048
+//   nx_l  int16[kTileHE] 12288 | Sw, Cw u32[192] 1536 | slist int16[kTileTris] 4096   (P4-P6)
+constexpr size_t kOffTw = kTileHE * 4, kOffSlot = kOffTw + kTileQ * 2, kOffLc = kOffSlot + kTileSlots * 4,
+                 kOffNx = kOffLc + kTileTris, kTileSmem = kOffNx + kTileHE * 2 + kTileHE / 4 + kTileTris * 2;  // 93,696 B -> 2 CTAs/SM
+constexpr uint32_t kSlotQ = (1u << 13) - 1;       // slot = fingerprint(19 bits) << 13 | quad index
+// rotation successors (P3/P4): quad index in the low 13 bits, terminal flags above
+constexpr uint16_t kSuccIdx = 0x1FFF, kSuccFront = 0x4000, kSuccUnknown = 0x8000;
+constexpr int kTileJumps = 4;            // pointer-jumping rounds: chains up to 2^4 steps resolved in-tile
+
+#ifdef POLYLLA_PHASE_TIMING
+__device__ unsigned long long g_phase_cycles[16];
+// (__syncthreads_count's result is consumed before the clock is read: clock64() right
+// after a plain __syncthreads records the deferred barrier's issue time, not its release)
+#define PHASE_MARK(i)                                                       \
+  do {                                                                      \
+    const int c_ = __syncthreads_count(1); /* result depends on release */  \
+    if (threadIdx.x == 0 && c_ > 0) {                                       \
+      const long long now_ = clock64();                                     \
+      atomicAdd(&g_phase_cycles[i], (unsigned long long)(now_ - t_phase_)); \
+      t_phase_ = now_;                                                      \
+    }                                                                       \
+  } while (0)
+#else
+#define PHASE_MARK(i) do { } while (0)
+#endif
 
 __device__ __forceinline__ int32_t next_local(int32_t j) { return (j % 3 == 2) ? j - 2 : j + 1; }
+// quad encoding of a local half-edge: q = 4*(j/3) + j%3 (bit ops in the walks)
+__device__ __forceinline__ int32_t q_of(int32_t j) { const int32_t t = j / 3; return 4 * t + (j - 3 * t); }
+__device__ __forceinline__ int32_t j_of(int32_t q) { return 3 * (q >> 2) + (q & 3); }
+__device__ __forceinline__ int32_t next_q(int32_t q) { return (q & 3) == 2 ? q - 2 : q + 1; }
+__device__ __forceinline__ bool bit_s(const uint32_t* w, int32_t i) { return (w[i >> 5] >> (i & 31)) & 1u; }
 
 __device__ __forceinline__ double sq_len(double2 p, double2 q) {
   // |q - p|^2 = dx*dx + dy*dy, dx = x[target] - x[origin]; IEEE RN, no FMA (R11)
@@ -39,8 +71,7 @@ __device__ __forceinline__ double sq_len(double2 p, double2 q) {
   return __dadd_rn(__dmul_rn(dx, dx), __dmul_rn(dy, dy));
 }
 
-// L2 policies: keep the randomly gathered coordinates (vertex ids are spatially random)
-// resident, stream the triangle tile through.
+// L2 policy for the randomly gathered coordinates (vertex ids are spatially random)
 __device__ __forceinline__ uint64_t policy_evict_last() {
   uint64_t p;
   asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
@@ -52,32 +83,130 @@ __device__ __forceinline__ double2 ld_xy(const double2* ptr, uint64_t pol) {
   return r;
 }
 
+// block-wide exclusive scan of 4 counters (kTileThreads threads); returns the prefix
+__device__ __forceinline__ int4 block_scan4(int4 v, int4* tot, int* sm /* [4 * 32 + 4] */) {
+  constexpr int NW = kTileThreads / 32;
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  int4 inc = v;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int a = __shfl_up_sync(0xffffffffu, inc.x, o), b = __shfl_up_sync(0xffffffffu, inc.y, o),
+              c = __shfl_up_sync(0xffffffffu, inc.z, o), d = __shfl_up_sync(0xffffffffu, inc.w, o);
+    if (lane >= o) { inc.x += a; inc.y += b; inc.z += c; inc.w += d; }
+  }
+  if (lane == 31) { sm[wid] = inc.x; sm[32 + wid] = inc.y; sm[64 + wid] = inc.z; sm[96 + wid] = inc.w; }
+  __syncthreads();
+  if (wid == 0) {
+    int a = lane < NW ? sm[lane] : 0, b = lane < NW ? sm[32 + lane] : 0, c = lane < NW ? sm[64 + lane] : 0,
+        d = lane < NW ? sm[96 + lane] : 0;
+    int ia = a, ib = b, ic = c, id = d;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int x = __shfl_up_sync(0xffffffffu, ia, o), y = __shfl_up_sync(0xffffffffu, ib, o),
+                z = __shfl_up_sync(0xffffffffu, ic, o), w = __shfl_up_sync(0xffffffffu, id, o);
+      if (lane >= o) { ia += x; ib += y; ic += z; id += w; }
+    }
+    if (lane < NW) { sm[lane] = ia - a; sm[32 + lane] = ib - b; sm[64 + lane] = ic - c; sm[96 + lane] = id - d; }
+    if (lane == NW - 1) { sm[128] = ia; sm[129] = ib; sm[130] = ic; sm[131] = id; }
+  }
+  __syncthreads();
+  *tot = make_int4(sm[128], sm[129], sm[130], sm[131]);
+  const int4 r = make_int4(sm[wid] + inc.x - v.x, sm[32 + wid] + inc.y - v.y, sm[64 + wid] + inc.z - v.z,
+                           sm[96 + wid] + inc.w - v.w);
+  __syncthreads();  // sm is reused by the caller
+  return r;
+}
+
+// Tile hash on the undirected key (lo, hi), linear probing over uint32 slots holding
+// fingerprint(19 bits) << 13 | q.  The half-edges with origin < target insert their key,
+// those with origin > target look it up (read-only).
+__device__ __forceinline__ uint32_t tile_hash(uint32_t lo, uint32_t hi) { return mix32(lo, hi); }
+
+__device__ __forceinline__ uint32_t tile_insert(uint32_t* slot, const int32_t* tri_s, int32_t q, uint32_t lo,
+                                                uint32_t hi) {
+  const uint32_t h = tile_hash(lo, hi);
+  const uint32_t fp = h & ~kSlotQ;
+  const uint32_t mine = fp | (uint32_t)q;
+  uint32_t p = h & (kTileSlots - 1);
+  for (int probe = 0; probe < kTileSlots; ++probe, p = (p + 1) & (kTileSlots - 1)) {
+    uint32_t w = slot[p];
+    if (w == kEmpty) {
+      w = atomicCAS(&slot[p], kEmpty, mine);
+      if (w == kEmpty) return 0;
+    }
+    if ((w & ~kSlotQ) == fp) {  // same fingerprint: confirm the key
+      const int32_t sq = (int32_t)(w & kSlotQ);
+      if ((uint32_t)tri_s[j_of(sq)] == lo && (uint32_t)tri_s[j_of(next_q(sq))] == hi)
+        return ST_NONMANIFOLD_EDGE;  // the same directed edge twice
+    }
+  }
+  return ST_INTERNAL;
+}
+
+// the quad holding key (lo, hi) in direction lo -> hi, or -1
+__device__ __forceinline__ int32_t tile_lookup(const uint32_t* slot, const int32_t* tri_s, uint32_t lo, uint32_t hi) {
+  const uint32_t h = tile_hash(lo, hi);
+  const uint32_t fp = h & ~kSlotQ;
+  uint32_t p = h & (kTileSlots - 1);
+  for (int probe = 0; probe < kTileSlots; ++probe, p = (p + 1) & (kTileSlots - 1)) {
+    const uint32_t w = slot[p];
+    if (w == kEmpty) return -1;
+    if ((w & ~kSlotQ) == fp) {
+      const int32_t sq = (int32_t)(w & kSlotQ);
+      if ((uint32_t)tri_s[j_of(sq)] == lo && (uint32_t)tri_s[j_of(next_q(sq))] == hi) return sq;
+    }
+  }
+  return -1;
+}
+
 // One CTA per tile of kTileTris triangles.  Phases (PAPER.md section in brackets):
 //  P0 stage the triangle tile (coalesced, streaming)
 //  P1 per triangle: checks, CCW orientation (R10), longest edge Lcode (Alg. 2/7)
-//  P2 tile-local twin matching in a shared-memory hash on (min, max)      [Sec. 4]
-//  P3 write origin/twin (coalesced); cross-tile half-edges -> leftover list
-//  P4 per half-edge whose twin is in the tile: frontier/seed bits (Alg. 8-9) and the
-//     unlink rewire (Alg. 11) with the rotation walk in shared memory; tips (next ==
-//     twin).  Half-edges that need a twin outside the tile are deferred to
-//     k_label_fixup (label phase), which sees the completed global twin array.
-__global__ void __launch_bounds__(kTileThreads, 3)
+//  P2 tile-local twin matching in a shared-memory hash on (min, max): the lo->hi halves
+//     insert (plain-store claim of the home slot, CAS only for collision losers -- shared
+//     atomics cost ~2 cycles per lane), the hi->lo halves look up read-only   [Sec. 4]
+//  P3 origin/twin out (coalesced); rotation successor of every half-edge: itself if it
+//     is a frontier edge (Alg. 8), else next_in(twin) (sweep_out, R1); a third copy of
+//     an edge breaks the twin involution
+//  P4 the unlink rewire (Alg. 11) by pointer jumping on the successors (lock-step, no
+//     divergent walks); frontier / seed bits (Alg. 8-9); tips (next == twin);
+//     half-edges needing a twin outside the tile (or a longer rotation) are deferred
+//     to k_label_fixup (label phase)
+//  P6 seeds whose polygon closes inside the tile: landing + loop walk in shared memory
+//     -> canonical seed bits and loop lengths (others go to the global seed walk)
+//  P5 block-aggregated appends of the leftover / deferred / tip / deferred-seed lists
+__global__ void __launch_bounds__(kTileThreads, 2)
     k_tile(const double2* __restrict__ xy, const int32_t* __restrict__ tri, int64_t V, int64_t T,
            int32_t* __restrict__ origin, int32_t* __restrict__ twin, int32_t* __restrict__ next,
            uint8_t* __restrict__ lcode, uint32_t* __restrict__ F0, uint32_t* __restrict__ F1,
-           uint32_t* __restrict__ S, unsigned long long* __restrict__ left_key, int32_t* __restrict__ left_e,
-           int32_t* __restrict__ def_e, int32_t* __restrict__ tips, DevCounters* ctr) {
+           uint32_t* __restrict__ S, uint32_t* __restrict__ C, int32_t* __restrict__ len,
+           unsigned long long* __restrict__ left_key, int32_t* __restrict__ left_e, int32_t* __restrict__ def_e,
+           int32_t* __restrict__ tips, int32_t* __restrict__ sdef, DevCounters* ctr) {
   extern __shared__ __align__(16) unsigned char smem_tile[];
   int32_t* tri_s = reinterpret_cast<int32_t*>(smem_tile);
-  int16_t* tw_s = reinterpret_cast<int16_t*>(smem_tile + kTileHE * 4);
-  uint16_t* slot = reinterpret_cast<uint16_t*>(smem_tile + kTileHE * 6);
-  uint8_t* lc_s = smem_tile + kTileHE * 6 + kTileSlots * 2;
+  int16_t* tw_s = reinterpret_cast<int16_t*>(smem_tile + kOffTw);
+  uint32_t* slot = reinterpret_cast<uint32_t*>(smem_tile + kOffSlot);
+  uint8_t* lc_s = smem_tile + kOffLc;
+  int16_t* nx_l = reinterpret_cast<int16_t*>(smem_tile + kOffNx);               // local next, -1: not walkable
+  uint32_t* Sw = reinterpret_cast<uint32_t*>(smem_tile + kOffNx + kTileHE * 2);  // seed bits (e order)
+  uint32_t* Cw = Sw + kTileWords;                                                // canonical seed bits
+  int16_t* slist = reinterpret_cast<int16_t*>(Cw + kTileWords);                 // compacted seeds
+  // overlays of the slot area (after P2)
+  uint16_t* succ = reinterpret_cast<uint16_t*>(slot);
+  uint32_t* Lm = slot + kTileQ / 2;
+  uint32_t* Dm = Lm + kTileWords;
+  uint32_t* Tm = Dm + kTileWords;
+  uint32_t* SDm = Tm + kTileWords;
+  int* scan_sm = reinterpret_cast<int*>(SDm + kTileWords);  // 136 ints
 
   const int64_t f0 = (int64_t)blockIdx.x * kTileTris;
   const int nt = (int)(T - f0 < kTileTris ? T - f0 : kTileTris);
-  const int nhe = 3 * nt;
+  const int nhe = 3 * nt, nq = 4 * nt;
   const int64_t e0 = 3 * f0;
   const int tid = threadIdx.x, lane = tid & 31;
+#ifdef POLYLLA_PHASE_TIMING
+  long long t_phase_ = clock64();
+#endif
 
   // ---- P0
   const int32_t* src = tri + e0;
@@ -87,15 +216,17 @@ __global__ void __launch_bounds__(kTileThreads, 3)
   } else {
     for (int i = tid; i < nhe; i += kTileThreads) tri_s[i] = __ldcs(src + i);
   }
-  for (int i = tid; i < kTileSlots / 2; i += kTileThreads) reinterpret_cast<uint32_t*>(slot)[i] = 0xFFFFFFFFu;
-  for (int i = tid; i < kTileHE / 2; i += kTileThreads) reinterpret_cast<uint32_t*>(tw_s)[i] = 0xFFFFFFFFu;
+  for (int i = tid; i < kTileSlots / 4; i += kTileThreads)
+    reinterpret_cast<uint4*>(slot)[i] = make_uint4(kEmpty, kEmpty, kEmpty, kEmpty);
+  for (int i = tid; i < kTileQ / 2; i += kTileThreads) reinterpret_cast<uint32_t*>(tw_s)[i] = 0xFFFFFFFFu;
   __syncthreads();
+  PHASE_MARK(0);
 
   // ---- P1
   const uint64_t pol = policy_evict_last();
   uint32_t bad = 0;
   int flips = 0;
-#pragma unroll 4
+#pragma unroll 2
   for (int t = tid; t < nt; t += kTileThreads) {
     int32_t a = tri_s[3 * t], b = tri_s[3 * t + 1], c = tri_s[3 * t + 2];
     if ((uint64_t)a >= (uint64_t)V || (uint64_t)b >= (uint64_t)V || (uint64_t)c >= (uint64_t)V) {
@@ -128,105 +259,223 @@ __global__ void __launch_bounds__(kTileThreads, 3)
     if (bad) raise_status(ctr, bad);
   }
   __syncthreads();
+  PHASE_MARK(1);
 
-  // ---- P2
+  // ---- P2a: the lo->hi halves claim their home slot with a plain store (last writer wins) ...
   uint32_t nm = 0;
   for (int j = tid; j < nhe; j += kTileThreads) {
     const int32_t o = tri_s[j], tg = tri_s[next_local(j)];
-    const uint32_t lo = (uint32_t)min(o, tg), hi = (uint32_t)max(o, tg);
-    uint32_t h = mix32(lo, hi) & (kTileSlots - 1);
-    for (int probe = 0; probe < kTileSlots; ++probe) {
-      uint16_t s = slot[h];
-      if (s == kEmpty16) {
-        const uint16_t old = atomicCAS(&slot[h], kEmpty16, (uint16_t)j);
-        if (old == kEmpty16) break;  // first of its key
-        s = old;
+    if (o < tg) {
+      const uint32_t h = tile_hash((uint32_t)o, (uint32_t)tg);
+      slot[h & (kTileSlots - 1)] = (h & ~kSlotQ) | (uint32_t)q_of(j);
+    }
+  }
+  __syncthreads();
+  // ... the losers of a home slot insert with CAS + linear probing from there
+  for (int j = tid; j < nhe; j += kTileThreads) {
+    const int32_t o = tri_s[j], tg = tri_s[next_local(j)];
+    if (o < tg) {
+      const uint32_t h = tile_hash((uint32_t)o, (uint32_t)tg);
+      const int32_t q = q_of(j);
+      if (slot[h & (kTileSlots - 1)] != ((h & ~kSlotQ) | (uint32_t)q))
+        nm |= tile_insert(slot, tri_s, q, (uint32_t)o, (uint32_t)tg);
+    }
+  }
+  __syncthreads();
+  // ---- P2b: the hi->lo halves find their twin (read-only probes)
+  for (int j = tid; j < nhe; j += kTileThreads) {
+    const int32_t o = tri_s[j], tg = tri_s[next_local(j)];
+    if (o > tg) {
+      const int32_t sq = tile_lookup(slot, tri_s, (uint32_t)tg, (uint32_t)o);
+      if (sq >= 0) {
+        const int32_t q = q_of(j);
+        tw_s[q] = (int16_t)sq;
+        tw_s[sq] = (int16_t)q;
       }
-      const int32_t sj = s & ~kPaired16;
-      const int32_t so = tri_s[sj], st = tri_s[next_local(sj)];
-      if ((uint32_t)min(so, st) == lo && (uint32_t)max(so, st) == hi) {
-        if ((s & kPaired16) || so == o) { nm = ST_NONMANIFOLD_EDGE; break; }
-        if (atomicCAS(&slot[h], s, (uint16_t)(s | kPaired16)) != s) { nm = ST_NONMANIFOLD_EDGE; break; }
-        tw_s[j] = (int16_t)sj;
-        tw_s[sj] = (int16_t)j;
-        break;
-      }
-      h = (h + 1) & (kTileSlots - 1);
     }
   }
   if (nm) raise_status(ctr, nm);
   __syncthreads();
+  PHASE_MARK(2);
 
-  // ---- P3 + P4 (one pass over the tile's half-edges, warp-aligned for the ballots)
-  for (int base = 0; base < nhe; base += kTileThreads) {
+  // ---- P3: origin/twin out; rotation successors:
+  //   succ[x] = x | FRONT   if x is a frontier half-edge (walk ends there)
+  //   succ[x] = x | UNKNOWN if twin(x) is outside the tile (walk must be deferred)
+  //   succ[x] = next_q(twin x)  otherwise (cross the non-frontier edge: sweep_out)
+  for (int q = tid; q < nq; q += kTileThreads) {
+    const int k = q & 3, t = q >> 2;
+    if (k == 3) continue;  // padding slot of the quad layout
+    const int32_t j = 3 * t + k;
+    const int32_t tq = tw_s[q];
+    if (tq >= 0 && tw_s[tq] != q) nm = ST_NONMANIFOLD_EDGE;  // twin claimed twice (edge in > 2 triangles)
+    __stcs(origin + e0 + j, tri_s[j]);
+    __stcs(twin + e0 + j, tq >= 0 ? (int32_t)(e0 + j_of(tq)) : -1);
+    uint16_t sc;
+    if (tq < 0) sc = (uint16_t)(q | kSuccUnknown);
+    else if (lc_s[t] != k && lc_s[tq >> 2] != (tq & 3)) sc = (uint16_t)(q | kSuccFront);  // neither half longest
+    else sc = (uint16_t)next_q(tq);
+    succ[q] = sc;
+  }
+  if (nm) raise_status(ctr, nm);
+  __syncthreads();
+  PHASE_MARK(3);
+
+  // ---- P4a: pointer jumping (in place; any value on a chain is a valid shortcut)
+#pragma unroll 1
+  for (int round = 0; round < kTileJumps; ++round) {
+    for (int q = tid; q < nq; q += kTileThreads) {
+      const uint16_t sc = succ[q];
+      if (!(sc & (kSuccFront | kSuccUnknown)) && (q & 3) != 3) succ[q] = succ[sc];
+    }
+    __syncthreads();
+  }
+  PHASE_MARK(4);
+
+  // ---- P4b: per half-edge (e order): F / S words (Alg. 8-9), next (Alg. 11), tips
+  for (int base = 0; base < kTileHE; base += kTileThreads) {
     const int j = base + tid;
-    const bool valid = j < nhe;
     bool fr = false, sd = false, tip = false, deferred = false, left = false;
-    if (valid) {
-      const int32_t t = tw_s[j];
-      __stcs(origin + e0 + j, tri_s[j]);
-      __stcs(twin + e0 + j, t >= 0 ? (int32_t)(e0 + t) : -1);
-      if (t < 0) {
-        left = true;
-        deferred = true;
+    int32_t nl_j = -1;
+    if (j < nhe) {
+      const int q = q_of(j);
+      const int32_t tq = tw_s[q];
+      if (tq < 0) {
+        deferred = left = true;
       } else {
-        const bool Le = lc_s[j / 3] == j % 3;
-        const bool Lt = lc_s[t / 3] == t % 3;
-        fr = !Le && !Lt;
-        sd = Le && Lt && j < t;
-        int32_t nx = next_local(j);
+        fr = succ[q] == (uint16_t)(q | kSuccFront);  // terminal of its own chain: a frontier half-edge
+        sd = lc_s[q >> 2] == (q & 3) && lc_s[tq >> 2] == (tq & 3) && q < tq;  // terminal edge, smaller id
+        int32_t nx = next_q(q);
         if (fr) {
-          int32_t x = nx;
-          for (int steps = 0;; ++steps) {
-            const int32_t tx = tw_s[x];
-            if (tx < 0 || steps >= kTileWalk) { deferred = true; break; }
-            if (lc_s[x / 3] != x % 3 && lc_s[tx / 3] != tx % 3) break;  // frontier edge
-            x = next_local(tx);                                        // cross it (sweep_out)
+          const uint16_t r = succ[nx];  // first frontier half-edge about target(j), if reached
+          if (r & kSuccFront) {
+            nx = r & kSuccIdx;
+            tip = nx == tq;  // barrier tip: next == twin (R4)
+          } else {
+            deferred = true;
           }
-          nx = x;
-          tip = !deferred && x == t;
         }
-        if (!deferred) __stcs(next + e0 + j, (int32_t)(e0 + nx));
-        else fr = sd = false;  // the fixup sets every bit of a deferred half-edge
+        if (!deferred) {
+          nx = j_of(nx);
+          __stcs(next + e0 + j, (int32_t)(e0 + nx));
+          if (!tip) nl_j = nx;
+        } else {
+          fr = sd = false;  // the fixup sets every bit of a deferred half-edge
+        }
       }
+      nx_l[j] = (int16_t)nl_j;
     }
-    const uint32_t fw = __ballot_sync(0xffffffffu, fr);
-    const uint32_t sw = __ballot_sync(0xffffffffu, sd);
-    const uint32_t tm = __ballot_sync(0xffffffffu, tip);
-    const uint32_t dm = __ballot_sync(0xffffffffu, deferred);
-    const uint32_t lm = __ballot_sync(0xffffffffu, left);
+    const uint32_t fw = __ballot_sync(0xffffffffu, fr), sw = __ballot_sync(0xffffffffu, sd);
+    const uint32_t tm = __ballot_sync(0xffffffffu, tip), dm = __ballot_sync(0xffffffffu, deferred),
+                   lm = __ballot_sync(0xffffffffu, left);
     const int wbase = j - lane;
-    if (lane == 0 && wbase < nhe) {
-      const int64_t w = (e0 + wbase) >> 5;
-      F0[w] = fw;
-      F1[w] = fw;
-      S[w] = sw;
-    }
-    if (lm) {
-      int pos = 0;
-      if (lane == 0) pos = atomicAdd(&ctr->n_left, __popc(lm));
-      pos = __shfl_sync(0xffffffffu, pos, 0) + __popc(lm & ((1u << lane) - 1));
-      if (left) {
-        const int32_t o = tri_s[j], tg = tri_s[next_local(j)];
-        const uint64_t lo = (uint32_t)min(o, tg), hi = (uint32_t)max(o, tg);
-        left_key[pos] = (lo << 32) | hi;
-        left_e[pos] = (int32_t)(e0 + j);
+    if (lane == 0) {
+      if (wbase < nhe) {
+        const int64_t w = (e0 + wbase) >> 5;
+        F0[w] = fw;
+        F1[w] = fw;
+        S[w] = sw;
       }
-    }
-    if (dm) {
-      int pos = 0;
-      if (lane == 0) pos = atomicAdd(&ctr->n_def, __popc(dm));
-      pos = __shfl_sync(0xffffffffu, pos, 0) + __popc(dm & ((1u << lane) - 1));
-      if (deferred) def_e[pos] = (int32_t)(e0 + j);
-    }
-    if (tm) {
-      int pos = 0;
-      if (lane == 0) pos = atomicAdd(&ctr->n_tips, __popc(tm));
-      pos = __shfl_sync(0xffffffffu, pos, 0) + __popc(tm & ((1u << lane) - 1));
-      if (tip) tips[pos] = (int32_t)(e0 + j);
+      Lm[wbase >> 5] = lm;
+      Dm[wbase >> 5] = dm;
+      Tm[wbase >> 5] = tm;
+      Sw[wbase >> 5] = sw;
+      Cw[wbase >> 5] = 0u;
+      SDm[wbase >> 5] = 0u;
     }
   }
+  __syncthreads();
+  PHASE_MARK(5);
+
+  // ---- P6: seeds whose polygon closes inside the tile (Alg. 12 + Overwrite seeds,
+  // PAPER.md L778-849): land on a frontier half-edge by rotation, walk the loop on nx_l,
+  // keep the minimum id and the length.  Loops that touch a deferred half-edge or a
+  // barrier tip (repaired later) are handed to the global seed walk.
+  {
+    const uint32_t w = tid < kTileWords ? Sw[tid] : 0u;
+    int4 tot;
+    const int4 pre = block_scan4(make_int4(__popc(w), 0, 0, 0), &tot, scan_sm);
+    int p = pre.x;
+    for (uint32_t b = w; b; b &= b - 1) slist[p++] = (int16_t)(tid * 32 + __ffs(b) - 1);
+    __syncthreads();
+    for (int i = tid; i < tot.x; i += kTileThreads) {
+      const int32_t sj = slist[i];
+      int32_t q = q_of(sj);
+      bool ok = true;
+      for (int steps = 0; succ[q] != (uint16_t)(q | kSuccFront); ++steps) {  // rotate to a frontier half-edge
+        const int32_t tq = tw_s[q];
+        if (tq < 0 || steps > 64) { ok = false; break; }
+        q = next_q(tq);
+      }
+      int32_t mn = 0, n = 0;
+      if (ok) {
+        const int32_t x = j_of(q);
+        int32_t y = x;
+        mn = x;
+        do {
+          mn = min(mn, y);
+          ++n;
+          y = nx_l[y];
+          if (y < 0 || n > 1024) { ok = false; break; }  // deferred / barrier-tip loop
+        } while (y != x);
+      }
+      if (ok) {
+        atomicOr(&Cw[mn >> 5], 1u << (mn & 31));
+        len[e0 + mn] = n;
+      } else {
+        atomicOr(&SDm[sj >> 5], 1u << (sj & 31));
+      }
+    }
+  }
+  __syncthreads();
+  for (int w = tid; w * 32 < nhe; w += kTileThreads) C[(e0 >> 5) + w] = Cw[w];
+  PHASE_MARK(6);
+
+  // ---- P5: one global atomic per list per tile, then write the entries
+  uint32_t lw = 0, dw = 0, tw = 0, sw = 0;
+  if (tid < kTileWords) { lw = Lm[tid]; dw = Dm[tid]; tw = Tm[tid]; sw = SDm[tid]; }
+  int4 tot;
+  const int4 pre = block_scan4(make_int4(__popc(lw), __popc(dw), __popc(tw), __popc(sw)), &tot, scan_sm);
+  if (tid == 0) {
+    scan_sm[132] = tot.x ? atomicAdd(&ctr->n_left, tot.x) : 0;
+    scan_sm[133] = tot.y ? atomicAdd(&ctr->n_def, tot.y) : 0;
+    scan_sm[134] = tot.z ? atomicAdd(&ctr->n_tips, tot.z) : 0;
+    scan_sm[135] = tot.w ? atomicAdd(&ctr->n_sdef, tot.w) : 0;
+  }
+  __syncthreads();
+  int pl = scan_sm[132] + pre.x, pd = scan_sm[133] + pre.y, pt = scan_sm[134] + pre.z, ps = scan_sm[135] + pre.w;
+  while (lw) {
+    const int j = tid * 32 + __ffs(lw) - 1;
+    lw &= lw - 1;
+    const int32_t o = tri_s[j], tg = tri_s[next_local(j)];
+    const uint64_t lo = (uint32_t)min(o, tg), hi = (uint32_t)max(o, tg);
+    left_key[pl] = (lo << 32) | hi;
+    left_e[pl++] = (int32_t)(e0 + j);
+  }
+  while (dw) {
+    def_e[pd++] = (int32_t)(e0 + tid * 32 + __ffs(dw) - 1);
+    dw &= dw - 1;
+  }
+  while (tw) {
+    tips[pt++] = (int32_t)(e0 + tid * 32 + __ffs(tw) - 1);
+    tw &= tw - 1;
+  }
+  while (sw) {
+    sdef[ps++] = (int32_t)(e0 + tid * 32 + __ffs(sw) - 1);
+    sw &= sw - 1;
+  }
+  PHASE_MARK(7);
 }
+
+#ifdef POLYLLA_PHASE_TIMING
+extern "C" __attribute__((visibility("default"))) int polylla_debug_phase_cycles(unsigned long long* out, int reset) {
+  if (cudaMemcpyFromSymbol(out, g_phase_cycles, sizeof(g_phase_cycles)) != cudaSuccess) return -1;
+  if (reset) {
+    static const unsigned long long z[16] = {0};
+    cudaMemcpyToSymbol(g_phase_cycles, z, sizeof(z));
+  }
+  return 0;
+}
+#endif
 
 __device__ __forceinline__ uint64_t hash_cap_for(int32_t n) {
   uint64_t c = 1024;
@@ -362,7 +611,8 @@ int launch_build(Ctx* c, cudaStream_t s) {
   prof_mark(s, "k_tile");
   k_tile<<<(unsigned)tiles, kTileThreads, kTileSmem, s>>>(reinterpret_cast<const double2*>(c->xy), c->tri, c->V, c->T,
                                                           c->origin, c->twin, c->next, c->lcode, c->F0, c->F1, c->S,
-                                                          c->left_key, c->left_e, c->def_e, c->tips, c->ctr);
+                                                          c->C, c->len, c->left_key, c->left_e, c->def_e, c->tips,
+                                                          c->sdef, c->ctr);
   ++n;
   const int grid = 148 * 8;
   prof_mark(s, "k_left_match");

@@ -60,6 +60,7 @@ static Layout layout(int64_t V, int64_t T) {
       (size_t)(3 * T) * 4,    // 25 tri staging
       sizeof(DevCounters),    // 26 counters
       (size_t)(3 * T) * 4,    // 27 deferred half-edges
+      (size_t)(T + 1) * 4,    // 28 deferred seeds
   };
   Layout L{};
   size_t o = 0;
@@ -107,6 +108,7 @@ bool carve(Ctx* c, void* ws, size_t bytes) {
   c->tri_stage = reinterpret_cast<int32_t*>(b + L.off[25]);
   c->ctr = reinterpret_cast<DevCounters*>(b + L.off[26]);
   c->def_e = reinterpret_cast<int32_t*>(b + L.off[27]);
+  c->sdef = reinterpret_cast<int32_t*>(b + L.off[28]);
   c->n_words = (3 * c->T + 31) / 32;
   return true;
 }

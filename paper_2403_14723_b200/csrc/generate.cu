@@ -9,7 +9,7 @@
 //   k_repair_rewire  one thread per touched vertex w (the tip v and the far end u of m):
 //                    recompute next[p] for every incoming frontier half-edge p of w with
 //                    the F1 bits (the only next values repair can change).
-//   k_seed_walk      one thread per seed (S bits + mids): rotate to the first frontier
+//   k_seed_walk      one thread per seed k_tile deferred + the repair seeds: rotate to the first frontier
 //                    half-edge (Alg. 12), walk the polygon through next, keep the minimum
 //                    id as the canonical seed and its loop length (Overwrite seeds,
 //                    PAPER.md L816).  Duplicate walks of one polygon write the same values.
@@ -79,7 +79,6 @@ __global__ void k_repair_rewire(int64_t T, const int32_t* __restrict__ twin, con
 }
 
 constexpr int kSeedThreads = 256;
-constexpr int kSeedWarps = kSeedThreads / 32;
 
 __device__ __forceinline__ void process_seed(int32_t s, int64_t T3, int64_t H, const int32_t* __restrict__ twin,
                                              const int32_t* __restrict__ next, const uint32_t* __restrict__ F1,
@@ -101,42 +100,18 @@ __device__ __forceinline__ void process_seed(int32_t s, int64_t T3, int64_t H, c
   len[mn] = (int32_t)n;
 }
 
+// the seeds k_tile could not close inside their tile, plus both halves of every middle
+// edge of the repair (they seed the split polygons)
 __global__ void __launch_bounds__(kSeedThreads)
-    k_seed_walk(int64_t T, int64_t n_words, const int32_t* __restrict__ twin, const int32_t* __restrict__ next,
-                const uint32_t* __restrict__ F1, const uint32_t* __restrict__ S, const int32_t* __restrict__ mids,
+    k_seed_walk(int64_t T, const int32_t* __restrict__ twin, const int32_t* __restrict__ next,
+                const uint32_t* __restrict__ F1, const int32_t* __restrict__ sdef, const int32_t* __restrict__ mids,
                 uint32_t* C, int32_t* len, DevCounters* ctr) {
-  __shared__ int32_t queue[kSeedWarps][32 * 32];
   if (ctr->status) return;
   const int64_t T3 = 3 * T;
   const int64_t H = T3 + ctr->n_border;
-  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  int32_t* q = queue[wid];
-  const int64_t groups = (n_words + 31) / 32;
-  for (int64_t g = (int64_t)blockIdx.x * kSeedWarps + wid; g < groups; g += (int64_t)gridDim.x * kSeedWarps) {
-    const int64_t w = g * 32 + lane;
-    uint32_t bits = w < n_words ? S[w] : 0u;
-    const int cnt = __popc(bits);
-    int incl = cnt;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      const int v = __shfl_up_sync(0xffffffffu, incl, o);
-      if (lane >= o) incl += v;
-    }
-    const int total = __shfl_sync(0xffffffffu, incl, 31);
-    int pos = incl - cnt;
-    while (bits) {
-      const int b = __ffs(bits) - 1;
-      bits &= bits - 1;
-      q[pos++] = (int32_t)(w * 32 + b);
-    }
-    __syncwarp();
-    for (int i = lane; i < total; i += 32) process_seed(q[i], T3, H, twin, next, F1, C, len, ctr);
-    __syncwarp();
-  }
-  // the repair's new seeds (both halves of every middle edge)
-  const int32_t nm = 2 * ctr->n_tips;
-  for (int32_t j = blockIdx.x * kSeedThreads + threadIdx.x; j < nm; j += gridDim.x * kSeedThreads)
-    process_seed(mids[j], T3, H, twin, next, F1, C, len, ctr);
+  const int32_t ns = ctr->n_sdef, nm = 2 * ctr->n_tips;
+  for (int32_t j = blockIdx.x * kSeedThreads + threadIdx.x; j < ns + nm; j += gridDim.x * kSeedThreads)
+    process_seed(j < ns ? sdef[j] : mids[j - ns], T3, H, twin, next, F1, C, len, ctr);
 }
 
 struct CanonOp {
@@ -170,9 +145,9 @@ int launch_generate(Ctx* c, cudaStream_t s) {
   k_repair_mid<<<148 * 16, 128, 0, s>>>(c->T, c->twin, c->F1, c->tips, c->mids, c->aff, c->ctr);
   k_repair_rewire<<<148 * 32, 128, 0, s>>>(c->T, c->twin, c->F1, c->aff, c->next, c->ctr);
   prof_mark(s, "k_seed_walk");
-  cudaMemsetAsync(c->C, 0, (size_t)c->n_words * 4, s);
-  k_seed_walk<<<148 * 8, kSeedThreads, 0, s>>>(c->T, c->n_words, c->twin, c->next, c->F1, c->S, c->mids, c->C,
-                                               c->len, c->ctr);
+  // (the canonical bit-vector C was written in full by k_tile; global walks OR into it)
+  k_seed_walk<<<148 * 8, kSeedThreads, 0, s>>>(c->T, c->twin, c->next, c->F1, c->sdef, c->mids, c->C, c->len,
+                                               c->ctr);
   n += 3;
   prof_mark(s, "k_canon_scan");
   CanonOp op{c->C, c->F1, c->len, c->seeds, c->offsets, c->ctr};

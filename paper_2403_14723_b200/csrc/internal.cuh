@@ -41,7 +41,8 @@ struct DevCounters {
   int32_t n_f1;      // #interior F1 half-edges
   uint32_t hash_cap; // capacity (pow2 <= 2^31) of the leftover hash for this run
   int32_t n_def;     // half-edges deferred by k_tile to the label fixup
-  int32_t pad[6];
+  int32_t n_sdef;    // seeds deferred by k_tile to the global seed walk
+  int32_t pad[5];
 };
 
 struct Ctx {
@@ -58,6 +59,7 @@ struct Ctx {
   unsigned long long* left_key;
   int32_t* left_e;
   int32_t* def_e;   // [3T] half-edges deferred by k_tile
+  int32_t* sdef;    // [T] seeds deferred by k_tile
   uint32_t* ehash;  // leftover-edge hash slots [hash_cap_max] (capacity chosen on device)
   uint32_t* vkey;   // border-vertex hash: key = vertex id [hash_cap_max]
   int32_t* vval;    //                      val = border half-edge id

@@ -27,14 +27,15 @@ __device__ __forceinline__ bool is_longest(const uint8_t* __restrict__ lcode, in
 __global__ void __launch_bounds__(kLabelThreads)
     k_label_fixup(int64_t T, const int32_t* __restrict__ def_e, const int32_t* __restrict__ twin,
                   const uint8_t* __restrict__ lcode, int32_t* __restrict__ next, uint32_t* __restrict__ F0,
-                  uint32_t* __restrict__ F1, uint32_t* __restrict__ S, int32_t* __restrict__ tips, DevCounters* ctr) {
+                  uint32_t* __restrict__ F1, uint32_t* __restrict__ S, int32_t* __restrict__ tips,
+                  int32_t* __restrict__ sdef, DevCounters* ctr) {
   if (ctr->status) return;
   const int64_t T3 = 3 * T;
   const int32_t n = ctr->n_def;
   const int lane = threadIdx.x & 31;
   for (int32_t base = blockIdx.x * kLabelThreads; base < n; base += gridDim.x * kLabelThreads) {
     const int32_t i = base + threadIdx.x;
-    bool tip = false, walk_err = false;
+    bool tip = false, walk_err = false, sd = false;
     int32_t e = -1;
     if (i < n) {
       e = def_e[i];
@@ -43,7 +44,7 @@ __global__ void __launch_bounds__(kLabelThreads)
       const bool Le = is_longest(lcode, e);
       const bool Lt = !tb && is_longest(lcode, t);
       const bool fr = tb || (!Le && !Lt);
-      const bool sd = Le && (tb || (Lt && e < t));
+      sd = Le && (tb || (Lt && e < t));
       int32_t nx = next_in(e);
       if (fr) {
         int32_t x = nx;
@@ -69,6 +70,13 @@ __global__ void __launch_bounds__(kLabelThreads)
       pos = __shfl_sync(0xffffffffu, pos, 0) + __popc(tm & ((1u << lane) - 1));
       if (tip) tips[pos] = e;
     }
+    const uint32_t sm = __ballot_sync(0xffffffffu, sd);  // seeds found here go to the global seed walk
+    if (sm) {
+      int pos = 0;
+      if (lane == 0) pos = atomicAdd(&ctr->n_sdef, __popc(sm));
+      pos = __shfl_sync(0xffffffffu, pos, 0) + __popc(sm & ((1u << lane) - 1));
+      if (sd) sdef[pos] = e;
+    }
     if (walk_err) raise_status(ctr, ST_WALK);
   }
 }
@@ -76,7 +84,7 @@ __global__ void __launch_bounds__(kLabelThreads)
 int launch_label(Ctx* c, cudaStream_t s) {
   prof_mark(s, "k_label_fixup");
   k_label_fixup<<<148 * 16, kLabelThreads, 0, s>>>(c->T, c->def_e, c->twin, c->lcode, c->next, c->F0, c->F1, c->S,
-                                                   c->tips, c->ctr);
+                                                   c->tips, c->sdef, c->ctr);
   prof_end(s);
   return cudaGetLastError() == cudaSuccess ? 1 : -1;
 }
