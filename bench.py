@@ -37,6 +37,7 @@ import numpy as np  # noqa: E402
 import torch  # noqa: E402
 
 import synth  # noqa: E402
+from paper_2403_14723_b200 import batch  # noqa: E402
 
 METRIC = "input triangles/sec (kernel-only pipeline build->label->generate->CSR, 1 mesh per GPU)"
 
@@ -46,7 +47,8 @@ def parse():
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=200)
     ap.add_argument("--warmup", type=int, default=10)
-    ap.add_argument("--config", type=int, default=3, choices=[1, 2, 3, 4, 5])
+    ap.add_argument("--config", type=int, default=3, choices=[1, 2, 3, 4, 5],
+                    help="BASELINE config: 1 tiny grid, 2 1M random, 3 10M random (default), 4 capacity, 5 batch")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--e2e-steps", type=int, default=10)
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -67,24 +69,35 @@ def dist_setup():
     return ws, rank, local
 
 
-def workload(cfg: int, rank: int):
-    """Synthetic input of BASELINE config `cfg` (recipes: DESIGN.md 'Input recipe')."""
-    if cfg == 1:
-        xy, tri = synth.grid(32, 0.2, 1)
-        name = "config1: jittered 32x32 grid (a=0.2), 1 mesh"
-    elif cfg == 2:
-        xy, tri = synth.random_delaunay(1_000_000, 2 + 1000 * rank)
-        name = "config2: 1M random points, Delaunay (Morton-ordered triangles), 1 mesh per GPU"
-    elif cfg == 3:
-        xy, tri = synth.random_delaunay(10_000_000, 3 + 1000 * rank)
-        name = "config3: 10M random points, Delaunay (Morton-ordered triangles), 1 mesh per GPU"
-    elif cfg == 4:
-        xy, tri = synth.grid(16000, 0.2, 4)
-        name = "config4: jittered 16000x16000 grid (256M vertices), 1 mesh per GPU"
-    else:
-        xy, tri = synth.grid(2000, 0.2 if rank % 2 == 0 else 0.0, 1000 + rank)
-        name = "config5-slice: one 4M-vertex grid per GPU (jittered on even ranks, regular on odd)"
-    return name, xy, tri
+def workload(cfg: int, rank: int, world: int, device):
+    """Synthetic input of BASELINE config `cfg` for this rank (recipes: DESIGN.md 'Input
+    recipe').  Returns (description, scaling, [mesh dicts with xy/tri device tensors and,
+    for the e2e leg, a host generator])."""
+    if cfg in (1, 2, 3):
+        if cfg == 1:
+            fn = lambda: synth.grid(32, 0.2, 1)  # noqa: E731
+            name = "config1: jittered 32x32 grid (a=0.2), 1 mesh per GPU"
+        else:
+            n = 1_000_000 if cfg == 2 else 10_000_000
+            fn = lambda: synth.random_delaunay(n, cfg + 1000 * rank)  # noqa: E731
+            name = f"config{cfg}: {n // 1_000_000}M random points, Delaunay (Morton-ordered triangles), 1 mesh per GPU"
+        xy, tri = fn()
+        m = dict(xy=torch.from_numpy(xy).to(device), tri=torch.from_numpy(tri).to(device), host=lambda: (xy, tri),
+                 xy_np=xy, tri_np=tri)
+        return name, "weak", [m]
+    if cfg == 4:
+        xy, tri = synth.grid_device(16000, 0.2, 4 + 1000 * rank, device=device)
+        name = "config4: jittered 16000x16000 grid (256M vertices, 512M triangles), generated on device, 1 per GPU"
+        return name, "weak", [dict(xy=xy, tri=tri, host=None)]
+    metas = [mm for mm in batch.config5_meshes() if mm["index"] in set(batch.shard(64, rank, world))]
+    out = []
+    for mm in metas:
+        xy, tri = synth.grid_device(mm["s"], mm["a"], mm["seed"], device=device)
+        out.append(dict(xy=xy, tri=tri, meta=mm,
+                        host=(lambda mm=mm: synth.grid(mm["s"], mm["a"], mm["seed"]))))
+    name = ("config5: batch of 64 independent 2000x2000 grids (4M vertices each; 32 jittered a=0.2 + 32 regular "
+            "Alg. 13), mesh i on rank i mod N, generated on device (excluded from timing)")
+    return name, "strong", out
 
 
 def load_peaks():
@@ -156,12 +169,8 @@ def alg_bytes(T, V, P, L):
     """Algorithmic bytes: the method's compulsory HBM traffic."""
     return {
         "pipeline": 60 * T + 16 * V + 12 * L + 4 * P,
-        # tri in + xy once + origin out + twin out + Lcode out
-        "k_build_tile": 12 * T + 16 * V + 12 * T + 12 * T + T,
-        # twin in + Lcode in + next out + F0/F1/S bit-vectors out
-        "k_label_rewire": 12 * T + T + 12 * T + 3 * (3 * T) // 8,
-        # S + F1 bits in, next re-read along the loops (L), canonical bits + len out
-        "k_seed_walk": 2 * (3 * T) // 8 + 4 * L + (3 * T) // 8 + 4 * P,
+        # tri in + xy once + origin/twin/next out + Lcode out + F0/F1/S/C bit-vectors out
+        "k_tile": 12 * T + 16 * V + 36 * T + T + 4 * (3 * T) // 8,
         # seeds + offsets in, next + origin along the loops, loops + offsets out
         "k_extract": 4 * P + 4 * (P + 1) + 8 * L + 4 * L + 4 * (P + 1),
     }
@@ -178,7 +187,7 @@ def ncu_traffic(kernel: str, cfg: int):
         return None
 
 
-def cpu_oracle_baseline(xy, tri, budget_s=30.0):
+def cpu_oracle_baseline(xy, tri):
     """Time the CPU oracle on a bounded sample of the workload (rank 0, N = 1)."""
     import oracle
     T = tri.shape[0]
@@ -240,35 +249,51 @@ def main():
     from paper_2403_14723_b200 import polylla as pp
 
     dev = torch.device("cuda", local if ws > 1 else 0)
-    name, xy_np, tri_np = workload(args.config, rank)
-    V, T = xy_np.shape[0], tri_np.shape[0]
-    xy = torch.from_numpy(xy_np).to(dev)
-    tri = torch.from_numpy(tri_np).to(dev)
-    wsp = pp.alloc_workspace(V, T, dev)
-    offsets = torch.empty(T + 1, dtype=torch.int32, device=dev)
-    loops = torch.empty(3 * T, dtype=torch.int32, device=dev)
+    if ws > 1:
+        import torch.distributed as dist
+    name, scaling, meshes = workload(args.config, rank, ws, dev)
+    Vmax = max(m["xy"].shape[0] for m in meshes)
+    Tmax = max(m["tri"].shape[0] for m in meshes)
+    wsp = pp.alloc_workspace(Vmax, Tmax, dev)
+    offsets = torch.empty(Tmax + 1, dtype=torch.int32, device=dev)
+    loops = torch.empty(3 * Tmax, dtype=torch.int32, device=dev)
     stream = torch.cuda.Stream(device=dev)
     launches = [0]
 
-    def step():
-        ctx = pp.build_halfedges(xy, tri, wsp, stream)
+    def convert(m):
+        ctx = pp.build_halfedges(m["xy"], m["tri"], wsp, stream)
         pp.label(ctx, stream)
         pp.generate(ctx, stream)
         pp.get_polygons(ctx, offsets, loops, stream=stream)
-        launches[0] = pp.launch_count(ctx)
         return ctx
 
-    # correctness gate + counts
-    ctx = step()
-    counts = pp.get_counts(ctx, stream)
-    pp.destroy(ctx)
-    P, L = counts["n_polygons"], counts["n_loop_entries"]
+    def step():
+        n = 0
+        for m in meshes:
+            ctx = convert(m)
+            n += pp.launch_count(ctx)
+            pp.destroy(ctx)
+        launches[0] = n
+
+    # correctness gate + per-mesh counts (and a checksum of each CSR for cross-rank logs)
+    stats = []
+    for m in meshes:
+        ctx = convert(m)
+        c = pp.get_counts(ctx, stream)
+        pp.destroy(ctx)
+        P, L = c["n_polygons"], c["n_loop_entries"]
+        m["counts"] = c
+        ck = batch.loop_checksum(offsets[:P + 1], loops[:L])
+        stats.append([m.get("meta", {}).get("index", rank), c["n_triangles"], P, L, c["n_tips"], c["n_border"], ck])
+    local_T = sum(m["tri"].shape[0] for m in meshes)
+    local_V = sum(m["xy"].shape[0] for m in meshes)
+    local_P = sum(m["counts"]["n_polygons"] for m in meshes)
+    local_L = sum(m["counts"]["n_loop_entries"] for m in meshes)
 
     for _ in range(args.warmup):
-        pp.destroy(step())
+        step()
     torch.cuda.synchronize(dev)
     if ws > 1:
-        import torch.distributed as dist
         dist.barrier()
     ev0 = torch.cuda.Event(enable_timing=True)
     ev1 = torch.cuda.Event(enable_timing=True)
@@ -276,92 +301,107 @@ def main():
         torch.cuda.synchronize(dev)
         ev0.record(stream)
         for _ in range(args.steps):
-            pp.destroy(step())
+            step()
         ev1.record(stream)
         torch.cuda.synchronize(dev)
     if ws > 1:
         dist.barrier()
-    ms_total = ev0.elapsed_time(ev1)
-    t_max = torch.tensor([ms_total], dtype=torch.float64, device=dev)
-    tris = torch.tensor([float(T)], dtype=torch.float64, device=dev)
+    ms_total = batch.max_time(ev0.elapsed_time(ev1), dev, ws)
+    tot = torch.tensor([float(local_T), float(local_P), float(local_V), float(local_L)], dtype=torch.float64, device=dev)
     if ws > 1:
-        dist.all_reduce(t_max, op=dist.ReduceOp.MAX)
-        dist.all_reduce(tris, op=dist.ReduceOp.SUM)
-    ms_total = float(t_max.item())
+        dist.all_reduce(tot, op=dist.ReduceOp.SUM)
+    all_T, all_P = float(tot[0].item()), float(tot[1].item())
     ms_step = ms_total / args.steps
-    value = float(tris.item()) * args.steps / (ms_total / 1e3)
-    ctx = step()
-    final = pp.get_counts(ctx, stream)
-    pp.destroy(ctx)
-    assert final["status"] == 0 and final["n_polygons"] == P
+    value = all_T * args.steps / (ms_total / 1e3)
+    n_meshes_total = 64 if args.config == 5 else ws
+    table = batch.gather_stats(torch.tensor(stats, dtype=torch.int64, device=dev), n_meshes_total, ws)
+    for m in meshes:  # the counts must not change between runs (determinism)
+        ctx = convert(m)
+        c = pp.get_counts(ctx, stream)
+        pp.destroy(ctx)
+        assert c["status"] == 0 and c["n_polygons"] == m["counts"]["n_polygons"]
 
     # ---- live per-kernel times (CUDA events recorded by the library on `stream`)
     pp.profile_enable(True)
-    prof_steps = max(5, min(args.steps, 50))
+    prof_steps = max(3, min(args.steps, 30 if args.config != 5 else 3))
     for _ in range(prof_steps):
-        pp.destroy(step())
+        step()
     prof = pp.profile_read()
     pp.profile_enable(False)
     per_launch = {k: ms / cnt for k, (ms, cnt) in prof.items()}
     prof_step_ms = sum(ms for ms, _ in prof.values()) / prof_steps
-    ab = alg_bytes(T, V, P, L)
+    nm = len(meshes)
+    # algorithmic bytes per launch (one mesh per launch; meshes of a batch have equal size)
+    ab = alg_bytes(local_T // nm, local_V // nm, local_P // nm, local_L // nm)
     peak, peak_src = load_peaks()
     top = max((k for k in per_launch if k in ab), key=lambda k: per_launch[k])
     achieved = ab[top] / (per_launch[top] * 1e-3) / 1e9
     traffic = ncu_traffic(top, args.config)
     roof = {"bound": "hbm", "kernel": top, "achieved": achieved, "peak": peak, "unit": "GB/s",
             "frac": achieved / peak, "traffic": traffic, "alg_bytes_per_launch": ab[top],
-            "kernel_ms": per_launch[top], "share_of_step": per_launch[top] / prof_step_ms, "peak_source": peak_src}
-    pipe_gbs = ab["pipeline"] / (ms_step * 1e-3) / 1e9
-    pipeline_roof = {"alg_bytes_per_step": ab["pipeline"], "achieved": pipe_gbs, "peak": peak,
+            "kernel_ms": per_launch[top], "share_of_step": per_launch[top] * nm / prof_step_ms,
+            "peak_source": peak_src}
+    pipe_gbs = ab["pipeline"] * nm / (ms_step * 1e-3) / 1e9  # per GPU
+    pipeline_roof = {"alg_bytes_per_step_per_gpu": ab["pipeline"] * nm, "achieved": pipe_gbs, "peak": peak,
                      "frac": pipe_gbs / peak, "frac_of_8TBs_nominal": pipe_gbs / 8000.0}
 
     # ---- end to end through polylla_run_host with pinned host buffers
     e2e = None
-    if not args.no_e2e:
-        xy_h = torch.from_numpy(xy_np).pin_memory()
-        tri_h = torch.from_numpy(tri_np).pin_memory()
-        outs = pp.alloc_host_outputs(T, arrays=True, pin=True)
-        xy_hn, tri_hn = xy_h.numpy(), tri_h.numpy()
-        for _ in range(2):
-            r = pp.run_host(xy_hn, tri_hn, wsp, pinned=outs, stream=stream)
-        torch.cuda.synchronize(dev)
-        if ws > 1:
-            dist.barrier()
-        e0 = torch.cuda.Event(enable_timing=True)
-        e1 = torch.cuda.Event(enable_timing=True)
-        e0.record(stream)
-        for _ in range(args.e2e_steps):
-            r = pp.run_host(xy_hn, tri_hn, wsp, pinned=outs, stream=stream)
-        e1.record(stream)
-        torch.cuda.synchronize(dev)
-        et = torch.tensor([e0.elapsed_time(e1)], dtype=torch.float64, device=dev)
-        if ws > 1:
-            dist.all_reduce(et, op=dist.ReduceOp.MAX)
-        e_ms = float(et.item()) / args.e2e_steps
-        H = r["H"]
-        e2e = {"value": float(tris.item()) / (e_ms / 1e3), "unit": "triangles/s", "ms_per_step": e_ms,
-               "h2d_bytes_per_step": 16 * V + 12 * T, "d2h_bytes_per_step": 4 * (P + 1) + 4 * L + 3 * 4 * H,
+    if not args.no_e2e and all(m.get("host") is not None for m in meshes):
+        outs = pp.alloc_host_outputs(Tmax, arrays=True, pin=True)
+        xy_pin = torch.empty((Vmax, 2), dtype=torch.float64).pin_memory()
+        tri_pin = torch.empty((Tmax, 3), dtype=torch.int32).pin_memory()
+        e_ms, h2d, d2h, n_e2e = 0.0, 0, 0, 0
+        e_steps = max(1, min(args.e2e_steps, 10 if args.config != 5 else 1))
+        for rep in range(e_steps + 1):
+            for m in meshes:
+                xy_h, tri_h = m["host"]()  # untimed: refill the pinned staging buffers
+                V, T = xy_h.shape[0], tri_h.shape[0]
+                xy_pin[:V].numpy()[:] = xy_h
+                tri_pin[:T].numpy()[:] = tri_h
+                torch.cuda.synchronize(dev)
+                e0 = torch.cuda.Event(enable_timing=True)
+                e1 = torch.cuda.Event(enable_timing=True)
+                e0.record(stream)
+                r = pp.run_host(xy_pin[:V].numpy(), tri_pin[:T].numpy(), wsp, pinned=outs, stream=stream)
+                e1.record(stream)
+                torch.cuda.synchronize(dev)
+                if rep > 0:  # rep 0 is the warm-up
+                    e_ms += e0.elapsed_time(e1)
+                    h2d += 16 * V + 12 * T
+                    d2h += 4 * (r["P"] + 1) + 4 * r["L"] + 3 * 4 * r["H"]
+                    n_e2e += 1
+        e_ms = batch.max_time(e_ms, dev, ws)
+        e2e = {"value": all_T * e_steps / (e_ms / 1e3), "unit": "triangles/s", "ms_per_step": e_ms / e_steps,
+               "h2d_bytes_per_step": h2d // e_steps, "d2h_bytes_per_step": d2h // e_steps,
                "api": "polylla_run_host (pinned host in/out; CSR + origin/twin/next returned)"}
 
     cpu = None
     if rank == 0 and ws == 1 and not args.no_cpu_baseline:
-        cpu = cpu_oracle_baseline(xy_np, tri_np)
+        if meshes[0].get("host") is not None:
+            hx, ht = meshes[0]["host"]()
+        else:
+            hx, ht = synth.grid(2000, 0.2, 4)
+        cpu = cpu_oracle_baseline(hx, ht)
 
     if rank == 0:
+        c0 = meshes[0]["counts"]
         out = {
             "metric": METRIC, "value": value, "unit": "triangles/s", "n_gpus": ws, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
+            "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": scaling,
             "vs_baseline": None, "dtype": "f64/i32", "data": "synthetic",
-            "config": {"workload": name, "V": V, "T": T, "P": P, "L": L, "H": counts["n_halfedges"],
-                       "tips": counts["n_tips"], "leftover_halfedges": counts["n_leftover"],
-                       "l2": "no flush: inputs 16V+12T = %.0f MB and working set > 126 MB L2" %
-                             ((16 * V + 12 * T) / 1e6)},
-            "polygons_per_s": P * ws * args.steps / (ms_total / 1e3),
+            "config": {"workload": name, "meshes": n_meshes_total, "T_total": int(all_T), "P_total": int(all_P),
+                       "per_mesh_rank0": {"V": meshes[0]["xy"].shape[0], "T": meshes[0]["tri"].shape[0],
+                                          "P": c0["n_polygons"], "L": c0["n_loop_entries"], "H": c0["n_halfedges"],
+                                          "tips": c0["n_tips"], "leftover_halfedges": c0["n_leftover"]},
+                       "l2": "no flush: per-step inputs and working set exceed the 126 MB L2" if args.config >= 3
+                             else "small working set: L2-resident between steps (reported, not the headline)"},
+            "polygons_per_s": all_P * args.steps / (ms_total / 1e3),
             "roofline": roof, "pipeline_roofline": pipeline_roof,
             "kernels_ms_per_step": {k: ms / prof_steps for k, (ms, _) in prof.items()},
             "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches[0] * args.steps,
             "clocks": clk.summary(),
+            "mesh_table_head": table[:4].tolist(),
         }
         print(json.dumps(out), flush=True)
     if ws > 1:

@@ -154,3 +154,30 @@ def make(kind: str, **kw):
     if kind == "random":
         return random_delaunay(kw["n"], kw["seed"], kw.get("delta"))
     raise ValueError(kind)
+
+
+# --------------------------------------------------------------------------- device generator
+_DEV = None
+
+
+def grid_device(s: int, a: float = 0.0, seed: int = 0, device="cuda", stream=None):
+    """Alg. 13 grid generated on the GPU (synth/csrc/gridgen_dev.cu); bit-identical to grid()."""
+    import torch
+
+    global _DEV
+    if _DEV is None:
+        path = os.path.join(_HERE, "libsynth_dev.so")
+        if not os.path.exists(path):
+            raise RuntimeError(f"{path} missing: run __graft_entry__.build()")
+        _DEV = ctypes.CDLL(path)
+        _DEV.synth_grid_dev.restype = ctypes.c_int
+        _DEV.synth_grid_dev.argtypes = [ctypes.c_int64, ctypes.c_double, ctypes.c_uint64, ctypes.c_void_p,
+                                        ctypes.c_void_p, ctypes.c_void_p]
+    s = int(s)
+    xy = torch.empty((s * s, 2), dtype=torch.float64, device=device)
+    tri = torch.empty((2 * (s - 1) * (s - 1), 3), dtype=torch.int32, device=device)
+    st = (stream or torch.cuda.current_stream(xy.device)).cuda_stream
+    rc = _DEV.synth_grid_dev(s, float(a), int(seed), xy.data_ptr(), tri.data_ptr(), ctypes.c_void_p(st))
+    if rc:
+        raise RuntimeError(f"synth_grid_dev failed ({rc})")
+    return xy, tri
