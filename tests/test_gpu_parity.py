@@ -197,3 +197,105 @@ def test_call_order_and_workspace_errors():
         pp.generate(ctx)
     assert pp.STATUS[ei.value.code] == "CALL_ORDER"
     pp.destroy(ctx)
+
+
+@pytest.mark.slow
+def test_config3_full():
+    """BASELINE config 3 at full size (10M random points, ~20M triangles), the bench
+    workload, in the launch configuration bench.py times: every array bit-exact."""
+    xy, tri = synth.random_delaunay(10_000_000, 3)
+    assert_parity(xy, tri, stages=False, invariants=False)
+
+
+@pytest.mark.slow
+def test_config5_jittered_full():
+    """A config-5 jittered mesh at full size (s = 2000, a = 0.2, seed 1000)."""
+    xy, tri = synth.grid(2000, 0.2, 1000)
+    assert_parity(xy, tri, stages=False, invariants=False)
+
+
+def device_invariants(xy, tri, origin, twin, nxt, offsets, loops, seeds, chunk=1 << 26):
+    """Invariants that hold at any size (north_star / SPEC.md L187-193), evaluated on the
+    device with plain torch ops in chunks (test infrastructure).  Returns P."""
+    T = tri.shape[0]
+    H = origin.numel()
+    dev = origin.device
+    for a in range(0, H, chunk):
+        b = min(H, a + chunk)
+        ids = torch.arange(a, b, device=dev)
+        tw = twin[a:b].long()
+        assert torch.equal(twin[tw].long(), ids) and not torch.any(tw == ids)   # twin involution
+        assert torch.equal(origin[nxt[a:b].long()], origin[tw])                 # origin(next e) = target(e)
+    P = seeds.numel()
+    off = offsets.long()
+    assert int(off[0]) == 0 and int(off[-1]) == loops.numel() and bool(torch.all(off[1:] > off[:-1]))
+    assert bool(torch.all(seeds[1:] > seeds[:-1])) and bool(torch.all(seeds < 3 * T))
+    poly_area = 0.0
+    xyd = xy.double()
+    for a in range(0, P, chunk):
+        b = min(P, a + chunk)
+        sd = seeds[a:b].long()
+        o0, o1 = off[a:b], off[a + 1:b + 1]
+        lens = o1 - o0
+        assert torch.equal(loops[o0].long(), origin[sd].long())                 # loops start at origin[seed]
+        # lock-step walk of the loops: each closes after exactly its length, never meets
+        # next == twin, and never visits a half-edge below its seed (canonical = min)
+        x = sd.clone()
+        px = xyd[origin[x].long()]
+        first = px.clone()
+        area = torch.zeros(b - a, dtype=torch.float64, device=dev)
+        for i in range(int(lens.max())):
+            live = lens > i
+            xi = x[live]
+            assert torch.equal(origin[xi].long(), loops[o0[live] + i].long())
+            assert not torch.any(nxt[xi] == twin[xi])
+            assert bool(torch.all(xi >= sd[live]))
+            x[live] = nxt[xi].long()
+            cur = px[live]
+            nx_pt = torch.where((lens[live] > i + 1).unsqueeze(1), xyd[origin[x[live]].long()], first[live])
+            area[live] += cur[:, 0] * nx_pt[:, 1] - nx_pt[:, 0] * cur[:, 1]
+            px[live] = nx_pt
+        assert torch.equal(x, sd)
+        poly_area += 0.5 * float(area.sum())
+    tri_area = 0.0
+    for a in range(0, T, chunk):
+        p = xyd[tri[a:a + chunk].long()]
+        tri_area += 0.5 * float(((p[:, 1, 0] - p[:, 0, 0]) * (p[:, 2, 1] - p[:, 0, 1]) -
+                                 (p[:, 1, 1] - p[:, 0, 1]) * (p[:, 2, 0] - p[:, 0, 0])).abs().sum())
+    assert abs(poly_area - tri_area) <= 1e-9 * tri_area, (poly_area, tri_area)
+    return P
+
+
+@pytest.mark.slow
+def test_config4_capacity_invariants():
+    """BASELINE config 4 (256M vertices, 512M triangles, H = 1,535,872,002 < 2^31): the
+    oracle cannot run at this size on the box, so the properties that hold at any size
+    are checked on the device, reading the arrays in place in the workspace."""
+    pp = _pp()
+    xy, tri = synth.grid_device(16000, 0.2, 4)
+    T = tri.shape[0]
+    ws = pp.alloc_workspace(xy.shape[0], T)
+    ctx = pp.build_halfedges(xy, tri, ws)
+    pp.label(ctx)
+    pp.generate(ctx)
+    c = pp.get_counts(ctx)
+    H, P, L = c["n_halfedges"], c["n_polygons"], c["n_loop_entries"]
+    assert H == 1_535_872_002 and c["n_border"] == 4 * 15999
+    offsets = torch.empty(T + 1, dtype=torch.int32, device="cuda")
+    loops = torch.empty(3 * T, dtype=torch.int32, device="cuda")
+    pp.get_polygons(ctx, offsets, loops)
+    pp.get_counts(ctx)
+    v = pp.get_views(ctx)
+    view = lambda k, n: pp.view_tensor(ctx, v[k], n, torch.int32)  # noqa: E731
+    got = device_invariants(xy, tri, view("origin", H), view("twin", H), view("next", H), offsets[:P + 1],
+                            loops[:L], view("seeds", P))
+    assert got == P
+    pp.destroy(ctx)
+
+
+def test_device_invariants_on_random_mesh():
+    xy, tri = synth.random_delaunay(100_000, 21)
+    res = gpu_run(xy, tri)
+    P = device_invariants(torch.from_numpy(xy).cuda(), torch.from_numpy(tri).cuda(), res["origin"], res["twin"],
+                          res["next"], res["offsets"], res["loops"], res["seeds"], chunk=1 << 14)
+    assert P == res["P"]
