@@ -262,35 +262,46 @@ __global__ void __launch_bounds__(kTileThreads, 2)
   PHASE_MARK(1);
 
   // ---- P2a: the lo->hi halves claim their home slot with a plain store (last writer wins) ...
+  // (one thread per triangle: its three half-edges (a,b), (b,c), (c,a) with q = 4t + k)
   uint32_t nm = 0;
-  for (int j = tid; j < nhe; j += kTileThreads) {
-    const int32_t o = tri_s[j], tg = tri_s[next_local(j)];
-    if (o < tg) {
-      const uint32_t h = tile_hash((uint32_t)o, (uint32_t)tg);
-      slot[h & (kTileSlots - 1)] = (h & ~kSlotQ) | (uint32_t)q_of(j);
+  for (int t = tid; t < nt; t += kTileThreads) {
+    const int32_t v[3] = {tri_s[3 * t], tri_s[3 * t + 1], tri_s[3 * t + 2]};
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+      const int32_t o = v[k], tg = v[(k + 1) % 3];
+      if (o < tg) {
+        const uint32_t h = tile_hash((uint32_t)o, (uint32_t)tg);
+        slot[h & (kTileSlots - 1)] = (h & ~kSlotQ) | (uint32_t)(4 * t + k);
+      }
     }
   }
   __syncthreads();
   // ... the losers of a home slot insert with CAS + linear probing from there
-  for (int j = tid; j < nhe; j += kTileThreads) {
-    const int32_t o = tri_s[j], tg = tri_s[next_local(j)];
-    if (o < tg) {
-      const uint32_t h = tile_hash((uint32_t)o, (uint32_t)tg);
-      const int32_t q = q_of(j);
-      if (slot[h & (kTileSlots - 1)] != ((h & ~kSlotQ) | (uint32_t)q))
-        nm |= tile_insert(slot, tri_s, q, (uint32_t)o, (uint32_t)tg);
+  for (int t = tid; t < nt; t += kTileThreads) {
+    const int32_t v[3] = {tri_s[3 * t], tri_s[3 * t + 1], tri_s[3 * t + 2]};
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+      const int32_t o = v[k], tg = v[(k + 1) % 3];
+      if (o < tg) {
+        const uint32_t h = tile_hash((uint32_t)o, (uint32_t)tg);
+        const uint32_t mine = (h & ~kSlotQ) | (uint32_t)(4 * t + k);
+        if (slot[h & (kTileSlots - 1)] != mine) nm |= tile_insert(slot, tri_s, 4 * t + k, (uint32_t)o, (uint32_t)tg);
+      }
     }
   }
   __syncthreads();
   // ---- P2b: the hi->lo halves find their twin (read-only probes)
-  for (int j = tid; j < nhe; j += kTileThreads) {
-    const int32_t o = tri_s[j], tg = tri_s[next_local(j)];
-    if (o > tg) {
-      const int32_t sq = tile_lookup(slot, tri_s, (uint32_t)tg, (uint32_t)o);
-      if (sq >= 0) {
-        const int32_t q = q_of(j);
-        tw_s[q] = (int16_t)sq;
-        tw_s[sq] = (int16_t)q;
+  for (int t = tid; t < nt; t += kTileThreads) {
+    const int32_t v[3] = {tri_s[3 * t], tri_s[3 * t + 1], tri_s[3 * t + 2]};
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+      const int32_t o = v[k], tg = v[(k + 1) % 3];
+      if (o > tg) {
+        const int32_t sq = tile_lookup(slot, tri_s, (uint32_t)tg, (uint32_t)o);
+        if (sq >= 0) {
+          tw_s[4 * t + k] = (int16_t)sq;
+          tw_s[sq] = (int16_t)(4 * t + k);
+        }
       }
     }
   }
