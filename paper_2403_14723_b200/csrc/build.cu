@@ -33,9 +33,10 @@ constexpr int kTileWords = kTileHE / 32; // 192
 //   tw_s  int16[kTileQ]  16384   twin as a quad index, -1 = outside the tile
 //   slot  u32[kTileSlots] 32768  (dead after P2: reused for succ u16[kTileQ] | Lm, Dm, Tm, SDm u32[192] | scan scratch)
 //   lc_s  u8[kTileTris]   2048
-//   nx_l  int16[kTileHE] 12288 | Sw, Cw u32[192] 1536 | slist int16[kTileTris] 4096   (P4-P6)
+//   nx_l  int16[kTileHE] 12288 | Sw, Cw, Wl u32[192] 2304 | slist int16[kTileTris] 4096   (P4-P6)
 constexpr size_t kOffTw = kTileHE * 4, kOffSlot = kOffTw + kTileQ * 2, kOffLc = kOffSlot + kTileSlots * 4,
-                 kOffNx = kOffLc + kTileTris, kTileSmem = kOffNx + kTileHE * 2 + kTileHE / 4 + kTileTris * 2;  // 93,696 B -> 2 CTAs/SM
+                 kOffNx = kOffLc + kTileTris,
+                 kTileSmem = kOffNx + kTileHE * 2 + 3 * (kTileHE / 8) + kTileTris * 2;  // 94,464 B -> 2 CTAs/SM
 constexpr uint32_t kSlotQ = (1u << 13) - 1;       // slot = fingerprint(19 bits) << 13 | quad index
 // rotation successors (P3/P4): quad index in the low 13 bits, terminal flags above
 constexpr uint16_t kSuccIdx = 0x1FFF, kSuccFront = 0x4000, kSuccUnknown = 0x8000;
@@ -179,7 +180,7 @@ __global__ void __launch_bounds__(kTileThreads, 2)
     k_tile(const double2* __restrict__ xy, const int32_t* __restrict__ tri, int64_t V, int64_t T,
            int32_t* __restrict__ origin, int32_t* __restrict__ twin, int32_t* __restrict__ next,
            uint8_t* __restrict__ lcode, uint32_t* __restrict__ F0, uint32_t* __restrict__ F1,
-           uint32_t* __restrict__ S, uint32_t* __restrict__ C, int32_t* __restrict__ len,
+           uint32_t* __restrict__ S, uint32_t* __restrict__ C, int32_t* __restrict__ len, int32_t* __restrict__ wlen,
            unsigned long long* __restrict__ left_key, int32_t* __restrict__ left_e, int32_t* __restrict__ def_e,
            int32_t* __restrict__ tips, int32_t* __restrict__ sdef, DevCounters* ctr) {
   extern __shared__ __align__(16) unsigned char smem_tile[];
@@ -190,7 +191,8 @@ __global__ void __launch_bounds__(kTileThreads, 2)
   int16_t* nx_l = reinterpret_cast<int16_t*>(smem_tile + kOffNx);               // local next, -1: not walkable
   uint32_t* Sw = reinterpret_cast<uint32_t*>(smem_tile + kOffNx + kTileHE * 2);  // seed bits (e order)
   uint32_t* Cw = Sw + kTileWords;                                                // canonical seed bits
-  int16_t* slist = reinterpret_cast<int16_t*>(Cw + kTileWords);                 // compacted seeds
+  int32_t* Wl = reinterpret_cast<int32_t*>(Cw + kTileWords);                     // loop lengths per C word
+  int16_t* slist = reinterpret_cast<int16_t*>(Wl + kTileWords);                 // compacted seeds
   // overlays of the slot area (after P2)
   uint16_t* succ = reinterpret_cast<uint16_t*>(slot);
   uint32_t* Lm = slot + kTileQ / 2;
@@ -391,6 +393,7 @@ __global__ void __launch_bounds__(kTileThreads, 2)
       Tm[wbase >> 5] = tm;
       Sw[wbase >> 5] = sw;
       Cw[wbase >> 5] = 0u;
+      Wl[wbase >> 5] = 0;
       SDm[wbase >> 5] = 0u;
     }
   }
@@ -430,15 +433,19 @@ __global__ void __launch_bounds__(kTileThreads, 2)
         } while (y != x);
       }
       if (ok) {
-        atomicOr(&Cw[mn >> 5], 1u << (mn & 31));
         len[e0 + mn] = n;
+        const uint32_t bit = 1u << (mn & 31);
+        if (!(atomicOr(&Cw[mn >> 5], bit) & bit)) atomicAdd(&Wl[mn >> 5], n);  // first setter only
       } else {
         atomicOr(&SDm[sj >> 5], 1u << (sj & 31));
       }
     }
   }
   __syncthreads();
-  for (int w = tid; w * 32 < nhe; w += kTileThreads) C[(e0 >> 5) + w] = Cw[w];
+  for (int w = tid; w * 32 < nhe; w += kTileThreads) {
+    C[(e0 >> 5) + w] = Cw[w];
+    wlen[(e0 >> 5) + w] = Wl[w];
+  }
   PHASE_MARK(6);
 
   // ---- P5: one global atomic per list per tile, then write the entries
@@ -563,6 +570,7 @@ struct BorderOp {
   __device__ bool skip() const { return ctr->status != 0; }
   __device__ uint32_t word(int64_t w) const { return Bd[w]; }
   __device__ long long aux(int32_t) const { return 0; }
+  __device__ long long word_aux(int64_t, uint32_t) const { return 0; }
   __device__ long long extra(int64_t) const { return 0; }
   __device__ void finish(long long cnt, long long, long long) const {
     if (T3 + cnt > 0x7fffffffLL) raise_status(ctr, ST_OVERFLOW);
@@ -622,7 +630,7 @@ int launch_build(Ctx* c, cudaStream_t s) {
   prof_mark(s, "k_tile");
   k_tile<<<(unsigned)tiles, kTileThreads, kTileSmem, s>>>(reinterpret_cast<const double2*>(c->xy), c->tri, c->V, c->T,
                                                           c->origin, c->twin, c->next, c->lcode, c->F0, c->F1, c->S,
-                                                          c->C, c->len, c->left_key, c->left_e, c->def_e, c->tips,
+                                                          c->C, c->len, c->wlen, c->left_key, c->left_e, c->def_e, c->tips,
                                                           c->sdef, c->ctr);
   ++n;
   const int grid = 148 * 8;

@@ -61,6 +61,7 @@ static Layout layout(int64_t V, int64_t T) {
       sizeof(DevCounters),    // 26 counters
       (size_t)(3 * T) * 4,    // 27 deferred half-edges
       (size_t)(T + 1) * 4,    // 28 deferred seeds
+      (size_t)nw * 4,         // 29 per-word loop lengths
   };
   Layout L{};
   size_t o = 0;
@@ -109,6 +110,7 @@ bool carve(Ctx* c, void* ws, size_t bytes) {
   c->ctr = reinterpret_cast<DevCounters*>(b + L.off[26]);
   c->def_e = reinterpret_cast<int32_t*>(b + L.off[27]);
   c->sdef = reinterpret_cast<int32_t*>(b + L.off[28]);
+  c->wlen = reinterpret_cast<int32_t*>(b + L.off[29]);
   c->n_words = (3 * c->T + 31) / 32;
   return true;
 }

@@ -82,7 +82,7 @@ constexpr int kSeedThreads = 256;
 
 __device__ __forceinline__ void process_seed(int32_t s, int64_t T3, int64_t H, const int32_t* __restrict__ twin,
                                              const int32_t* __restrict__ next, const uint32_t* __restrict__ F1,
-                                             uint32_t* C, int32_t* len, DevCounters* ctr) {
+                                             uint32_t* C, int32_t* len, int32_t* wlen, DevCounters* ctr) {
   int32_t x = s;
   int steps = 0;
   while (!f1_of(F1, T3, x)) {  // Alg. 12: rotate (sweep_out) to a frontier half-edge
@@ -96,8 +96,9 @@ __device__ __forceinline__ void process_seed(int32_t s, int64_t T3, int64_t H, c
     y = next[y];
     if (++n > H) { raise_status(ctr, ST_WALK); return; }
   } while (y != x);
-  atomicOr(&C[mn >> 5], 1u << (mn & 31));
   len[mn] = (int32_t)n;
+  const uint32_t bit = 1u << (mn & 31);
+  if (!(atomicOr(&C[mn >> 5], bit) & bit)) atomicAdd(&wlen[mn >> 5], (int32_t)n);  // first setter only
 }
 
 // the seeds k_tile could not close inside their tile, plus both halves of every middle
@@ -105,25 +106,27 @@ __device__ __forceinline__ void process_seed(int32_t s, int64_t T3, int64_t H, c
 __global__ void __launch_bounds__(kSeedThreads)
     k_seed_walk(int64_t T, const int32_t* __restrict__ twin, const int32_t* __restrict__ next,
                 const uint32_t* __restrict__ F1, const int32_t* __restrict__ sdef, const int32_t* __restrict__ mids,
-                uint32_t* C, int32_t* len, DevCounters* ctr) {
+                uint32_t* C, int32_t* len, int32_t* wlen, DevCounters* ctr) {
   if (ctr->status) return;
   const int64_t T3 = 3 * T;
   const int64_t H = T3 + ctr->n_border;
   const int32_t ns = ctr->n_sdef, nm = 2 * ctr->n_tips;
   for (int32_t j = blockIdx.x * kSeedThreads + threadIdx.x; j < ns + nm; j += gridDim.x * kSeedThreads)
-    process_seed(j < ns ? sdef[j] : mids[j - ns], T3, H, twin, next, F1, C, len, ctr);
+    process_seed(j < ns ? sdef[j] : mids[j - ns], T3, H, twin, next, F1, C, len, wlen, ctr);
 }
 
 struct CanonOp {
   const uint32_t* C;
   const uint32_t* F1;
   const int32_t* len;
+  const int32_t* wlen;
   int32_t* seeds;
   int32_t* offsets;
   DevCounters* ctr;
   __device__ bool skip() const { return ctr->status != 0; }
   __device__ uint32_t word(int64_t w) const { return C[w]; }
   __device__ long long aux(int32_t e) const { return len[e]; }
+  __device__ long long word_aux(int64_t w, uint32_t) const { return wlen[w]; }  // dense per-word sums
   __device__ long long extra(int64_t w) const { return __popc(F1[w]); }
   __device__ void finish(long long P, long long L, long long nf1) const {
     ctr->P = (int32_t)P;
@@ -147,10 +150,10 @@ int launch_generate(Ctx* c, cudaStream_t s) {
   prof_mark(s, "k_seed_walk");
   // (the canonical bit-vector C was written in full by k_tile; global walks OR into it)
   k_seed_walk<<<148 * 8, kSeedThreads, 0, s>>>(c->T, c->twin, c->next, c->F1, c->sdef, c->mids, c->C, c->len,
-                                               c->ctr);
+                                               c->wlen, c->ctr);
   n += 3;
   prof_mark(s, "k_canon_scan");
-  CanonOp op{c->C, c->F1, c->len, c->seeds, c->offsets, c->ctr};
+  CanonOp op{c->C, c->F1, c->len, c->wlen, c->seeds, c->offsets, c->ctr};
   const int r = launch_scan(op, c->n_words, c->scan_a, c->scan_b, c->scan_c, s);
   if (r < 0) return -1;
   n += r;

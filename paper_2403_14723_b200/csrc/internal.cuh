@@ -56,6 +56,7 @@ struct Ctx {
   uint8_t* lcode;
   uint32_t *F0, *F1, *S, *C, *Bd;
   int32_t* len;
+  int32_t* wlen;    // [n_words] sum of loop lengths of the canonical seeds of each C word
   unsigned long long* left_key;
   int32_t* left_e;
   int32_t* def_e;   // [3T] half-edges deferred by k_tile

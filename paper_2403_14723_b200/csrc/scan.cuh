@@ -1,7 +1,7 @@
 // scan.cuh -- order-preserving compaction of a bit-vector ("scan and
 // compact seed edges array"), reduce-then-scan in three launches:
-//   1. k_scan_reduce : per block of kScanWords words, (#set bits, sum of aux over set
-//                      bits, extra per-word sum) -> 3 block sums;
+//   1. k_scan_reduce : per block of kScanWords words, (#set bits, Op::word_aux = dense
+//                      per-word sum of aux, extra per-word sum) -> 3 block sums;
 //   2. k_scan_top    : one block, exclusive scan of the block sums, totals to Op::finish;
 //   3. k_scan_down   : per block, the rank and aux-prefix of every set bit -> Op::emit.
 // Ranks follow ascending bit position, so the output is deterministic.  The paper
@@ -67,12 +67,8 @@ __global__ void __launch_bounds__(kScanThreads) k_scan_reduce(Op op, int64_t n_w
     if (w < n_words) {
       uint32_t bits = op.word(w);
       v.a += __popc(bits);
+      v.b += op.word_aux(w, bits);  // sum of aux over the set bits of word w
       v.c += op.extra(w);
-      while (bits) {
-        const int b = __ffs(bits) - 1;
-        bits &= bits - 1;
-        v.b += op.aux((int32_t)(w * 32 + b));
-      }
     }
   }
   Sum3 tot;
@@ -109,12 +105,7 @@ __global__ void __launch_bounds__(kScanThreads) k_scan_down(Op op, int64_t n_wor
     const int64_t w = w0 + i;
     bits[i] = w < n_words ? op.word(w) : 0u;
     v.a += __popc(bits[i]);
-    uint32_t b = bits[i];
-    while (b) {
-      const int k = __ffs(b) - 1;
-      b &= b - 1;
-      v.b += op.aux((int32_t)(w * 32 + k));
-    }
+    if (bits[i]) v.b += op.word_aux(w, bits[i]);
   }
   Sum3 tot;
   Sum3 ex = block_excl_scan(v, &tot);
