@@ -393,7 +393,9 @@ def main():
             "config": {"workload": name, "meshes": n_meshes_total, "T_total": int(all_T), "P_total": int(all_P),
                        "per_mesh_rank0": {"V": meshes[0]["xy"].shape[0], "T": meshes[0]["tri"].shape[0],
                                           "P": c0["n_polygons"], "L": c0["n_loop_entries"], "H": c0["n_halfedges"],
-                                          "tips": c0["n_tips"], "leftover_halfedges": c0["n_leftover"]},
+                                          "tips": c0["n_tips"], "leftover_halfedges": c0["n_leftover"],
+                                          "deferred_halfedges": c0["n_deferred"],
+                                          "deferred_seeds": c0["n_seed_deferred"]},
                        "l2": "no flush: per-step inputs and working set exceed the 126 MB L2" if args.config >= 3
                              else "small working set: L2-resident between steps (reported, not the headline)"},
             "polygons_per_s": all_P * args.steps / (ms_total / 1e3),

@@ -252,6 +252,8 @@ POLYLLA_API polylla_status polylla_get_counts(polylla_ctx* p, polylla_stream str
   r.n_tips = h.n_tips;
   r.n_flips = h.n_flips;
   r.n_leftover = h.n_left;
+  r.n_deferred = h.n_def;
+  r.n_seed_deferred = h.n_sdef;
   r.status = (int32_t)map_status(h.status);
   c->host_counts = r;
   if (c->stage == 3) c->stage = 4;

@@ -41,7 +41,8 @@ class PolyllaError(RuntimeError):
 class Counts(ctypes.Structure):
     _fields_ = [(n, ctypes.c_int64) for n in (
         "n_vertices", "n_triangles", "n_halfedges", "n_border", "n_polygons", "n_loop_entries",
-        "n_tips", "n_flips", "n_leftover")] + [("status", ctypes.c_int32), ("reserved", ctypes.c_int32)]
+        "n_tips", "n_flips", "n_leftover", "n_deferred", "n_seed_deferred")] + [("status", ctypes.c_int32),
+                                                                               ("reserved", ctypes.c_int32)]
 
     def as_dict(self):
         return {k: int(getattr(self, k)) for k, _ in self._fields_ if k != "reserved"}
