@@ -633,7 +633,7 @@ int launch_build(Ctx* c, cudaStream_t s) {
                                                           c->C, c->len, c->wlen, c->left_key, c->left_e, c->def_e, c->tips,
                                                           c->sdef, c->ctr);
   ++n;
-  const int grid = 148 * 8;
+  const int grid = 148 * 32;  // enough threads for ~1 leftover each on 10M-vertex meshes (latency-bound)
   prof_mark(s, "k_left_match");
   k_hash_clear<<<grid, 256, 0, s>>>(c->ctr, c->ehash, c->vkey, c->hash_cap_max);
   k_left_insert<<<grid, 256, 0, s>>>(c->ctr, c->left_key, c->left_e, c->origin, c->twin, c->ehash);

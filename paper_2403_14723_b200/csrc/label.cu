@@ -35,7 +35,7 @@ __global__ void __launch_bounds__(kLabelThreads)
   const int lane = threadIdx.x & 31;
   for (int32_t base = blockIdx.x * kLabelThreads; base < n; base += gridDim.x * kLabelThreads) {
     const int32_t i = base + threadIdx.x;
-    bool tip = false, walk_err = false, sd = false;
+    bool tip = false, walk_err = false, sd = false, fr = false;
     int32_t e = -1;
     if (i < n) {
       e = def_e[i];
@@ -43,7 +43,7 @@ __global__ void __launch_bounds__(kLabelThreads)
       const bool tb = t >= T3;
       const bool Le = is_longest(lcode, e);
       const bool Lt = !tb && is_longest(lcode, t);
-      const bool fr = tb || (!Le && !Lt);
+      fr = tb || (!Le && !Lt);
       sd = Le && (tb || (Lt && e < t));
       int32_t nx = next_in(e);
       if (fr) {
@@ -57,11 +57,19 @@ __global__ void __launch_bounds__(kLabelThreads)
         }
         nx = x;
         tip = (x == t);
-        atomicOr(&F0[e >> 5], 1u << (e & 31));
-        atomicOr(&F1[e >> 5], 1u << (e & 31));
       }
-      if (sd) atomicOr(&S[e >> 5], 1u << (e & 31));
       next[e] = nx;
+    }
+    // bit-vector words: deferred entries are appended in ascending order per tile, so
+    // neighbouring lanes usually share a word -> one atomicOr per distinct word
+    const uint32_t word = e >= 0 ? (uint32_t)(e >> 5) : 0xFFFFFFFFu;
+    const uint32_t peers = __match_any_sync(0xffffffffu, word);
+    const uint32_t bit = e >= 0 ? 1u << (e & 31) : 0u;
+    const uint32_t fbits = __reduce_or_sync(peers, fr ? bit : 0u);
+    const uint32_t sbits = __reduce_or_sync(peers, sd ? bit : 0u);
+    if (e >= 0 && lane == __ffs(peers) - 1) {
+      if (fbits) { atomicOr(&F0[word], fbits); atomicOr(&F1[word], fbits); }
+      if (sbits) atomicOr(&S[word], sbits);
     }
     const uint32_t tm = __ballot_sync(0xffffffffu, tip);
     if (tm) {
