@@ -53,6 +53,7 @@ def parse():
     ap.add_argument("--e2e-steps", type=int, default=10)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-graph", action="store_true", help="launch the C-ABI calls eagerly instead of a CUDA graph")
     return ap.parse_args()
 
 
@@ -267,13 +268,15 @@ def main():
         pp.get_polygons(ctx, offsets, loops, stream=stream)
         return ctx
 
-    def step():
+    def step_eager():
         n = 0
         for m in meshes:
             ctx = convert(m)
             n += pp.launch_count(ctx)
             pp.destroy(ctx)
         launches[0] = n
+
+    step = step_eager
 
     # correctness gate + per-mesh counts (and a checksum of each CSR for cross-rank logs)
     stats = []
@@ -289,6 +292,16 @@ def main():
     local_V = sum(m["xy"].shape[0] for m in meshes)
     local_P = sum(m["counts"]["n_polygons"] for m in meshes)
     local_L = sum(m["counts"]["n_loop_entries"] for m in meshes)
+
+    graphs = None
+    if not args.no_graph and len(meshes) == 1:
+        # the whole step as one CUDA graph launch (same kernels, same stream order)
+        graphs = [pp.GraphStep(m["xy"], m["tri"], wsp, offsets, loops, stream) for m in meshes]
+
+        def step():
+            for g in graphs:
+                g.replay()
+            launches[0] = sum(g.launches for g in graphs)
 
     for _ in range(args.warmup):
         step()
@@ -321,11 +334,12 @@ def main():
         pp.destroy(ctx)
         assert c["status"] == 0 and c["n_polygons"] == m["counts"]["n_polygons"]
 
-    # ---- live per-kernel times (CUDA events recorded by the library on `stream`)
+    # ---- live per-kernel times (CUDA events recorded by the library on `stream`; eager
+    # launches, since events cannot be recorded from inside a replayed graph)
     pp.profile_enable(True)
     prof_steps = max(3, min(args.steps, 30 if args.config != 5 else 3))
     for _ in range(prof_steps):
-        step()
+        step_eager()
     prof = pp.profile_read()
     pp.profile_enable(False)
     per_launch = {k: ms / cnt for k, (ms, cnt) in prof.items()}
@@ -402,6 +416,7 @@ def main():
             "roofline": roof, "pipeline_roofline": pipeline_roof,
             "kernels_ms_per_step": {k: ms / prof_steps for k, (ms, _) in prof.items()},
             "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches[0] * args.steps,
+            "launch_mode": "cuda_graph (one graph launch per step)" if graphs else "eager",
             "clocks": clk.summary(),
             "mesh_table_head": table[:4].tolist(),
         }

@@ -296,3 +296,36 @@ def alloc_host_outputs(T: int, arrays=True, pin=True) -> dict:
         for k in ("origin", "twin", "next"):
             d[k] = mk(6 * T)
     return d
+
+
+class GraphStep:
+    """One whole conversion (build -> label -> generate -> CSR) captured as a CUDA graph on
+    a fixed workspace/inputs/outputs and replayed with a single launch: the ~20 kernel
+    launches of a step become one graph launch (the small configs are launch-bound).
+    The C ABI is called unchanged during capture; its kernels read the mesh size from the
+    workspace counters on the device, so a replay recomputes everything."""
+
+    def __init__(self, xy, tri, workspace, offsets, loops, stream=None):
+        self.stream = stream or torch.cuda.Stream(device=xy.device)
+        self.args = (xy, tri, workspace, offsets, loops)
+        # warm once outside capture (lazy CUDA attribute setup inside the library)
+        with torch.cuda.stream(self.stream):
+            ctx = build_halfedges(xy, tri, workspace, self.stream)
+            label(ctx, self.stream)
+            generate(ctx, self.stream)
+            get_polygons(ctx, offsets, loops, stream=self.stream)
+            self.launches = launch_count(ctx)
+            destroy(ctx)
+        self.stream.synchronize()
+        self.graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(self.graph, stream=self.stream):
+            s = torch.cuda.current_stream()
+            ctx = build_halfedges(xy, tri, workspace, s)
+            label(ctx, s)
+            generate(ctx, s)
+            get_polygons(ctx, offsets, loops, stream=s)
+            destroy(ctx)
+
+    def replay(self):
+        with torch.cuda.stream(self.stream):
+            self.graph.replay()

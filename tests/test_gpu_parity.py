@@ -299,3 +299,22 @@ def test_device_invariants_on_random_mesh():
     P = device_invariants(torch.from_numpy(xy).cuda(), torch.from_numpy(tri).cuda(), res["origin"], res["twin"],
                           res["next"], res["offsets"], res["loops"], res["seeds"], chunk=1 << 14)
     assert P == res["P"]
+
+
+def test_cuda_graph_replay_matches_eager():
+    pp = _pp()
+    xy, tri = synth.random_delaunay(50_000, 31)
+    xd, td = torch.from_numpy(xy).cuda(), torch.from_numpy(tri).cuda()
+    ref = gpu_run(xy, tri)
+    T = tri.shape[0]
+    ws = pp.alloc_workspace(xy.shape[0], T)
+    offsets = torch.empty(T + 1, dtype=torch.int32, device="cuda")
+    loops = torch.empty(3 * T, dtype=torch.int32, device="cuda")
+    g = pp.GraphStep(xd, td, ws, offsets, loops)
+    for _ in range(3):
+        offsets.fill_(-1)
+        loops.fill_(-1)
+        g.replay()
+        g.stream.synchronize()
+        P, L = ref["P"], ref["L"]
+        assert torch.equal(offsets[:P + 1], ref["offsets"]) and torch.equal(loops[:L], ref["loops"])
