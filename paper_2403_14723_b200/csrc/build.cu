@@ -121,14 +121,19 @@ __device__ __forceinline__ int4 block_scan4(int4 v, int4* tot, int* sm /* [4 * 3
 // Tile hash on the undirected key (lo, hi), linear probing over uint32 slots holding
 // fingerprint(19 bits) << 13 | q.  The half-edges with origin < target insert their key,
 // those with origin > target look it up (read-only).
-__device__ __forceinline__ uint32_t tile_hash(uint32_t lo, uint32_t hi) { return mix32(lo, hi); }
+// two multiplies: the high bits of the final product are well mixed; they give the slot
+// (position = top 13 bits via tile_pos) and the fingerprint (bits 13..31)
+__device__ __forceinline__ uint32_t tile_hash(uint32_t lo, uint32_t hi) {
+  return ((lo * 0x9E3779B1u) ^ hi) * 0x85EBCA6Bu;
+}
+__device__ __forceinline__ uint32_t tile_pos(uint32_t h) { return h >> (32 - 13); }
 
 __device__ __forceinline__ uint32_t tile_insert(uint32_t* slot, const int32_t* tri_s, int32_t q, uint32_t lo,
                                                 uint32_t hi) {
   const uint32_t h = tile_hash(lo, hi);
   const uint32_t fp = h & ~kSlotQ;
   const uint32_t mine = fp | (uint32_t)q;
-  uint32_t p = h & (kTileSlots - 1);
+  uint32_t p = tile_pos(h);
   for (int probe = 0; probe < kTileSlots; ++probe, p = (p + 1) & (kTileSlots - 1)) {
     uint32_t w = slot[p];
     if (w == kEmpty) {
@@ -148,7 +153,7 @@ __device__ __forceinline__ uint32_t tile_insert(uint32_t* slot, const int32_t* t
 __device__ __forceinline__ int32_t tile_lookup(const uint32_t* slot, const int32_t* tri_s, uint32_t lo, uint32_t hi) {
   const uint32_t h = tile_hash(lo, hi);
   const uint32_t fp = h & ~kSlotQ;
-  uint32_t p = h & (kTileSlots - 1);
+  uint32_t p = tile_pos(h);
   for (int probe = 0; probe < kTileSlots; ++probe, p = (p + 1) & (kTileSlots - 1)) {
     const uint32_t w = slot[p];
     if (w == kEmpty) return -1;
@@ -273,7 +278,7 @@ __global__ void __launch_bounds__(kTileThreads, 2)
       const int32_t o = v[k], tg = v[(k + 1) % 3];
       if (o < tg) {
         const uint32_t h = tile_hash((uint32_t)o, (uint32_t)tg);
-        slot[h & (kTileSlots - 1)] = (h & ~kSlotQ) | (uint32_t)(4 * t + k);
+        slot[tile_pos(h)] = (h & ~kSlotQ) | (uint32_t)(4 * t + k);
       }
     }
   }
@@ -287,7 +292,7 @@ __global__ void __launch_bounds__(kTileThreads, 2)
       if (o < tg) {
         const uint32_t h = tile_hash((uint32_t)o, (uint32_t)tg);
         const uint32_t mine = (h & ~kSlotQ) | (uint32_t)(4 * t + k);
-        if (slot[h & (kTileSlots - 1)] != mine) nm |= tile_insert(slot, tri_s, 4 * t + k, (uint32_t)o, (uint32_t)tg);
+        if (slot[tile_pos(h)] != mine) nm |= tile_insert(slot, tri_s, 4 * t + k, (uint32_t)o, (uint32_t)tg);
       }
     }
   }
