@@ -66,6 +66,18 @@ __device__ __forceinline__ int32_t j_of(int32_t q) { return 3 * (q >> 2) + (q & 
 __device__ __forceinline__ int32_t next_q(int32_t q) { return (q & 3) == 2 ? q - 2 : q + 1; }
 __device__ __forceinline__ bool bit_s(const uint32_t* w, int32_t i) { return (w[i >> 5] >> (i & 31)) & 1u; }
 
+// Relaxed CTA-scope atomic load/store on shared memory (plain LDS/STS in SASS): the hash
+// slot claim is last-writer-wins by design and is read while collision losers CAS, so
+// these accesses are atomics in the memory model rather than data races.
+__device__ __forceinline__ void st_relaxed(uint32_t* p, uint32_t v) {
+  asm volatile("st.relaxed.cta.shared.u32 [%0], %1;" ::"r"((uint32_t)__cvta_generic_to_shared(p)), "r"(v));
+}
+__device__ __forceinline__ uint32_t ld_relaxed(const uint32_t* p) {
+  uint32_t v;
+  asm volatile("ld.relaxed.cta.shared.u32 %0, [%1];" : "=r"(v) : "r"((uint32_t)__cvta_generic_to_shared(p)));
+  return v;
+}
+
 __device__ __forceinline__ double sq_len(double2 p, double2 q) {
   // |q - p|^2 = dx*dx + dy*dy, dx = x[target] - x[origin]; IEEE RN, no FMA (R11)
   const double dx = __dsub_rn(q.x, p.x), dy = __dsub_rn(q.y, p.y);
@@ -135,7 +147,7 @@ __device__ __forceinline__ uint32_t tile_insert(uint32_t* slot, const int32_t* t
   const uint32_t mine = fp | (uint32_t)q;
   uint32_t p = tile_pos(h);
   for (int probe = 0; probe < kTileSlots; ++probe, p = (p + 1) & (kTileSlots - 1)) {
-    uint32_t w = slot[p];
+    uint32_t w = ld_relaxed(&slot[p]);
     if (w == kEmpty) {
       w = atomicCAS(&slot[p], kEmpty, mine);
       if (w == kEmpty) return 0;
@@ -278,7 +290,7 @@ __global__ void __launch_bounds__(kTileThreads, 2)
       const int32_t o = v[k], tg = v[(k + 1) % 3];
       if (o < tg) {
         const uint32_t h = tile_hash((uint32_t)o, (uint32_t)tg);
-        slot[tile_pos(h)] = (h & ~kSlotQ) | (uint32_t)(4 * t + k);
+        st_relaxed(&slot[tile_pos(h)], (h & ~kSlotQ) | (uint32_t)(4 * t + k));
       }
     }
   }
@@ -292,7 +304,7 @@ __global__ void __launch_bounds__(kTileThreads, 2)
       if (o < tg) {
         const uint32_t h = tile_hash((uint32_t)o, (uint32_t)tg);
         const uint32_t mine = (h & ~kSlotQ) | (uint32_t)(4 * t + k);
-        if (slot[tile_pos(h)] != mine) nm |= tile_insert(slot, tri_s, 4 * t + k, (uint32_t)o, (uint32_t)tg);
+        if (ld_relaxed(&slot[tile_pos(h)]) != mine) nm |= tile_insert(slot, tri_s, 4 * t + k, (uint32_t)o, (uint32_t)tg);
       }
     }
   }
@@ -338,12 +350,18 @@ __global__ void __launch_bounds__(kTileThreads, 2)
   __syncthreads();
   PHASE_MARK(3);
 
-  // ---- P4a: pointer jumping (in place; any value on a chain is a valid shortcut)
+  // ---- P4a: pointer jumping, double-buffered between succ and the (still unused) P4-P6
+  // area: each round doubles the resolved chain length; an even number of rounds leaves
+  // the result in succ.
+  static_assert(kTileJumps % 2 == 0, "result must end in succ");
+  uint16_t* succ_b = reinterpret_cast<uint16_t*>(smem_tile + kOffNx);  // 16 KB <= the 18.7 KB P4-P6 area
 #pragma unroll 1
   for (int round = 0; round < kTileJumps; ++round) {
+    const uint16_t* src = (round & 1) ? succ_b : succ;
+    uint16_t* dst = (round & 1) ? succ : succ_b;
     for (int q = tid; q < nq; q += kTileThreads) {
-      const uint16_t sc = succ[q];
-      if (!(sc & (kSuccFront | kSuccUnknown)) && (q & 3) != 3) succ[q] = succ[sc];
+      const uint16_t sc = src[q];
+      dst[q] = ((sc & (kSuccFront | kSuccUnknown)) || (q & 3) == 3) ? sc : src[sc];
     }
     __syncthreads();
   }
