@@ -21,7 +21,7 @@ static int64_t hash_cap_max_for(int64_t T) {
 }
 
 struct Layout {
-  size_t off[32];
+  size_t off[48];
   size_t total;
 };
 
@@ -64,6 +64,7 @@ static Layout layout(int64_t V, int64_t T) {
       (size_t)nw * 4,         // 29 per-word loop lengths
   };
   Layout L{};
+  static_assert(sizeof(sz) / sizeof(sz[0]) <= sizeof(L.off) / sizeof(L.off[0]), "Layout::off too small");
   size_t o = 0;
   for (size_t i = 0; i < sizeof(sz) / sizeof(sz[0]); ++i) {
     L.off[i] = o;
