@@ -11,8 +11,10 @@ the mesh the north_star's roofline target is stated on; its inputs (400 MB) and
 working set (~1.7 GB) exceed the 126 MB L2, so no flush is needed between steps.
 
 value      : input triangles/s, kernel-only, whole job (sum over ranks / max time)
-e2e        : the same through polylla_run_host with pinned HOST buffers (H2D of xy+tri,
-             kernels, D2H of CSR + origin/twin/next), CUDA events on the stream
+e2e        : the same from pinned HOST buffers through polylla.HostPipeline (per mesh: H2D of
+             xy+tri, the four C-ABI calls, D2H of CSR + origin/twin/next; the upload of mesh
+             i+1 overlaps the download of mesh i), wall clock; `single_call_ms` = one
+             synchronous polylla_run_host call, for reference
 roofline   : dominant kernel group, algorithmic bytes / its live CUDA-event time
 cpu_baseline: the CPU oracle (oracle/, 1 thread) on a bounded sample, rank 0 at N=1
 --impl reference: the oracle as the reference arm (each step a bounded sample).
@@ -359,36 +361,46 @@ def main():
     pipeline_roof = {"alg_bytes_per_step_per_gpu": ab["pipeline"] * nm, "achieved": pipe_gbs, "peak": peak,
                      "frac": pipe_gbs / peak, "frac_of_8TBs_nominal": pipe_gbs / 8000.0}
 
-    # ---- end to end through polylla_run_host with pinned host buffers
+    # ---- end to end from pinned HOST buffers through the public API: HostPipeline
+    # (H2D of xy/tri, build -> label -> generate -> CSR, D2H of CSR + origin/twin/next for
+    # every mesh; upload of mesh i+1 overlaps the download of mesh i on full-duplex PCIe)
     e2e = None
     if not args.no_e2e and all(m.get("host") is not None for m in meshes):
-        outs = pp.alloc_host_outputs(Tmax, arrays=True, pin=True)
-        xy_pin = torch.empty((Vmax, 2), dtype=torch.float64).pin_memory()
-        tri_pin = torch.empty((Tmax, 3), dtype=torch.int32).pin_memory()
-        e_ms, h2d, d2h, n_e2e = 0.0, 0, 0, 0
-        e_steps = max(1, min(args.e2e_steps, 10 if args.config != 5 else 1))
-        for rep in range(e_steps + 1):
-            for m in meshes:
-                xy_h, tri_h = m["host"]()  # untimed: refill the pinned staging buffers
-                V, T = xy_h.shape[0], tri_h.shape[0]
-                xy_pin[:V].numpy()[:] = xy_h
-                tri_pin[:T].numpy()[:] = tri_h
-                torch.cuda.synchronize(dev)
-                e0 = torch.cuda.Event(enable_timing=True)
-                e1 = torch.cuda.Event(enable_timing=True)
-                e0.record(stream)
-                r = pp.run_host(xy_pin[:V].numpy(), tri_pin[:T].numpy(), wsp, pinned=outs, stream=stream)
-                e1.record(stream)
-                torch.cuda.synchronize(dev)
-                if rep > 0:  # rep 0 is the warm-up
-                    e_ms += e0.elapsed_time(e1)
-                    h2d += 16 * V + 12 * T
-                    d2h += 4 * (r["P"] + 1) + 4 * r["L"] + 3 * 4 * r["H"]
-                    n_e2e += 1
-        e_ms = batch.max_time(e_ms, dev, ws)
-        e2e = {"value": all_T * e_steps / (e_ms / 1e3), "unit": "triangles/s", "ms_per_step": e_ms / e_steps,
-               "h2d_bytes_per_step": h2d // e_steps, "d2h_bytes_per_step": d2h // e_steps,
-               "api": "polylla_run_host (pinned host in/out; CSR + origin/twin/next returned)"}
+        e_steps = max(2, min(args.e2e_steps, 10 if args.config != 5 else 1))
+        hosts = []
+        for m in meshes:
+            xy_h, tri_h = m["host"]()
+            hosts.append((torch.from_numpy(xy_h).pin_memory(), torch.from_numpy(tri_h).pin_memory()))
+        inputs = [hosts[i % len(hosts)] for i in range(e_steps * len(hosts))]
+        pipe = pp.HostPipeline(Vmax, Tmax, arrays=True, device=dev)
+        outs = [pp.alloc_host_outputs(Tmax, arrays=True, pin=True) for _ in range(2)]
+        out_list = [outs[i % 2] for i in range(len(inputs))]
+        pipe.run(inputs[:2], out_list[:2])  # warm-up (first-touch of the pinned buffers)
+        torch.cuda.synchronize(dev)
+        if ws > 1:
+            dist.barrier()
+        t0 = time.perf_counter()
+        cnts = pipe.run(inputs, out_list)
+        torch.cuda.synchronize(dev)
+        e_s = batch.max_time((time.perf_counter() - t0) * 1e3, dev, ws) / 1e3
+        h2d = sum(16 * x.shape[0] + 12 * t.shape[0] for x, t in inputs) // e_steps
+        d2h = sum(4 * (c["n_polygons"] + 1) + 4 * c["n_loop_entries"] + 12 * c["n_halfedges"] for c in cnts) // e_steps
+        e2e = {"value": all_T * e_steps / e_s, "unit": "triangles/s", "ms_per_step": 1e3 * e_s / e_steps,
+               "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
+               "api": "polylla.HostPipeline over the C ABI (pinned host in/out; CSR + origin/twin/next "
+                      "returned; H2D of mesh i+1 overlapped with D2H of mesh i; wall clock, max over ranks)"}
+        # the unpipelined single call, for reference
+        r_ms = 0.0
+        xy_h, tri_h = hosts[0]
+        o1 = pp.alloc_host_outputs(Tmax, arrays=True, pin=True)
+        pp.run_host(xy_h.numpy(), tri_h.numpy(), wsp, pinned=o1, stream=stream)
+        torch.cuda.synchronize(dev)
+        t0 = time.perf_counter()
+        for _ in range(3):
+            pp.run_host(xy_h.numpy(), tri_h.numpy(), wsp, pinned=o1, stream=stream)
+        torch.cuda.synchronize(dev)
+        e2e["single_call_ms"] = 1e3 * (time.perf_counter() - t0) / 3
+        assert cnts[-1]["n_polygons"] == meshes[(len(inputs) - 1) % len(meshes)]["counts"]["n_polygons"]
 
     cpu = None
     if rank == 0 and ws == 1 and not args.no_cpu_baseline:

@@ -318,3 +318,21 @@ def test_cuda_graph_replay_matches_eager():
         g.stream.synchronize()
         P, L = ref["P"], ref["L"]
         assert torch.equal(offsets[:P + 1], ref["offsets"]) and torch.equal(loops[:L], ref["loops"])
+
+
+def test_host_pipeline_matches_device():
+    pp = _pp()
+    meshes = [synth.random_delaunay(20_000, 50 + i) for i in range(3)]
+    V = max(m[0].shape[0] for m in meshes)
+    T = max(m[1].shape[0] for m in meshes)
+    pipe = pp.HostPipeline(V, T)
+    inputs = [(torch.from_numpy(x).pin_memory(), torch.from_numpy(t).pin_memory()) for x, t in meshes]
+    outs = [pp.alloc_host_outputs(T) for _ in meshes]
+    counts = pipe.run(inputs, outs)
+    for (x, t), o, c in zip(meshes, outs, counts):
+        ref = gpu_run(x, t)
+        P, L, H = c["n_polygons"], c["n_loop_entries"], c["n_halfedges"]
+        assert torch.equal(o["offsets"][:P + 1], ref["offsets"].cpu())
+        assert torch.equal(o["loops"][:L], ref["loops"].cpu())
+        for k in ("origin", "twin", "next"):
+            assert torch.equal(o[k][:H], ref[k].cpu()), k
