@@ -24,19 +24,24 @@ namespace polylla {
 
 constexpr int kTileTris = 2048;
 constexpr int kTileHE = 3 * kTileTris;   // 6144 half-edges = 192 bit-vector words (e order)
-constexpr int kTileQ = 4 * kTileTris;    // quad slots q = 4t + k (slot 3 unused) -> 256 words
+constexpr int kTileQ = 4 * kTileTris;    // quad slots q = 4t + k (slot 3: copy of vertex 0 / unused)
 constexpr int kTileSlots = 8192;         // pow2 hash slots (load ~0.38: only the lo->hi halves insert)
 constexpr int kTileThreads = 768;
 constexpr int kTileWords = kTileHE / 32; // 192
+constexpr int kTriIters = (kTileTris + kTileThreads - 1) / kTileThreads;  // 3 (the third: threads < 512)
+constexpr int kHeIters = kTileHE / kTileThreads;                           // 8 exactly
+static_assert(kTileHE % kTileThreads == 0 && kTileThreads % 96 == 0, "j = tid + 768 i  <=>  q = q_of(tid) + 1024 i");
+static_assert(kTileThreads % 32 == 0 && (kTileTris - 2 * kTileThreads) % 32 == 0, "warp-uniform third triangle");
 // shared memory (bytes):
-//   tri_s int32[kTileHE] 24576
-//   tw_s  int16[kTileQ]  16384   twin as a quad index, -1 = outside the tile
+//   tri_q int32[kTileQ]   32768  quad layout (v0, v1, v2, v0): half-edge q runs tri_q[q] -> tri_q[q+1]
+//   tw_s  int16[kTileQ]   16384  twin as a quad index, -1 = outside the tile
 //   slot  u32[kTileSlots] 32768  (dead after P2: reused for succ u16[kTileQ] | Lm, Dm, Tm, SDm u32[192] | scan scratch)
-//   lc_s  u8[kTileTris]   2048
+//   lc_s  u8[kTileTris]    2048
 //   nx_l  int16[kTileHE] 12288 | Sw, Cw, Wl u32[192] 2304 | slist int16[kTileTris] 4096   (P4-P6)
-constexpr size_t kOffTw = kTileHE * 4, kOffSlot = kOffTw + kTileQ * 2, kOffLc = kOffSlot + kTileSlots * 4,
+constexpr size_t kOffTw = kTileQ * 4, kOffSlot = kOffTw + kTileQ * 2, kOffLc = kOffSlot + kTileSlots * 4,
                  kOffNx = kOffLc + kTileTris,
-                 kTileSmem = kOffNx + kTileHE * 2 + 3 * (kTileHE / 8) + kTileTris * 2;  // 94,464 B -> 2 CTAs/SM
+                 kTileSmem = kOffNx + kTileHE * 2 + 3 * (kTileHE / 8) + kTileTris * 2;  // 102,656 B -> 2 CTAs/SM
+static_assert(2 * (kTileSmem + 1024) <= 228 * 1024, "two tiles per SM");
 constexpr uint32_t kSlotQ = (1u << 13) - 1;       // slot = fingerprint(19 bits) << 13 | quad index
 // rotation successors (P3/P4): quad index in the low 13 bits, terminal flags above
 constexpr uint16_t kSuccIdx = 0x1FFF, kSuccFront = 0x4000, kSuccUnknown = 0x8000;
@@ -59,12 +64,10 @@ __device__ unsigned long long g_phase_cycles[16];
 #define PHASE_MARK(i) do { } while (0)
 #endif
 
-__device__ __forceinline__ int32_t next_local(int32_t j) { return (j % 3 == 2) ? j - 2 : j + 1; }
 // quad encoding of a local half-edge: q = 4*(j/3) + j%3 (bit ops in the walks)
 __device__ __forceinline__ int32_t q_of(int32_t j) { const int32_t t = j / 3; return 4 * t + (j - 3 * t); }
 __device__ __forceinline__ int32_t j_of(int32_t q) { return 3 * (q >> 2) + (q & 3); }
 __device__ __forceinline__ int32_t next_q(int32_t q) { return (q & 3) == 2 ? q - 2 : q + 1; }
-__device__ __forceinline__ bool bit_s(const uint32_t* w, int32_t i) { return (w[i >> 5] >> (i & 31)) & 1u; }
 
 // Relaxed CTA-scope atomic load/store on shared memory (plain LDS/STS in SASS): the hash
 // slot claim is last-writer-wins by design and is read while collision losers CAS, so
@@ -140,8 +143,16 @@ __device__ __forceinline__ uint32_t tile_hash(uint32_t lo, uint32_t hi) {
 }
 __device__ __forceinline__ uint32_t tile_pos(uint32_t h) { return h >> (32 - 13); }
 
-__device__ __forceinline__ uint32_t tile_insert(uint32_t* slot, const int32_t* tri_s, int32_t q, uint32_t lo,
-                                                uint32_t hi) {
+// does slot word w hold the directed key lo -> hi? (fingerprint, then the vertices)
+__device__ __forceinline__ bool slot_is(uint32_t w, uint32_t fp, const int32_t* tri_q, uint32_t lo, uint32_t hi) {
+  if ((w & ~kSlotQ) != fp) return false;
+  const int32_t sq = (int32_t)(w & kSlotQ);
+  return (uint32_t)tri_q[sq] == lo && (uint32_t)tri_q[sq + 1] == hi;
+}
+
+// collision loser: CAS + linear probing from the slot after its home
+__device__ __noinline__ uint32_t tile_insert_probe(uint32_t* slot, const int32_t* tri_q, int32_t q, uint32_t lo,
+                                                   uint32_t hi) {
   const uint32_t h = tile_hash(lo, hi);
   const uint32_t fp = h & ~kSlotQ;
   const uint32_t mine = fp | (uint32_t)q;
@@ -152,38 +163,41 @@ __device__ __forceinline__ uint32_t tile_insert(uint32_t* slot, const int32_t* t
       w = atomicCAS(&slot[p], kEmpty, mine);
       if (w == kEmpty) return 0;
     }
-    if ((w & ~kSlotQ) == fp) {  // same fingerprint: confirm the key
-      const int32_t sq = (int32_t)(w & kSlotQ);
-      if ((uint32_t)tri_s[j_of(sq)] == lo && (uint32_t)tri_s[j_of(next_q(sq))] == hi)
-        return ST_NONMANIFOLD_EDGE;  // the same directed edge twice
-    }
+    if (slot_is(w, fp, tri_q, lo, hi)) return ST_NONMANIFOLD_EDGE;  // the same directed edge twice
   }
   return ST_INTERNAL;
 }
 
-// the quad holding key (lo, hi) in direction lo -> hi, or -1
-__device__ __forceinline__ int32_t tile_lookup(const uint32_t* slot, const int32_t* tri_s, uint32_t lo, uint32_t hi) {
+// the quad holding key lo -> hi, probing from the slot after `p` (the home slot missed), or -1
+__device__ __noinline__ int32_t tile_lookup_probe(const uint32_t* slot, const int32_t* tri_q, uint32_t lo, uint32_t hi) {
   const uint32_t h = tile_hash(lo, hi);
   const uint32_t fp = h & ~kSlotQ;
   uint32_t p = tile_pos(h);
-  for (int probe = 0; probe < kTileSlots; ++probe, p = (p + 1) & (kTileSlots - 1)) {
+  for (int probe = 1; probe < kTileSlots; ++probe) {
+    p = (p + 1) & (kTileSlots - 1);
     const uint32_t w = slot[p];
     if (w == kEmpty) return -1;
-    if ((w & ~kSlotQ) == fp) {
-      const int32_t sq = (int32_t)(w & kSlotQ);
-      if ((uint32_t)tri_s[j_of(sq)] == lo && (uint32_t)tri_s[j_of(next_q(sq))] == hi) return sq;
-    }
+    if (slot_is(w, fp, tri_q, lo, hi)) return (int32_t)(w & kSlotQ);
   }
   return -1;
 }
 
+// is triangle slot i (t = tid + 768 i) of this thread inside the tile?  For a full tile
+// this is compile-time true for i < 2 and warp-uniform for i = 2 (threads < 512).
+template <bool FULL>
+__device__ __forceinline__ bool tri_ok(int i, int t, int nt) {
+  return FULL ? (i < 2 || threadIdx.x < kTileTris - 2 * kTileThreads) : t < nt;
+}
+
 // One CTA per tile of kTileTris triangles.  Phases (PAPER.md section in brackets):
 //  P0 stage the triangle tile (coalesced, streaming)
-//  P1 per triangle: checks, CCW orientation (R10), longest edge Lcode (Alg. 2/7)
+//  P1 per triangle: checks, CCW orientation (R10), longest edge Lcode (Alg. 2/7); the
+//     oriented triangle goes to shared memory in quad layout
 //  P2 tile-local twin matching in a shared-memory hash on (min, max): the lo->hi halves
 //     insert (plain-store claim of the home slot, CAS only for collision losers -- shared
-//     atomics cost ~2 cycles per lane), the hi->lo halves look up read-only   [Sec. 4]
-//  P3 origin/twin out (coalesced); rotation successor of every half-edge: itself if it
+//     atomics cost ~2 cycles per lane), the hi->lo halves look up read-only; the home
+//     slot of every half-edge is probed without divergence, only misses loop   [Sec. 4]
+//  P3 origin/twin written back coalesced; rotation successor of every half-edge: itself if it
 //     is a frontier edge (Alg. 8), else next_in(twin) (sweep_out, R1); a third copy of
 //     an edge breaks the twin involution
 //  P4 the unlink rewire (Alg. 11) by pointer jumping on the successors (lock-step, no
@@ -193,15 +207,18 @@ __device__ __forceinline__ int32_t tile_lookup(const uint32_t* slot, const int32
 //  P6 seeds whose polygon closes inside the tile: landing + loop walk in shared memory
 //     -> canonical seed bits and loop lengths (others go to the global seed walk)
 //  P5 block-aggregated appends of the leftover / deferred / tip / deferred-seed lists
-__global__ void __launch_bounds__(kTileThreads, 2)
-    k_tile(const double2* __restrict__ xy, const int32_t* __restrict__ tri, int64_t V, int64_t T,
-           int32_t* __restrict__ origin, int32_t* __restrict__ twin, int32_t* __restrict__ next,
-           uint8_t* __restrict__ lcode, uint32_t* __restrict__ F0, uint32_t* __restrict__ F1,
-           uint32_t* __restrict__ S, uint32_t* __restrict__ C, int32_t* __restrict__ len, int32_t* __restrict__ wlen,
-           unsigned long long* __restrict__ left_key, int32_t* __restrict__ left_e, int32_t* __restrict__ def_e,
-           int32_t* __restrict__ tips, int32_t* __restrict__ sdef, DevCounters* ctr) {
-  extern __shared__ __align__(16) unsigned char smem_tile[];
-  int32_t* tri_s = reinterpret_cast<int32_t*>(smem_tile);
+// Loops are indexed so that no lane divides: triangle t = tid + 768 i, half-edge
+// j = tid + 768 i with quad q = q_of(tid) + 1024 i (768 = 3 * 256).
+template <bool FULL>
+__device__ __forceinline__ void tile_body(
+    unsigned char* smem_tile, const double2* __restrict__ xy, const int32_t* __restrict__ tri, int64_t V, int64_t T,
+    int32_t* __restrict__ origin, int32_t* __restrict__ twin, int32_t* __restrict__ next, uint8_t* __restrict__ lcode,
+    uint32_t* __restrict__ F0, uint32_t* __restrict__ F1, uint32_t* __restrict__ S, uint32_t* __restrict__ C,
+    int32_t* __restrict__ len, int32_t* __restrict__ wlen, unsigned long long* __restrict__ left_key,
+    int32_t* __restrict__ left_e, int32_t* __restrict__ def_e, int32_t* __restrict__ tips, int32_t* __restrict__ sdef,
+    DevCounters* ctr) {
+  int32_t* tri_q = reinterpret_cast<int32_t*>(smem_tile);
+  int4* tri_q4 = reinterpret_cast<int4*>(smem_tile);
   int16_t* tw_s = reinterpret_cast<int16_t*>(smem_tile + kOffTw);
   uint32_t* slot = reinterpret_cast<uint32_t*>(smem_tile + kOffSlot);
   uint8_t* lc_s = smem_tile + kOffLc;
@@ -219,35 +236,51 @@ __global__ void __launch_bounds__(kTileThreads, 2)
   int* scan_sm = reinterpret_cast<int*>(SDm + kTileWords);  // 136 ints
 
   const int64_t f0 = (int64_t)blockIdx.x * kTileTris;
-  const int nt = (int)(T - f0 < kTileTris ? T - f0 : kTileTris);
-  const int nhe = 3 * nt, nq = 4 * nt;
+  const int nt = FULL ? kTileTris : (int)(T - f0 < kTileTris ? T - f0 : kTileTris);
+  const int nhe = 3 * nt;
   const int64_t e0 = 3 * f0;
   const int tid = threadIdx.x, lane = tid & 31;
+  const int q0 = q_of(tid);  // quad of half-edge j = tid; j + 768 i -> q0 + 1024 i
 #ifdef POLYLLA_PHASE_TIMING
   long long t_phase_ = clock64();
 #endif
 
-  // ---- P0
-  const int32_t* src = tri + e0;
-  if (nhe == kTileHE && ((reinterpret_cast<uintptr_t>(src) & 15) == 0)) {
-    const int4* s4 = reinterpret_cast<const int4*>(src);
-    for (int i = tid; i < kTileHE / 4; i += kTileThreads) reinterpret_cast<int4*>(tri_s)[i] = __ldcs(s4 + i);
-  } else {
-    for (int i = tid; i < nhe; i += kTileThreads) tri_s[i] = __ldcs(src + i);
+  // ---- P0: stage the raw triangle tile (coalesced 16-B streaming loads) in the slot
+  // area; every thread then takes its triangles' vertex ids into registers
+  {
+    int32_t* raw = reinterpret_cast<int32_t*>(slot);  // 24 KB of the 32-KB slot area
+    const int32_t* src = tri + e0;
+    if (FULL && ((reinterpret_cast<uintptr_t>(src) & 15) == 0)) {
+      const int4* s4 = reinterpret_cast<const int4*>(src);
+#pragma unroll
+      for (int i = tid; i < kTileHE / 4; i += kTileThreads) reinterpret_cast<int4*>(raw)[i] = __ldcs(s4 + i);
+    } else {
+      for (int i = tid; i < nhe; i += kTileThreads) raw[i] = __ldcs(src + i);
+    }
   }
+  __syncthreads();
+  int32_t va[kTriIters], vb[kTriIters], vc[kTriIters];
+#pragma unroll
+  for (int i = 0; i < kTriIters; ++i) {
+    const int t = tid + i * kTileThreads;
+    const int32_t* raw = reinterpret_cast<const int32_t*>(slot) + 3 * t;
+    if (tri_ok<FULL>(i, t, nt)) { va[i] = raw[0]; vb[i] = raw[1]; vc[i] = raw[2]; }
+  }
+  __syncthreads();
   for (int i = tid; i < kTileSlots / 4; i += kTileThreads)
     reinterpret_cast<uint4*>(slot)[i] = make_uint4(kEmpty, kEmpty, kEmpty, kEmpty);
   for (int i = tid; i < kTileQ / 2; i += kTileThreads) reinterpret_cast<uint32_t*>(tw_s)[i] = 0xFFFFFFFFu;
-  __syncthreads();
   PHASE_MARK(0);
 
-  // ---- P1
+  // ---- P1: per triangle: checks, orientation, Lcode
   const uint64_t pol = policy_evict_last();
   uint32_t bad = 0;
   int flips = 0;
-#pragma unroll 2
-  for (int t = tid; t < nt; t += kTileThreads) {
-    int32_t a = tri_s[3 * t], b = tri_s[3 * t + 1], c = tri_s[3 * t + 2];
+#pragma unroll
+  for (int i = 0; i < kTriIters; ++i) {
+    const int t = tid + i * kTileThreads;
+    if (!tri_ok<FULL>(i, t, nt)) continue;
+    int32_t a = va[i], b = vb[i], c = vc[i];
     if ((uint64_t)a >= (uint64_t)V || (uint64_t)b >= (uint64_t)V || (uint64_t)c >= (uint64_t)V) {
       bad |= ST_DANGLING;
       a = 0; b = 0; c = 0;
@@ -269,7 +302,7 @@ __global__ void __launch_bounds__(kTileThreads, 2)
     if (d2 > dk) { k = 2; }
     lc_s[t] = (uint8_t)k;
     lcode[f0 + t] = (uint8_t)k;
-    tri_s[3 * t] = a; tri_s[3 * t + 1] = b; tri_s[3 * t + 2] = c;
+    tri_q4[t] = make_int4(a, b, c, a);
   }
   flips = __reduce_add_sync(0xffffffffu, flips);
   bad = __reduce_or_sync(0xffffffffu, bad);
@@ -280,47 +313,80 @@ __global__ void __launch_bounds__(kTileThreads, 2)
   __syncthreads();
   PHASE_MARK(1);
 
-  // ---- P2a: the lo->hi halves claim their home slot with a plain store (last writer wins) ...
-  // (one thread per triangle: its three half-edges (a,b), (b,c), (c,a) with q = 4t + k)
+  // ---- P2a: the lo->hi halves claim their home slot with a plain store (last writer wins)
+#pragma unroll
+  for (int i = 0; i < kTriIters; ++i) {
+    const int t = tid + i * kTileThreads;
+    if (!tri_ok<FULL>(i, t, nt)) continue;
+    const int4 v = tri_q4[t];
+    const int32_t vs[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+      const uint32_t o = (uint32_t)vs[k], tg = (uint32_t)vs[k + 1];
+      const uint32_t h = tile_hash(min(o, tg), max(o, tg));
+      if (o < tg) st_relaxed(&slot[tile_pos(h)], (h & ~kSlotQ) | (uint32_t)(4 * t + k));
+    }
+  }
+  __syncthreads();
+  // ... the losers of a home slot insert with CAS + linear probing (one merged loop per lane)
   uint32_t nm = 0;
-  for (int t = tid; t < nt; t += kTileThreads) {
-    const int32_t v[3] = {tri_s[3 * t], tri_s[3 * t + 1], tri_s[3 * t + 2]};
+  {
+    uint32_t pend = 0;
 #pragma unroll
-    for (int k = 0; k < 3; ++k) {
-      const int32_t o = v[k], tg = v[(k + 1) % 3];
-      if (o < tg) {
-        const uint32_t h = tile_hash((uint32_t)o, (uint32_t)tg);
-        st_relaxed(&slot[tile_pos(h)], (h & ~kSlotQ) | (uint32_t)(4 * t + k));
+    for (int i = 0; i < kTriIters; ++i) {
+      const int t = tid + i * kTileThreads;
+      if (!tri_ok<FULL>(i, t, nt)) continue;
+      const int4 v = tri_q4[t];
+      const int32_t vs[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+      for (int k = 0; k < 3; ++k) {
+        const uint32_t o = (uint32_t)vs[k], tg = (uint32_t)vs[k + 1];
+        const uint32_t h = tile_hash(min(o, tg), max(o, tg));
+        if (o < tg && ld_relaxed(&slot[tile_pos(h)]) != ((h & ~kSlotQ) | (uint32_t)(4 * t + k)))
+          pend |= 1u << (4 * i + k);
       }
+    }
+    while (pend) {
+      const int b = __ffs(pend) - 1;
+      pend &= pend - 1;
+      const int q = 4 * (tid + (b >> 2) * kTileThreads) + (b & 3);
+      nm |= tile_insert_probe(slot, tri_q, q, (uint32_t)tri_q[q], (uint32_t)tri_q[q + 1]);
     }
   }
   __syncthreads();
-  // ... the losers of a home slot insert with CAS + linear probing from there
-  for (int t = tid; t < nt; t += kTileThreads) {
-    const int32_t v[3] = {tri_s[3 * t], tri_s[3 * t + 1], tri_s[3 * t + 2]};
+  // ---- P2b: the hi->lo halves find their twin: home slot probed by every lane, misses loop
+  {
+    uint32_t pend = 0;
 #pragma unroll
-    for (int k = 0; k < 3; ++k) {
-      const int32_t o = v[k], tg = v[(k + 1) % 3];
-      if (o < tg) {
-        const uint32_t h = tile_hash((uint32_t)o, (uint32_t)tg);
-        const uint32_t mine = (h & ~kSlotQ) | (uint32_t)(4 * t + k);
-        if (ld_relaxed(&slot[tile_pos(h)]) != mine) nm |= tile_insert(slot, tri_s, 4 * t + k, (uint32_t)o, (uint32_t)tg);
-      }
-    }
-  }
-  __syncthreads();
-  // ---- P2b: the hi->lo halves find their twin (read-only probes)
-  for (int t = tid; t < nt; t += kTileThreads) {
-    const int32_t v[3] = {tri_s[3 * t], tri_s[3 * t + 1], tri_s[3 * t + 2]};
+    for (int i = 0; i < kTriIters; ++i) {
+      const int t = tid + i * kTileThreads;
+      if (!tri_ok<FULL>(i, t, nt)) continue;
+      const int4 v = tri_q4[t];
+      const int32_t vs[4] = {v.x, v.y, v.z, v.w};
 #pragma unroll
-    for (int k = 0; k < 3; ++k) {
-      const int32_t o = v[k], tg = v[(k + 1) % 3];
-      if (o > tg) {
-        const int32_t sq = tile_lookup(slot, tri_s, (uint32_t)tg, (uint32_t)o);
-        if (sq >= 0) {
-          tw_s[4 * t + k] = (int16_t)sq;
-          tw_s[sq] = (int16_t)(4 * t + k);
+      for (int k = 0; k < 3; ++k) {
+        const uint32_t o = (uint32_t)vs[k], tg = (uint32_t)vs[k + 1];
+        if (o > tg) {
+          const uint32_t h = tile_hash(tg, o);
+          const uint32_t w = slot[tile_pos(h)];
+          if (slot_is(w, h & ~kSlotQ, tri_q, tg, o)) {
+            const int32_t sq = (int32_t)(w & kSlotQ);
+            tw_s[4 * t + k] = (int16_t)sq;
+            tw_s[sq] = (int16_t)(4 * t + k);
+          } else if (w != kEmpty) {
+            pend |= 1u << (4 * i + k);
+          }
         }
+      }
+    }
+    while (pend) {
+      const int b = __ffs(pend) - 1;
+      pend &= pend - 1;
+      const int q = 4 * (tid + (b >> 2) * kTileThreads) + (b & 3);
+      const int32_t sq = tile_lookup_probe(slot, tri_q, (uint32_t)tri_q[q + 1], (uint32_t)tri_q[q]);
+      if (sq >= 0) {
+        tw_s[q] = (int16_t)sq;
+        tw_s[sq] = (int16_t)q;
       }
     }
   }
@@ -328,17 +394,19 @@ __global__ void __launch_bounds__(kTileThreads, 2)
   __syncthreads();
   PHASE_MARK(2);
 
-  // ---- P3: origin/twin out; rotation successors:
+  // ---- P3: origin/twin out (coalesced); rotation successors:
   //   succ[x] = x | FRONT   if x is a frontier half-edge (walk ends there)
   //   succ[x] = x | UNKNOWN if twin(x) is outside the tile (walk must be deferred)
   //   succ[x] = next_q(twin x)  otherwise (cross the non-frontier edge: sweep_out)
-  for (int q = tid; q < nq; q += kTileThreads) {
+  nm = 0;
+#pragma unroll 4
+  for (int i = 0; i < kHeIters; ++i) {
+    const int j = tid + i * kTileThreads, q = q0 + 4 * 256 * i;
+    if (!FULL && j >= nhe) break;
     const int k = q & 3, t = q >> 2;
-    if (k == 3) continue;  // padding slot of the quad layout
-    const int32_t j = 3 * t + k;
     const int32_t tq = tw_s[q];
     if (tq >= 0 && tw_s[tq] != q) nm = ST_NONMANIFOLD_EDGE;  // twin claimed twice (edge in > 2 triangles)
-    __stcs(origin + e0 + j, tri_s[j]);
+    __stcs(origin + e0 + j, tri_q[q]);
     __stcs(twin + e0 + j, tq >= 0 ? (int32_t)(e0 + j_of(tq)) : -1);
     uint16_t sc;
     if (tq < 0) sc = (uint16_t)(q | kSuccUnknown);
@@ -359,21 +427,24 @@ __global__ void __launch_bounds__(kTileThreads, 2)
   for (int round = 0; round < kTileJumps; ++round) {
     const uint16_t* src = (round & 1) ? succ_b : succ;
     uint16_t* dst = (round & 1) ? succ : succ_b;
-    for (int q = tid; q < nq; q += kTileThreads) {
+#pragma unroll
+    for (int i = 0; i < kHeIters; ++i) {
+      const int q = q0 + 4 * 256 * i;
+      if (!FULL && tid + i * kTileThreads >= nhe) break;
       const uint16_t sc = src[q];
-      dst[q] = ((sc & (kSuccFront | kSuccUnknown)) || (q & 3) == 3) ? sc : src[sc];
+      dst[q] = (sc & (kSuccFront | kSuccUnknown)) ? sc : src[sc];
     }
     __syncthreads();
   }
   PHASE_MARK(4);
 
   // ---- P4b: per half-edge (e order): F / S words (Alg. 8-9), next (Alg. 11), tips
-  for (int base = 0; base < kTileHE; base += kTileThreads) {
-    const int j = base + tid;
+#pragma unroll 2
+  for (int i = 0; i < kHeIters; ++i) {
+    const int j = tid + i * kTileThreads, q = q0 + 4 * 256 * i;
     bool fr = false, sd = false, tip = false, deferred = false, left = false;
     int32_t nl_j = -1;
-    if (j < nhe) {
-      const int q = q_of(j);
+    if (FULL || j < nhe) {
       const int32_t tq = tw_s[q];
       if (tq < 0) {
         deferred = left = true;
@@ -403,30 +474,31 @@ __global__ void __launch_bounds__(kTileThreads, 2)
     const uint32_t fw = __ballot_sync(0xffffffffu, fr), sw = __ballot_sync(0xffffffffu, sd);
     const uint32_t tm = __ballot_sync(0xffffffffu, tip), dm = __ballot_sync(0xffffffffu, deferred),
                    lm = __ballot_sync(0xffffffffu, left);
-    const int wbase = j - lane;
+    const int wl = (j - lane) >> 5;  // tile-local word of this warp
     if (lane == 0) {
-      if (wbase < nhe) {
-        const int64_t w = (e0 + wbase) >> 5;
+      if (FULL || j < nhe) {
+        const int64_t w = (e0 >> 5) + wl;
         F0[w] = fw;
         F1[w] = fw;
         S[w] = sw;
       }
-      Lm[wbase >> 5] = lm;
-      Dm[wbase >> 5] = dm;
-      Tm[wbase >> 5] = tm;
-      Sw[wbase >> 5] = sw;
-      Cw[wbase >> 5] = 0u;
-      Wl[wbase >> 5] = 0;
-      SDm[wbase >> 5] = 0u;
+      Lm[wl] = lm;
+      Dm[wl] = dm;
+      Tm[wl] = tm;
+      Sw[wl] = sw;
+      Cw[wl] = 0u;
+      Wl[wl] = 0;
+      SDm[wl] = 0u;
     }
   }
   __syncthreads();
   PHASE_MARK(5);
 
   // ---- P6: seeds whose polygon closes inside the tile (Alg. 12 + Overwrite seeds,
-  // PAPER.md L778-849): land on a frontier half-edge by rotation, walk the loop on nx_l,
-  // keep the minimum id and the length.  Loops that touch a deferred half-edge or a
-  // barrier tip (repaired later) are handed to the global seed walk.
+  // PAPER.md L778-849): land on a frontier half-edge by rotation (the resolved successor
+  // chain), walk the loop on nx_l, keep the minimum id and the length.  Loops that touch
+  // a deferred half-edge or a barrier tip (repaired later) are handed to the global
+  // seed walk.
   {
     const uint32_t w = tid < kTileWords ? Sw[tid] : 0u;
     int4 tot;
@@ -436,16 +508,11 @@ __global__ void __launch_bounds__(kTileThreads, 2)
     __syncthreads();
     for (int i = tid; i < tot.x; i += kTileThreads) {
       const int32_t sj = slist[i];
-      int32_t q = q_of(sj);
-      bool ok = true;
-      for (int steps = 0; succ[q] != (uint16_t)(q | kSuccFront); ++steps) {  // rotate to a frontier half-edge
-        const int32_t tq = tw_s[q];
-        if (tq < 0 || steps > 64) { ok = false; break; }
-        q = next_q(tq);
-      }
+      const uint16_t r = succ[q_of(sj)];  // the frontier half-edge the rotation reaches, if resolved
+      bool ok = (r & kSuccFront) != 0;
       int32_t mn = 0, n = 0;
       if (ok) {
-        const int32_t x = j_of(q);
+        const int32_t x = j_of(r & kSuccIdx);
         int32_t y = x;
         mn = x;
         do {
@@ -465,9 +532,9 @@ __global__ void __launch_bounds__(kTileThreads, 2)
     }
   }
   __syncthreads();
-  for (int w = tid; w * 32 < nhe; w += kTileThreads) {
-    C[(e0 >> 5) + w] = Cw[w];
-    wlen[(e0 >> 5) + w] = Wl[w];
+  if (tid * 32 < nhe) {
+    C[(e0 >> 5) + tid] = Cw[tid];
+    wlen[(e0 >> 5) + tid] = Wl[tid];
   }
   PHASE_MARK(6);
 
@@ -487,7 +554,8 @@ __global__ void __launch_bounds__(kTileThreads, 2)
   while (lw) {
     const int j = tid * 32 + __ffs(lw) - 1;
     lw &= lw - 1;
-    const int32_t o = tri_s[j], tg = tri_s[next_local(j)];
+    const int q = q_of(j);
+    const int32_t o = tri_q[q], tg = tri_q[q + 1];
     const uint64_t lo = (uint32_t)min(o, tg), hi = (uint32_t)max(o, tg);
     left_key[pl] = (lo << 32) | hi;
     left_e[pl++] = (int32_t)(e0 + j);
@@ -507,6 +575,24 @@ __global__ void __launch_bounds__(kTileThreads, 2)
   PHASE_MARK(7);
 }
 
+// full tiles take the specialised body (constant trip counts, no bounds checks); the
+// ragged last tile the generic one
+__global__ void __launch_bounds__(kTileThreads, 2)
+    k_tile(const double2* __restrict__ xy, const int32_t* __restrict__ tri, int64_t V, int64_t T,
+           int32_t* __restrict__ origin, int32_t* __restrict__ twin, int32_t* __restrict__ next,
+           uint8_t* __restrict__ lcode, uint32_t* __restrict__ F0, uint32_t* __restrict__ F1,
+           uint32_t* __restrict__ S, uint32_t* __restrict__ C, int32_t* __restrict__ len, int32_t* __restrict__ wlen,
+           unsigned long long* __restrict__ left_key, int32_t* __restrict__ left_e, int32_t* __restrict__ def_e,
+           int32_t* __restrict__ tips, int32_t* __restrict__ sdef, DevCounters* ctr) {
+  extern __shared__ __align__(16) unsigned char smem_tile[];
+  if ((int64_t)(blockIdx.x + 1) * kTileTris <= T)
+    tile_body<true>(smem_tile, xy, tri, V, T, origin, twin, next, lcode, F0, F1, S, C, len, wlen, left_key, left_e,
+                    def_e, tips, sdef, ctr);
+  else
+    tile_body<false>(smem_tile, xy, tri, V, T, origin, twin, next, lcode, F0, F1, S, C, len, wlen, left_key, left_e,
+                     def_e, tips, sdef, ctr);
+}
+
 #ifdef POLYLLA_PHASE_TIMING
 extern "C" __attribute__((visibility("default"))) int polylla_debug_phase_cycles(unsigned long long* out, int reset) {
   if (cudaMemcpyFromSymbol(out, g_phase_cycles, sizeof(g_phase_cycles)) != cudaSuccess) return -1;
@@ -524,7 +610,7 @@ __device__ __forceinline__ uint64_t hash_cap_for(int32_t n) {
   return c;
 }
 
-__global__ void k_hash_clear(DevCounters* ctr, uint32_t* ehash, uint32_t* vkey, int64_t cap_max) {
+__global__ void k_hash_clear(DevCounters* ctr, uint32_t* ehash, int64_t cap_max) {
   const uint64_t cap = hash_cap_for(ctr->n_left);
   if ((int64_t)cap > cap_max) {
     if (blockIdx.x == 0 && threadIdx.x == 0) raise_status(ctr, ST_INTERNAL);
@@ -533,7 +619,6 @@ __global__ void k_hash_clear(DevCounters* ctr, uint32_t* ehash, uint32_t* vkey, 
   if (blockIdx.x == 0 && threadIdx.x == 0) ctr->hash_cap = (uint32_t)cap;
   for (uint64_t i = blockIdx.x * blockDim.x + threadIdx.x; i < cap; i += gridDim.x * blockDim.x) {
     ehash[i] = kEmpty;
-    vkey[i] = kEmpty;
   }
 }
 
@@ -582,12 +667,13 @@ __global__ void k_left_unmatched(DevCounters* ctr, const int32_t* __restrict__ l
   }
 }
 
-// border records: b = 3T + rank(e) over unmatched interior e (R9)
+// border records: b = 3T + rank(e) over unmatched interior e (R9); vmap[origin(b)] = b
+// (written only at border vertices, so it needs no clearing: k_border_next reads it only
+// at border vertices and verifies what it reads)
 struct BorderOp {
   const uint32_t* Bd;
   int32_t *origin, *twin;
-  uint32_t* vkey;
-  int32_t* vval;
+  int32_t* vmap;
   DevCounters* ctr;
   int64_t T3;
   __device__ bool skip() const { return ctr->status != 0; }
@@ -605,38 +691,24 @@ struct BorderOp {
     twin[e] = b;
     twin[b] = e;
     origin[b] = v;
-    const uint32_t mask = (uint32_t)ctr->hash_cap - 1;
-    uint32_t h = mix32((uint32_t)v, 0x5bd1e995u) & mask;
-    for (uint32_t probe = 0; probe <= mask; ++probe) {
-      const uint32_t old = atomicCAS(&vkey[h], kEmpty, (uint32_t)v);
-      if (old == kEmpty) { vval[h] = b; return; }
-      if (old == (uint32_t)v) { raise_status(ctr, ST_NONMANIFOLD_VERTEX); return; }
-      h = (h + 1) & mask;
-    }
-    raise_status(ctr, ST_INTERNAL);
+    vmap[v] = b;
   }
 };
 
-// next(b) = the border half-edge whose origin is target(b) = origin(twin(b))
+// next(b) = the border half-edge whose origin is target(b) = origin(twin(b)).  A vertex
+// with two outgoing border half-edges keeps only one of them in vmap: the other fails
+// the vmap[origin(b)] == b check (NON_MANIFOLD_VERTEX).
 __global__ void k_border_next(DevCounters* ctr, int64_t T3, const int32_t* __restrict__ origin,
-                              const int32_t* __restrict__ twin, const uint32_t* __restrict__ vkey,
-                              const int32_t* __restrict__ vval, int32_t* next) {
+                              const int32_t* __restrict__ twin, const int32_t* __restrict__ vmap, int32_t* next) {
   if (ctr->status) return;
   const int32_t nb = ctr->n_border;
-  const uint32_t mask = (uint32_t)ctr->hash_cap - 1;
   for (int32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < nb; i += gridDim.x * blockDim.x) {
     const int32_t b = (int32_t)(T3 + i);
-    const uint32_t v = (uint32_t)origin[twin[b]];
-    uint32_t h = mix32(v, 0x5bd1e995u) & mask;
-    int32_t nx = -1;
-    for (uint32_t probe = 0; probe <= mask; ++probe) {
-      const uint32_t k = vkey[h];
-      if (k == v) { nx = vval[h]; break; }
-      if (k == kEmpty) break;
-      h = (h + 1) & mask;
-    }
-    if (nx < 0) raise_status(ctr, ST_NONMANIFOLD_VERTEX);
-    next[b] = nx;
+    const int32_t v = origin[twin[b]];
+    const int32_t nx = vmap[v];
+    const bool ok = vmap[origin[b]] == b && nx >= T3 && nx - T3 < nb && origin[nx] == v;
+    if (!ok) raise_status(ctr, ST_NONMANIFOLD_VERTEX);
+    next[b] = ok ? nx : -1;
   }
 }
 
@@ -658,17 +730,17 @@ int launch_build(Ctx* c, cudaStream_t s) {
   ++n;
   const int grid = 148 * 32;  // enough threads for ~1 leftover each on 10M-vertex meshes (latency-bound)
   prof_mark(s, "k_left_match");
-  k_hash_clear<<<grid, 256, 0, s>>>(c->ctr, c->ehash, c->vkey, c->hash_cap_max);
+  k_hash_clear<<<grid, 256, 0, s>>>(c->ctr, c->ehash, c->hash_cap_max);
   k_left_insert<<<grid, 256, 0, s>>>(c->ctr, c->left_key, c->left_e, c->origin, c->twin, c->ehash);
   k_left_unmatched<<<grid, 256, 0, s>>>(c->ctr, c->left_e, c->twin, c->Bd);
   n += 3;
   prof_mark(s, "k_border_scan");
-  BorderOp op{c->Bd, c->origin, c->twin, c->vkey, c->vval, c->ctr, 3 * c->T};
+  BorderOp op{c->Bd, c->origin, c->twin, c->vmap, c->ctr, 3 * c->T};
   const int r = launch_scan(op, c->n_words, c->scan_a, c->scan_b, c->scan_c, s);
   if (r < 0) return -1;
   n += r;
   prof_mark(s, "k_border_next");
-  k_border_next<<<grid, 256, 0, s>>>(c->ctr, 3 * c->T, c->origin, c->twin, c->vkey, c->vval, c->next);
+  k_border_next<<<grid, 256, 0, s>>>(c->ctr, 3 * c->T, c->origin, c->twin, c->vmap, c->next);
   ++n;
   prof_end(s);
   return cudaGetLastError() == cudaSuccess ? n : -1;

@@ -45,8 +45,8 @@ static Layout layout(int64_t V, int64_t T) {
       (size_t)(3 * T) * 8,    // 10 left_key
       (size_t)(3 * T) * 4,    // 11 left_e
       (size_t)cap * 4,        // 12 ehash
-      (size_t)cap * 4,        // 13 vkey
-      (size_t)cap * 4,        // 14 vval
+      (size_t)V * 4,          // 13 vmap
+      0,                      // 14 (unused)
       (size_t)V * 4,          // 15 tips
       (size_t)(2 * V) * 4,    // 16 aff
       (size_t)(2 * V) * 4,    // 17 mids
@@ -94,8 +94,7 @@ bool carve(Ctx* c, void* ws, size_t bytes) {
   c->left_key = reinterpret_cast<unsigned long long*>(b + L.off[10]);
   c->left_e = reinterpret_cast<int32_t*>(b + L.off[11]);
   c->ehash = reinterpret_cast<uint32_t*>(b + L.off[12]);
-  c->vkey = reinterpret_cast<uint32_t*>(b + L.off[13]);
-  c->vval = reinterpret_cast<int32_t*>(b + L.off[14]);
+  c->vmap = reinterpret_cast<int32_t*>(b + L.off[13]);
   c->hash_cap_max = hash_cap_max_for(c->T);
   c->tips = reinterpret_cast<int32_t*>(b + L.off[15]);
   c->aff = reinterpret_cast<int32_t*>(b + L.off[16]);

@@ -6,7 +6,7 @@
 //   F0, F1, S, C, Bd : uint32 bit-vectors over the interior half-edges [0, 3T)
 //                      (frontier before/after repair, seed, canonical seed, unmatched)
 //   len              : int32 [3T]  loop length, written only at canonical seeds
-//   leftover keys/ids, global edge hash, border-vertex hash, tips, mids, scan sums,
+//   leftover keys/ids, global edge hash, border-vertex map vmap[V], tips, mids, scan sums,
 //   seeds/offsets/loops staging, input staging (run_host).
 #pragma once
 #include <cstdint>
@@ -62,8 +62,7 @@ struct Ctx {
   int32_t* def_e;   // [3T] half-edges deferred by k_tile
   int32_t* sdef;    // [T] seeds deferred by k_tile
   uint32_t* ehash;  // leftover-edge hash slots [hash_cap_max] (capacity chosen on device)
-  uint32_t* vkey;   // border-vertex hash: key = vertex id [hash_cap_max]
-  int32_t* vval;    //                      val = border half-edge id
+  int32_t* vmap;    // [V] border half-edge leaving each border vertex (written at border vertices only)
   int64_t hash_cap_max;
   int32_t* tips;    // [V]
   int32_t* aff;     // [2V] affected (outgoing half-edge) per tip side
