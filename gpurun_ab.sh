@@ -1,0 +1,8 @@
+mkdir -p gpurun_out
+timeout 900 python -m pytest tests -m gpu -x -q 2>&1 | tail -2
+POLYLLA_LIB=$PWD/paper_2403_14723_b200/libpolylla_walks.so timeout 900 python -m pytest tests -m gpu -x -q -k "config3_full or config2 or fan or random or config5" 2>&1 | tail -2
+for lib in libpolylla.so libpolylla_walks.so libpolylla.so libpolylla_walks.so; do
+POLYLLA_LIB=$PWD/paper_2403_14723_b200/$lib timeout 300 python bench.py --no-cpu-baseline --no-e2e --steps 100 > gpurun_out/bench_q.json 2>gpurun_out/bench_q.err; tail -2 gpurun_out/bench_q.err
+python -c "
+import json; d=json.load(open('gpurun_out/bench_q.json')); print('$lib ms/step %.3f  Gtris/s %.2f  pipe_frac %.3f' % (d['ms_per_step'], d['value']/1e9, d['pipeline_roofline']['frac'])); print({k: round(v,3) for k,v in d['kernels_ms_per_step'].items()})"
+done

@@ -1,0 +1,7 @@
+mkdir -p gpurun_out
+timeout 900 python -m pytest tests -m gpu -x -q -k "config3_full or config2 or fan or random or config5_grid" 2>&1 | tail -2
+for d in 296 0 148 444 592; do
+POLYLLA_PREFETCH_DIST=$d timeout 300 python bench.py --no-cpu-baseline --no-e2e --steps 100 > gpurun_out/bench_q.json 2>gpurun_out/bench_q.err; tail -2 gpurun_out/bench_q.err
+python -c "
+import json; d=json.load(open('gpurun_out/bench_q.json')); print('dist $d ms/step %.3f  Gtris/s %.2f  pipe_frac %.3f' % (d['ms_per_step'], d['value']/1e9, d['pipeline_roofline']['frac'])); print({k: round(v,3) for k,v in d['kernels_ms_per_step'].items()})"
+done

@@ -87,7 +87,7 @@ typedef struct {
   int64_t n_flips;         /* CW input triangles re-oriented */
   int64_t n_leftover;      /* half-edges whose twin was matched outside their build tile */
   int64_t n_deferred;      /* half-edges whose label/rewire needed data outside their tile (polylla_label) */
-  int64_t n_seed_deferred; /* seeds whose polygon did not close inside their tile (global seed walk) */
+  int64_t n_seed_deferred; /* seeds walked globally: polygon not closed inside the build tile, or a repair half */
   int32_t status;          /* the device status, as a polylla_status */
   int32_t reserved;
 } polylla_counts;

@@ -17,12 +17,14 @@
 //   border scan (scan.cuh)             -- border ids 3T + rank(e) (R9), twin/origin of
 //                                         border half-edges, border-vertex hash;
 //   k_border_next                      -- next(b) = border half-edge leaving target(b).
+#include <cstdlib>
+
 #include "internal.cuh"
 #include "scan.cuh"
 
 namespace polylla {
 
-constexpr int kTileTris = 2048;
+constexpr int kTileTris = kBuildTileTris;
 constexpr int kTileHE = 3 * kTileTris;   // 6144 half-edges = 192 bit-vector words (e order)
 constexpr int kTileQ = 4 * kTileTris;    // quad slots q = 4t + k (slot 3: copy of vertex 0 / unused)
 constexpr int kTileSlots = 8192;         // pow2 hash slots (load ~0.38: only the lo->hi halves insert)
@@ -35,12 +37,15 @@ static_assert(kTileThreads % 32 == 0 && (kTileTris - 2 * kTileThreads) % 32 == 0
 // shared memory (bytes):
 //   tri_q int32[kTileQ]   32768  quad layout (v0, v1, v2, v0): half-edge q runs tri_q[q] -> tri_q[q+1]
 //   tw_s  int16[kTileQ]   16384  twin as a quad index, -1 = outside the tile
-//   slot  u32[kTileSlots] 32768  (dead after P2: reused for succ u16[kTileQ] | Lm, Dm, Tm, SDm u32[192] | scan scratch)
+//   slot  u32[kTileSlots] 32768  (dead after P2: reused for succ u16[kTileQ] | Lm, Dm, SDm u32[192] | scratch, offL, offD)
 //   lc_s  u8[kTileTris]    2048
 //   nx_l  int16[kTileHE] 12288 | Sw, Cw, Wl u32[192] 2304 | slist int16[kTileTris] 4096   (P4-P6)
+//         (P0-P1: the raw triangle tile int32[kTileHE], 24576)
 constexpr size_t kOffTw = kTileQ * 4, kOffSlot = kOffTw + kTileQ * 2, kOffLc = kOffSlot + kTileSlots * 4,
                  kOffNx = kOffLc + kTileTris,
-                 kTileSmem = kOffNx + kTileHE * 2 + 3 * (kTileHE / 8) + kTileTris * 2;  // 102,656 B -> 2 CTAs/SM
+                 kNxBytes = kTileHE * 2 + 3 * (kTileHE / 8) + kTileTris * 2,  // P4-P6 arrays (18,688 B)
+                 kRawBytes = kTileHE * 4,                                      // P0-P1 raw tile (24,576 B)
+                 kTileSmem = kOffNx + (kNxBytes > kRawBytes ? kNxBytes : kRawBytes);  // 108,544 B -> 2 CTAs/SM
 static_assert(2 * (kTileSmem + 1024) <= 228 * 1024, "two tiles per SM");
 constexpr uint32_t kSlotQ = (1u << 13) - 1;       // slot = fingerprint(19 bits) << 13 | quad index
 // rotation successors (P3/P4): quad index in the low 13 bits, terminal flags above
@@ -96,40 +101,6 @@ __device__ __forceinline__ uint64_t policy_evict_last() {
 __device__ __forceinline__ double2 ld_xy(const double2* ptr, uint64_t pol) {
   double2 r;
   asm volatile("ld.global.nc.L2::cache_hint.v2.f64 {%0, %1}, [%2], %3;" : "=d"(r.x), "=d"(r.y) : "l"(ptr), "l"(pol));
-  return r;
-}
-
-// block-wide exclusive scan of 4 counters (kTileThreads threads); returns the prefix
-__device__ __forceinline__ int4 block_scan4(int4 v, int4* tot, int* sm /* [4 * 32 + 4] */) {
-  constexpr int NW = kTileThreads / 32;
-  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  int4 inc = v;
-#pragma unroll
-  for (int o = 1; o < 32; o <<= 1) {
-    const int a = __shfl_up_sync(0xffffffffu, inc.x, o), b = __shfl_up_sync(0xffffffffu, inc.y, o),
-              c = __shfl_up_sync(0xffffffffu, inc.z, o), d = __shfl_up_sync(0xffffffffu, inc.w, o);
-    if (lane >= o) { inc.x += a; inc.y += b; inc.z += c; inc.w += d; }
-  }
-  if (lane == 31) { sm[wid] = inc.x; sm[32 + wid] = inc.y; sm[64 + wid] = inc.z; sm[96 + wid] = inc.w; }
-  __syncthreads();
-  if (wid == 0) {
-    int a = lane < NW ? sm[lane] : 0, b = lane < NW ? sm[32 + lane] : 0, c = lane < NW ? sm[64 + lane] : 0,
-        d = lane < NW ? sm[96 + lane] : 0;
-    int ia = a, ib = b, ic = c, id = d;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      const int x = __shfl_up_sync(0xffffffffu, ia, o), y = __shfl_up_sync(0xffffffffu, ib, o),
-                z = __shfl_up_sync(0xffffffffu, ic, o), w = __shfl_up_sync(0xffffffffu, id, o);
-      if (lane >= o) { ia += x; ib += y; ic += z; id += w; }
-    }
-    if (lane < NW) { sm[lane] = ia - a; sm[32 + lane] = ib - b; sm[64 + lane] = ic - c; sm[96 + lane] = id - d; }
-    if (lane == NW - 1) { sm[128] = ia; sm[129] = ib; sm[130] = ic; sm[131] = id; }
-  }
-  __syncthreads();
-  *tot = make_int4(sm[128], sm[129], sm[130], sm[131]);
-  const int4 r = make_int4(sm[wid] + inc.x - v.x, sm[32 + wid] + inc.y - v.y, sm[64 + wid] + inc.z - v.z,
-                           sm[96 + wid] + inc.w - v.w);
-  __syncthreads();  // sm is reused by the caller
   return r;
 }
 
@@ -204,9 +175,10 @@ __device__ __forceinline__ bool tri_ok(int i, int t, int nt) {
 //     divergent walks); frontier / seed bits (Alg. 8-9); tips (next == twin);
 //     half-edges needing a twin outside the tile (or a longer rotation) are deferred
 //     to k_label_fixup (label phase)
+//  P5 the leftover and deferred lists as per-tile segments (one warp ranks the words)
 //  P6 seeds whose polygon closes inside the tile: landing + loop walk in shared memory
-//     -> canonical seed bits and loop lengths (others go to the global seed walk)
-//  P5 block-aggregated appends of the leftover / deferred / tip / deferred-seed lists
+//     -> canonical seed bits and loop lengths (others go to the global seed walk via the
+//     bit-vector SDB; tips go to the bit-vector TB)
 // Loops are indexed so that no lane divides: triangle t = tid + 768 i, half-edge
 // j = tid + 768 i with quad q = q_of(tid) + 1024 i (768 = 3 * 256).
 template <bool FULL>
@@ -215,8 +187,8 @@ __device__ __forceinline__ void tile_body(
     int32_t* __restrict__ origin, int32_t* __restrict__ twin, int32_t* __restrict__ next, uint8_t* __restrict__ lcode,
     uint32_t* __restrict__ F0, uint32_t* __restrict__ F1, uint32_t* __restrict__ S, uint32_t* __restrict__ C,
     int32_t* __restrict__ len, int32_t* __restrict__ wlen, unsigned long long* __restrict__ left_key,
-    int32_t* __restrict__ left_e, int32_t* __restrict__ def_e, int32_t* __restrict__ tips, int32_t* __restrict__ sdef,
-    DevCounters* ctr) {
+    int32_t* __restrict__ left_e, int32_t* __restrict__ def_e, uint32_t* __restrict__ TB, uint32_t* __restrict__ SDB,
+    int32_t* __restrict__ cnt_ld, DevCounters* ctr, int64_t tile, int64_t tile_next) {
   int32_t* tri_q = reinterpret_cast<int32_t*>(smem_tile);
   int4* tri_q4 = reinterpret_cast<int4*>(smem_tile);
   int16_t* tw_s = reinterpret_cast<int16_t*>(smem_tile + kOffTw);
@@ -231,11 +203,11 @@ __device__ __forceinline__ void tile_body(
   uint16_t* succ = reinterpret_cast<uint16_t*>(slot);
   uint32_t* Lm = slot + kTileQ / 2;
   uint32_t* Dm = Lm + kTileWords;
-  uint32_t* Tm = Dm + kTileWords;
-  uint32_t* SDm = Tm + kTileWords;
-  int* scan_sm = reinterpret_cast<int*>(SDm + kTileWords);  // 136 ints
+  uint32_t* SDm = Dm + kTileWords;
+  int* scan_sm = reinterpret_cast<int*>(SDm + kTileWords);  // 136 ints + offL/offD [2 x 192]
 
-  const int64_t f0 = (int64_t)blockIdx.x * kTileTris;
+  const int64_t f0 = tile * kTileTris;
+  const int64_t f0n = tile_next * kTileTris;  // this CTA's next tile (prefetched), if tile_next >= 0
   const int nt = FULL ? kTileTris : (int)(T - f0 < kTileTris ? T - f0 : kTileTris);
   const int nhe = 3 * nt;
   const int64_t e0 = 3 * f0;
@@ -245,31 +217,31 @@ __device__ __forceinline__ void tile_body(
   long long t_phase_ = clock64();
 #endif
 
-  // ---- P0: stage the raw triangle tile (coalesced 16-B streaming loads) in the slot
-  // area; every thread then takes its triangles' vertex ids into registers
+  // ---- P0: stage the raw triangle tile (coalesced 16-B streaming loads) in the P4-P6
+  // area (free until P4); clear the hash slots and the twins meanwhile
+  const int32_t* raw = reinterpret_cast<const int32_t*>(smem_tile + kOffNx);
   {
-    int32_t* raw = reinterpret_cast<int32_t*>(slot);  // 24 KB of the 32-KB slot area
+    int32_t* dst = reinterpret_cast<int32_t*>(smem_tile + kOffNx);
     const int32_t* src = tri + e0;
     if (FULL && ((reinterpret_cast<uintptr_t>(src) & 15) == 0)) {
       const int4* s4 = reinterpret_cast<const int4*>(src);
 #pragma unroll
-      for (int i = tid; i < kTileHE / 4; i += kTileThreads) reinterpret_cast<int4*>(raw)[i] = __ldcs(s4 + i);
+      for (int i = tid; i < kTileHE / 4; i += kTileThreads) reinterpret_cast<int4*>(dst)[i] = __ldcs(s4 + i);
     } else {
-      for (int i = tid; i < nhe; i += kTileThreads) raw[i] = __ldcs(src + i);
+      for (int i = tid; i < nhe; i += kTileThreads) dst[i] = __ldcs(src + i);
     }
   }
-  __syncthreads();
-  int32_t va[kTriIters], vb[kTriIters], vc[kTriIters];
-#pragma unroll
-  for (int i = 0; i < kTriIters; ++i) {
-    const int t = tid + i * kTileThreads;
-    const int32_t* raw = reinterpret_cast<const int32_t*>(slot) + 3 * t;
-    if (tri_ok<FULL>(i, t, nt)) { va[i] = raw[0]; vb[i] = raw[1]; vc[i] = raw[2]; }
-  }
-  __syncthreads();
   for (int i = tid; i < kTileSlots / 4; i += kTileThreads)
     reinterpret_cast<uint4*>(slot)[i] = make_uint4(kEmpty, kEmpty, kEmpty, kEmpty);
   for (int i = tid; i < kTileQ / 2; i += kTileThreads) reinterpret_cast<uint32_t*>(tw_s)[i] = 0xFFFFFFFFu;
+  if (tid == 0 && tile_next >= 0) {  // the next tile's triangles -> L2 (TMA bulk prefetch)
+    const int64_t nn = T - f0n < kTileTris ? T - f0n : kTileTris;
+    const int32_t* pn = tri + 3 * f0n;
+    const uint32_t bytes = (uint32_t)((3 * nn * 4) & ~int64_t(15));
+    if (bytes && (reinterpret_cast<uintptr_t>(pn) & 15) == 0)
+      asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(pn), "r"(bytes) : "memory");
+  }
+  __syncthreads();
   PHASE_MARK(0);
 
   // ---- P1: per triangle: checks, orientation, Lcode
@@ -280,7 +252,7 @@ __device__ __forceinline__ void tile_body(
   for (int i = 0; i < kTriIters; ++i) {
     const int t = tid + i * kTileThreads;
     if (!tri_ok<FULL>(i, t, nt)) continue;
-    int32_t a = va[i], b = vb[i], c = vc[i];
+    int32_t a = raw[3 * t], b = raw[3 * t + 1], c = raw[3 * t + 2];
     if ((uint64_t)a >= (uint64_t)V || (uint64_t)b >= (uint64_t)V || (uint64_t)c >= (uint64_t)V) {
       bad |= ST_DANGLING;
       a = 0; b = 0; c = 0;
@@ -394,6 +366,19 @@ __device__ __forceinline__ void tile_body(
   __syncthreads();
   PHASE_MARK(2);
 
+  // ---- prefetch the coordinates of the next tile's vertices into L2 (its triangles were
+  // bulk-prefetched in P0), so that tile's P1 gathers hit L2 instead of HBM
+  if (tile_next >= 0) {
+    const int64_t nn = T - f0n < kTileTris ? T - f0n : kTileTris;
+    for (int t = tid; t < nn; t += kTileThreads) {
+      const int32_t* src = tri + 3 * (f0n + t);
+      const int32_t a = __ldg(src), b = __ldg(src + 1), c = __ldg(src + 2);
+      if ((uint64_t)a < (uint64_t)V) asm volatile("prefetch.global.L2::evict_last [%0];" ::"l"(xy + a));
+      if ((uint64_t)b < (uint64_t)V) asm volatile("prefetch.global.L2::evict_last [%0];" ::"l"(xy + b));
+      if ((uint64_t)c < (uint64_t)V) asm volatile("prefetch.global.L2::evict_last [%0];" ::"l"(xy + c));
+    }
+  }
+
   // ---- P3: origin/twin out (coalesced); rotation successors:
   //   succ[x] = x | FRONT   if x is a frontier half-edge (walk ends there)
   //   succ[x] = x | UNKNOWN if twin(x) is outside the tile (walk must be deferred)
@@ -421,8 +406,9 @@ __device__ __forceinline__ void tile_body(
   // ---- P4a: pointer jumping, double-buffered between succ and the (still unused) P4-P6
   // area: each round doubles the resolved chain length; an even number of rounds leaves
   // the result in succ.
+#ifndef POLYLLA_TILE_WALKS
   static_assert(kTileJumps % 2 == 0, "result must end in succ");
-  uint16_t* succ_b = reinterpret_cast<uint16_t*>(smem_tile + kOffNx);  // 16 KB <= the 18.7 KB P4-P6 area
+  uint16_t* succ_b = reinterpret_cast<uint16_t*>(smem_tile + kOffNx);  // 16 KB <= the P4-P6 area
 #pragma unroll 1
   for (int round = 0; round < kTileJumps; ++round) {
     const uint16_t* src = (round & 1) ? succ_b : succ;
@@ -436,6 +422,7 @@ __device__ __forceinline__ void tile_body(
     }
     __syncthreads();
   }
+#endif
   PHASE_MARK(4);
 
   // ---- P4b: per half-edge (e order): F / S words (Alg. 8-9), next (Alg. 11), tips
@@ -453,7 +440,12 @@ __device__ __forceinline__ void tile_body(
         sd = lc_s[q >> 2] == (q & 3) && lc_s[tq >> 2] == (tq & 3) && q < tq;  // terminal edge, smaller id
         int32_t nx = next_q(q);
         if (fr) {
+#ifdef POLYLLA_TILE_WALKS
+          uint16_t r = succ[nx];
+          for (int st = 0; !(r & (kSuccFront | kSuccUnknown)) && st < 15; ++st) r = succ[r];  // chains <= 16 (as the jumping)
+#else
           const uint16_t r = succ[nx];  // first frontier half-edge about target(j), if reached
+#endif
           if (r & kSuccFront) {
             nx = r & kSuccIdx;
             tip = nx == tq;  // barrier tip: next == twin (R4)
@@ -481,10 +473,10 @@ __device__ __forceinline__ void tile_body(
         F0[w] = fw;
         F1[w] = fw;
         S[w] = sw;
+        TB[w] = tm;
       }
       Lm[wl] = lm;
       Dm[wl] = dm;
-      Tm[wl] = tm;
       Sw[wl] = sw;
       Cw[wl] = 0u;
       Wl[wl] = 0;
@@ -494,21 +486,90 @@ __device__ __forceinline__ void tile_body(
   __syncthreads();
   PHASE_MARK(5);
 
+  // ---- P6 setup, one warp each (no block-wide scan, no global atomic): warp 0 lists the
+  // seed candidates of the tile (slist); warp 1 ranks the leftover and deferred half-edges
+  // of every word (their lists are per-tile segments at e0 of left_e/left_key/def_e, with
+  // the counts in cnt_ld[2 * tile + {0, 1}])
+  int* offL = scan_sm + 136;  // [kTileWords] exclusive prefix of leftovers per word
+  int* offD = offL + kTileWords;
+  {
+    constexpr int kWPL = kTileWords / 32;  // 6 words per lane
+    const int warp = tid >> 5;
+    if (warp < 2) {
+      const uint32_t* src0 = warp == 0 ? Sw : Lm;
+      uint32_t m0[kWPL], m1[kWPL];
+      int c0 = 0, c1 = 0;
+#pragma unroll
+      for (int k = 0; k < kWPL; ++k) {
+        m0[k] = src0[kWPL * lane + k];
+        m1[k] = warp == 0 ? 0u : Dm[kWPL * lane + k];
+        c0 += __popc(m0[k]);
+        c1 += __popc(m1[k]);
+      }
+      int i0 = c0, i1 = c1;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int a = __shfl_up_sync(0xffffffffu, i0, o), b = __shfl_up_sync(0xffffffffu, i1, o);
+        if (lane >= o) { i0 += a; i1 += b; }
+      }
+      int p0 = i0 - c0, p1 = i1 - c1;
+      if (warp == 0) {
+#pragma unroll
+        for (int k = 0; k < kWPL; ++k)
+          for (uint32_t b = m0[k]; b; b &= b - 1) slist[p0++] = (int16_t)((kWPL * lane + k) * 32 + __ffs(b) - 1);
+        if (lane == 31) scan_sm[0] = i0;  // number of seed candidates
+      } else {
+#pragma unroll
+        for (int k = 0; k < kWPL; ++k) {
+          offL[kWPL * lane + k] = p0;
+          offD[kWPL * lane + k] = p1;
+          p0 += __popc(m0[k]);
+          p1 += __popc(m1[k]);
+        }
+        if (lane == 31) {
+          reinterpret_cast<int2*>(cnt_ld)[tile] = make_int2(i0, i1);
+          if (i0) atomicAdd(&ctr->n_left, i0);  // totals (result unused: a reduction)
+          if (i1) atomicAdd(&ctr->n_def, i1);
+        }
+      }
+    }
+  }
+  __syncthreads();
+
+  // ---- P5: the leftover (key, id) and deferred lists, one word per thread
+  if (tid < kTileWords) {
+    uint32_t lw = Lm[tid], dw = Dm[tid];
+    int pl = (int)e0 + offL[tid], pd = (int)e0 + offD[tid];
+    while (lw) {
+      const int j = tid * 32 + __ffs(lw) - 1;
+      lw &= lw - 1;
+      const int q = q_of(j);
+      const int32_t o = tri_q[q], tg = tri_q[q + 1];
+      const uint64_t lo = (uint32_t)min(o, tg), hi = (uint32_t)max(o, tg);
+      left_key[pl] = (lo << 32) | hi;
+      left_e[pl++] = (int32_t)(e0 + j);
+    }
+    while (dw) {
+      def_e[pd++] = (int32_t)(e0 + tid * 32 + __ffs(dw) - 1);
+      dw &= dw - 1;
+    }
+  }
+
   // ---- P6: seeds whose polygon closes inside the tile (Alg. 12 + Overwrite seeds,
   // PAPER.md L778-849): land on a frontier half-edge by rotation (the resolved successor
   // chain), walk the loop on nx_l, keep the minimum id and the length.  Loops that touch
   // a deferred half-edge or a barrier tip (repaired later) are handed to the global
-  // seed walk.
+  // seed walk (bit-vector SDB).
   {
-    const uint32_t w = tid < kTileWords ? Sw[tid] : 0u;
-    int4 tot;
-    const int4 pre = block_scan4(make_int4(__popc(w), 0, 0, 0), &tot, scan_sm);
-    int p = pre.x;
-    for (uint32_t b = w; b; b &= b - 1) slist[p++] = (int16_t)(tid * 32 + __ffs(b) - 1);
-    __syncthreads();
-    for (int i = tid; i < tot.x; i += kTileThreads) {
+    const int nseed = scan_sm[0];
+    for (int i = tid; i < nseed; i += kTileThreads) {
       const int32_t sj = slist[i];
+#ifdef POLYLLA_TILE_WALKS
+      uint16_t r = succ[q_of(sj)];
+      for (int st = 0; !(r & (kSuccFront | kSuccUnknown)) && st < 15; ++st) r = succ[r];  // chains <= 16 (as the jumping)
+#else
       const uint16_t r = succ[q_of(sj)];  // the frontier half-edge the rotation reaches, if resolved
+#endif
       bool ok = (r & kSuccFront) != 0;
       int32_t mn = 0, n = 0;
       if (ok) {
@@ -533,64 +594,37 @@ __device__ __forceinline__ void tile_body(
   }
   __syncthreads();
   if (tid * 32 < nhe) {
-    C[(e0 >> 5) + tid] = Cw[tid];
-    wlen[(e0 >> 5) + tid] = Wl[tid];
-  }
-  PHASE_MARK(6);
-
-  // ---- P5: one global atomic per list per tile, then write the entries
-  uint32_t lw = 0, dw = 0, tw = 0, sw = 0;
-  if (tid < kTileWords) { lw = Lm[tid]; dw = Dm[tid]; tw = Tm[tid]; sw = SDm[tid]; }
-  int4 tot;
-  const int4 pre = block_scan4(make_int4(__popc(lw), __popc(dw), __popc(tw), __popc(sw)), &tot, scan_sm);
-  if (tid == 0) {
-    scan_sm[132] = tot.x ? atomicAdd(&ctr->n_left, tot.x) : 0;
-    scan_sm[133] = tot.y ? atomicAdd(&ctr->n_def, tot.y) : 0;
-    scan_sm[134] = tot.z ? atomicAdd(&ctr->n_tips, tot.z) : 0;
-    scan_sm[135] = tot.w ? atomicAdd(&ctr->n_sdef, tot.w) : 0;
-  }
-  __syncthreads();
-  int pl = scan_sm[132] + pre.x, pd = scan_sm[133] + pre.y, pt = scan_sm[134] + pre.z, ps = scan_sm[135] + pre.w;
-  while (lw) {
-    const int j = tid * 32 + __ffs(lw) - 1;
-    lw &= lw - 1;
-    const int q = q_of(j);
-    const int32_t o = tri_q[q], tg = tri_q[q + 1];
-    const uint64_t lo = (uint32_t)min(o, tg), hi = (uint32_t)max(o, tg);
-    left_key[pl] = (lo << 32) | hi;
-    left_e[pl++] = (int32_t)(e0 + j);
-  }
-  while (dw) {
-    def_e[pd++] = (int32_t)(e0 + tid * 32 + __ffs(dw) - 1);
-    dw &= dw - 1;
-  }
-  while (tw) {
-    tips[pt++] = (int32_t)(e0 + tid * 32 + __ffs(tw) - 1);
-    tw &= tw - 1;
-  }
-  while (sw) {
-    sdef[ps++] = (int32_t)(e0 + tid * 32 + __ffs(sw) - 1);
-    sw &= sw - 1;
+    const int64_t w = (e0 >> 5) + tid;
+    C[w] = Cw[tid];
+    wlen[w] = Wl[tid];
+    SDB[w] = SDm[tid];
   }
   PHASE_MARK(7);
 }
 
-// full tiles take the specialised body (constant trip counts, no bounds checks); the
-// ragged last tile the generic one
+// One CTA per tile; while it works it prefetches into L2 the triangles and vertex
+// coordinates of the tile that will start when it ends.  Full tiles take the specialised
+// body (constant trip counts, no bounds checks), the ragged last tile the generic one.
 __global__ void __launch_bounds__(kTileThreads, 2)
     k_tile(const double2* __restrict__ xy, const int32_t* __restrict__ tri, int64_t V, int64_t T,
            int32_t* __restrict__ origin, int32_t* __restrict__ twin, int32_t* __restrict__ next,
            uint8_t* __restrict__ lcode, uint32_t* __restrict__ F0, uint32_t* __restrict__ F1,
            uint32_t* __restrict__ S, uint32_t* __restrict__ C, int32_t* __restrict__ len, int32_t* __restrict__ wlen,
            unsigned long long* __restrict__ left_key, int32_t* __restrict__ left_e, int32_t* __restrict__ def_e,
-           int32_t* __restrict__ tips, int32_t* __restrict__ sdef, DevCounters* ctr) {
+           uint32_t* __restrict__ TB, uint32_t* __restrict__ SDB, int32_t* __restrict__ cnt_ld, DevCounters* ctr,
+           int64_t prefetch_dist) {
   extern __shared__ __align__(16) unsigned char smem_tile[];
-  if ((int64_t)(blockIdx.x + 1) * kTileTris <= T)
+  const int64_t ntiles = (T + kTileTris - 1) / kTileTris;
+  const int64_t tile = blockIdx.x;
+  // the tile that starts about when this one ends (blocks are dispatched in index order,
+  // kResident at a time): its data is prefetched into L2, which every SM shares
+  const int64_t nxt = tile + prefetch_dist < ntiles ? tile + prefetch_dist : -1;
+  if ((tile + 1) * kTileTris <= T)
     tile_body<true>(smem_tile, xy, tri, V, T, origin, twin, next, lcode, F0, F1, S, C, len, wlen, left_key, left_e,
-                    def_e, tips, sdef, ctr);
+                    def_e, TB, SDB, cnt_ld, ctr, tile, nxt);
   else
     tile_body<false>(smem_tile, xy, tri, V, T, origin, twin, next, lcode, F0, F1, S, C, len, wlen, left_key, left_e,
-                     def_e, tips, sdef, ctr);
+                     def_e, TB, SDB, cnt_ld, ctr, tile, nxt);
 }
 
 #ifdef POLYLLA_PHASE_TIMING
@@ -622,48 +656,56 @@ __global__ void k_hash_clear(DevCounters* ctr, uint32_t* ehash, int64_t cap_max)
   }
 }
 
-// global hash over leftover half-edges: pair the two halves of each cross-tile edge
-__global__ void k_left_insert(DevCounters* ctr, const unsigned long long* __restrict__ left_key,
-                              const int32_t* __restrict__ left_e, const int32_t* __restrict__ origin,
-                              int32_t* twin, uint32_t* ehash) {
+// global hash over leftover half-edges: pair the two halves of each cross-tile edge.
+// The leftovers of tile t are entries [3 * kTileTris * t, + cnt_ld[2t]) of left_key/left_e;
+// one block per tile segment (grid-stride over tiles).
+__global__ void k_left_insert(DevCounters* ctr, int64_t ntiles, const int32_t* __restrict__ cnt_ld,
+                              const unsigned long long* __restrict__ left_key, const int32_t* __restrict__ left_e,
+                              const int32_t* __restrict__ origin, int32_t* twin, uint32_t* ehash) {
   if (ctr->status) return;
-  const int32_t n = ctr->n_left;
   const uint32_t mask = (uint32_t)ctr->hash_cap - 1;
-  for (int32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
-    const unsigned long long key = left_key[i];
-    uint32_t h = mix32((uint32_t)(key >> 32), (uint32_t)key) & mask;
-    for (uint32_t probe = 0; probe <= mask; ++probe) {
-      uint32_t s = ehash[h];
-      if (s == kEmpty) {
-        const uint32_t old = atomicCAS(&ehash[h], kEmpty, (uint32_t)i);
-        if (old == kEmpty) break;
-        s = old;
-      }
-      const int32_t si = (int32_t)(s & ~kPaired);
-      if (left_key[si] == key) {
-        const int32_t ei = left_e[i], es = left_e[si];
-        if ((s & kPaired) || origin[ei] == origin[es] ||
-            atomicCAS(&ehash[h], s, s | kPaired) != s) {
-          raise_status(ctr, ST_NONMANIFOLD_EDGE);
+  for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+    const int32_t n = cnt_ld[2 * tile];
+    const int32_t base = (int32_t)(3 * kTileTris * tile);
+    for (int32_t k = threadIdx.x; k < n; k += blockDim.x) {
+      const int32_t i = base + k;
+      const unsigned long long key = left_key[i];
+      uint32_t h = mix32((uint32_t)(key >> 32), (uint32_t)key) & mask;
+      for (uint32_t probe = 0; probe <= mask; ++probe) {
+        uint32_t s = ehash[h];
+        if (s == kEmpty) {
+          const uint32_t old = atomicCAS(&ehash[h], kEmpty, (uint32_t)i);
+          if (old == kEmpty) break;
+          s = old;
+        }
+        const int32_t si = (int32_t)(s & ~kPaired);
+        if (left_key[si] == key) {
+          const int32_t ei = left_e[i], es = left_e[si];
+          if ((s & kPaired) || origin[ei] == origin[es] || atomicCAS(&ehash[h], s, s | kPaired) != s) {
+            raise_status(ctr, ST_NONMANIFOLD_EDGE);
+            break;
+          }
+          twin[ei] = es;
+          twin[es] = ei;
           break;
         }
-        twin[ei] = es;
-        twin[es] = ei;
-        break;
+        h = (h + 1) & mask;
       }
-      h = (h + 1) & mask;
     }
   }
 }
 
 // mark leftovers that found no partner: they lie on the domain boundary
-__global__ void k_left_unmatched(DevCounters* ctr, const int32_t* __restrict__ left_e,
-                                 const int32_t* __restrict__ twin, uint32_t* Bd) {
+__global__ void k_left_unmatched(DevCounters* ctr, int64_t ntiles, const int32_t* __restrict__ cnt_ld,
+                                 const int32_t* __restrict__ left_e, const int32_t* __restrict__ twin, uint32_t* Bd) {
   if (ctr->status) return;
-  const int32_t n = ctr->n_left;
-  for (int32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
-    const int32_t e = left_e[i];
-    if (twin[e] < 0) atomicOr(&Bd[e >> 5], 1u << (e & 31));
+  for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+    const int32_t n = cnt_ld[2 * tile];
+    const int32_t base = (int32_t)(3 * kTileTris * tile);
+    for (int32_t k = threadIdx.x; k < n; k += blockDim.x) {
+      const int32_t e = left_e[base + k];
+      if (twin[e] < 0) atomicOr(&Bd[e >> 5], 1u << (e & 31));
+    }
   }
 }
 
@@ -723,16 +765,32 @@ int launch_build(Ctx* c, cudaStream_t s) {
     attr = true;
   }
   prof_mark(s, "k_tile");
+  static int n_sm = 0;
+  if (!n_sm) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, dev);
+  }
+  // L2 prefetch distance in tiles (default: one per SM, measured best of {0, 148, 296, 444, 592} on config 3);
+  // POLYLLA_PREFETCH_DIST overrides it (<= 0 disables the prefetch) for experiments
+  static int64_t pf_dist = -1;
+  if (pf_dist < 0) {
+    const char* env = std::getenv("POLYLLA_PREFETCH_DIST");
+    pf_dist = env ? std::atoll(env) : (int64_t)n_sm;
+    if (pf_dist <= 0) pf_dist = int64_t(1) << 40;
+  }
   k_tile<<<(unsigned)tiles, kTileThreads, kTileSmem, s>>>(reinterpret_cast<const double2*>(c->xy), c->tri, c->V, c->T,
                                                           c->origin, c->twin, c->next, c->lcode, c->F0, c->F1, c->S,
-                                                          c->C, c->len, c->wlen, c->left_key, c->left_e, c->def_e, c->tips,
-                                                          c->sdef, c->ctr);
+                                                          c->C, c->len, c->wlen, c->left_key, c->left_e, c->def_e, c->TB,
+                                                          c->SDB, c->cnt_ld, c->ctr, pf_dist);
   ++n;
   const int grid = 148 * 32;  // enough threads for ~1 leftover each on 10M-vertex meshes (latency-bound)
   prof_mark(s, "k_left_match");
   k_hash_clear<<<grid, 256, 0, s>>>(c->ctr, c->ehash, c->hash_cap_max);
-  k_left_insert<<<grid, 256, 0, s>>>(c->ctr, c->left_key, c->left_e, c->origin, c->twin, c->ehash);
-  k_left_unmatched<<<grid, 256, 0, s>>>(c->ctr, c->left_e, c->twin, c->Bd);
+  const unsigned seg_grid = (unsigned)(tiles < 148 * 16 ? tiles : 148 * 16);
+  k_left_insert<<<seg_grid, 256, 0, s>>>(c->ctr, tiles, c->cnt_ld, c->left_key, c->left_e, c->origin, c->twin,
+                                         c->ehash);
+  k_left_unmatched<<<seg_grid, 256, 0, s>>>(c->ctr, tiles, c->cnt_ld, c->left_e, c->twin, c->Bd);
   n += 3;
   prof_mark(s, "k_border_scan");
   BorderOp op{c->Bd, c->origin, c->twin, c->vmap, c->ctr, 3 * c->T};

@@ -60,8 +60,10 @@ static Layout layout(int64_t V, int64_t T) {
       (size_t)(3 * T) * 4,    // 25 tri staging
       sizeof(DevCounters),    // 26 counters
       (size_t)(3 * T) * 4,    // 27 deferred half-edges
-      (size_t)(T + 1) * 4,    // 28 deferred seeds
+      (size_t)nw * 4,         // 28 SDB: seeds for the global seed walk
       (size_t)nw * 4,         // 29 per-word loop lengths
+      (size_t)nw * 4,         // 30 TB: barrier tips
+      (size_t)(2 * ((T + 2047) / 2048) + 2) * 4,  // 31 per-tile leftover / deferred counts
   };
   Layout L{};
   static_assert(sizeof(sz) / sizeof(sz[0]) <= sizeof(L.off) / sizeof(L.off[0]), "Layout::off too small");
@@ -109,7 +111,9 @@ bool carve(Ctx* c, void* ws, size_t bytes) {
   c->tri_stage = reinterpret_cast<int32_t*>(b + L.off[25]);
   c->ctr = reinterpret_cast<DevCounters*>(b + L.off[26]);
   c->def_e = reinterpret_cast<int32_t*>(b + L.off[27]);
-  c->sdef = reinterpret_cast<int32_t*>(b + L.off[28]);
+  c->SDB = reinterpret_cast<uint32_t*>(b + L.off[28]);
+  c->TB = reinterpret_cast<uint32_t*>(b + L.off[30]);
+  c->cnt_ld = reinterpret_cast<int32_t*>(b + L.off[31]);
   c->wlen = reinterpret_cast<int32_t*>(b + L.off[29]);
   c->n_words = (3 * c->T + 31) / 32;
   return true;

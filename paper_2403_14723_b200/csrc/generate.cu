@@ -2,14 +2,15 @@
 // ("Label extra seed and frontier edges" (Alg. 10), "Search frontier
 // edges for each seed edge" (Alg. 12), "Overwrite seeds", "Scan and compact").
 //
-//   k_repair_mid     one thread per barrier tip (found by the label pass as next == twin):
+//   k_repair_mid     one thread per barrier tip (bit-vector TB, set where next == twin):
 //                    d = degree(v); m = sweep_out^k(e0), k = floor((d-1)/2) (R5) from the
 //                    tip's outgoing frontier half-edge e0; F1[m] = F1[twin m] = 1; both
-//                    halves become seeds (mids list).  Topology only -> snapshot (R6).
+//                    halves become seeds (bit-vector SDB).  Topology only -> snapshot (R6).
 //   k_repair_rewire  one thread per touched vertex w (the tip v and the far end u of m):
 //                    recompute next[p] for every incoming frontier half-edge p of w with
 //                    the F1 bits (the only next values repair can change).
-//   k_seed_walk      one thread per seed k_tile deferred + the repair seeds: rotate to the first frontier
+//   k_seed_walk      one thread per seed of SDB (deferred by k_tile / the fixup, repair
+//                    halves; expanded per warp into a shared queue): rotate to the first frontier
 //                    half-edge (Alg. 12), walk the polygon through next, keep the minimum
 //                    id as the canonical seed and its loop length (Overwrite seeds,
 //                    PAPER.md L816).  Duplicate walks of one polygon write the same values.
@@ -24,13 +25,22 @@ __device__ __forceinline__ bool f1_of(const uint32_t* __restrict__ F1, int64_t T
   return x >= T3 || bit_of(F1, x);
 }
 
-__global__ void k_repair_mid(int64_t T, const int32_t* __restrict__ twin, uint32_t* F1, const int32_t* __restrict__ tips,
-                             int32_t* __restrict__ mids, int32_t* __restrict__ aff, DevCounters* ctr) {
+// The tips of the bit-vector TB (set by k_tile and the label fixup), balanced over warps
+// (warp_foreach_bit) and compacted (one atomic per round of 32) into tips[] / aff[].
+constexpr int kRepairThreads = 128;
+__global__ void __launch_bounds__(kRepairThreads)
+    k_repair_mid(int64_t T, int64_t n_words, const uint32_t* __restrict__ TB, const int32_t* __restrict__ twin,
+                 uint32_t* F1, uint32_t* SDB, int32_t* __restrict__ tips, int32_t* __restrict__ aff, DevCounters* ctr) {
+  __shared__ int32_t queue[kRepairThreads / 32][kBitQueue];
   if (ctr->status) return;
   const int64_t T3 = 3 * T;
-  const int32_t n = ctr->n_tips;
-  for (int32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
-    const int32_t e = tips[i];
+  const int lane = threadIdx.x & 31;
+  warp_foreach_bit(TB, n_words, queue[threadIdx.x >> 5], [&](int32_t e, bool valid) {
+    const uint32_t m32 = __ballot_sync(0xffffffffu, valid);
+    int base = 0;
+    if (lane == 0) base = atomicAdd(&ctr->n_tips, __popc(m32));
+    const int i = __shfl_sync(0xffffffffu, base, 0) + __popc(m32 & ((1u << lane) - 1));
+    if (!valid) return;
     const int32_t e0 = twin[e];  // the tip's only outgoing frontier half-edge
     int32_t x = e0, d = 0;
     bool ok = true;
@@ -39,17 +49,22 @@ __global__ void k_repair_mid(int64_t T, const int32_t* __restrict__ twin, uint32
       if (tx >= T3 || ++d > kWalkBound) { ok = false; break; }
       x = next_in(tx);
     } while (x != e0);
-    if (!ok) { raise_status(ctr, ST_WALK); continue; }
+    tips[i] = e;
+    if (!ok) {
+      raise_status(ctr, ST_WALK);
+      aff[2 * i] = aff[2 * i + 1] = e0;
+      return;
+    }
     int32_t m = e0;
     for (int k = 0; k < (d - 1) / 2; ++k) m = next_in(twin[m]);  // CWvertexEdge steps (R1, R5)
     const int32_t tm = twin[m];
     atomicOr(&F1[m >> 5], 1u << (m & 31));
     atomicOr(&F1[tm >> 5], 1u << (tm & 31));
-    mids[2 * i] = m;
-    mids[2 * i + 1] = tm;
+    atomicOr(&SDB[m >> 5], 1u << (m & 31));  // both halves seed the split polygons
+    atomicOr(&SDB[tm >> 5], 1u << (tm & 31));
     aff[2 * i] = e0;     // outgoing from v
     aff[2 * i + 1] = tm; // outgoing from u = target(m)
-  }
+  });
 }
 
 __global__ void k_repair_rewire(int64_t T, const int32_t* __restrict__ twin, const uint32_t* __restrict__ F1,
@@ -101,18 +116,21 @@ __device__ __forceinline__ void process_seed(int32_t s, int64_t T3, int64_t H, c
   if (!(atomicOr(&C[mn >> 5], bit) & bit)) atomicAdd(&wlen[mn >> 5], (int32_t)n);  // first setter only
 }
 
-// the seeds k_tile could not close inside their tile, plus both halves of every middle
-// edge of the repair (they seed the split polygons)
+// The seeds of the bit-vector SDB: those k_tile could not close inside their tile, those
+// the label fixup found, and both halves of every middle edge of the repair; balanced
+// over warps (warp_foreach_bit), one seed per lane.
 __global__ void __launch_bounds__(kSeedThreads)
-    k_seed_walk(int64_t T, const int32_t* __restrict__ twin, const int32_t* __restrict__ next,
-                const uint32_t* __restrict__ F1, const int32_t* __restrict__ sdef, const int32_t* __restrict__ mids,
-                uint32_t* C, int32_t* len, int32_t* wlen, DevCounters* ctr) {
+    k_seed_walk(int64_t T, int64_t n_words, const uint32_t* __restrict__ SDB, const int32_t* __restrict__ twin,
+                const int32_t* __restrict__ next, const uint32_t* __restrict__ F1, uint32_t* C, int32_t* len,
+                int32_t* wlen, DevCounters* ctr) {
+  __shared__ int32_t queue[kSeedThreads / 32][kBitQueue];
   if (ctr->status) return;
   const int64_t T3 = 3 * T;
   const int64_t H = T3 + ctr->n_border;
-  const int32_t ns = ctr->n_sdef, nm = 2 * ctr->n_tips;
-  for (int32_t j = blockIdx.x * kSeedThreads + threadIdx.x; j < ns + nm; j += gridDim.x * kSeedThreads)
-    process_seed(j < ns ? sdef[j] : mids[j - ns], T3, H, twin, next, F1, C, len, wlen, ctr);
+  const int n = warp_foreach_bit(SDB, n_words, queue[threadIdx.x >> 5], [&](int32_t s, bool valid) {
+    if (valid) process_seed(s, T3, H, twin, next, F1, C, len, wlen, ctr);
+  });
+  if ((threadIdx.x & 31) == 0 && n) atomicAdd(&ctr->n_sdef, n);
 }
 
 struct CanonOp {
@@ -145,11 +163,11 @@ int launch_generate(Ctx* c, cudaStream_t s) {
   int n = 0;
   if (c->next_pre) cudaMemcpyAsync(c->next_pre, c->next, (size_t)c->Hmax * 4, cudaMemcpyDeviceToDevice, s);
   prof_mark(s, "k_repair");
-  k_repair_mid<<<148 * 16, 128, 0, s>>>(c->T, c->twin, c->F1, c->tips, c->mids, c->aff, c->ctr);
+  k_repair_mid<<<148 * 12, kRepairThreads, 0, s>>>(c->T, c->n_words, c->TB, c->twin, c->F1, c->SDB, c->tips, c->aff, c->ctr);
   k_repair_rewire<<<148 * 32, 128, 0, s>>>(c->T, c->twin, c->F1, c->aff, c->next, c->ctr);
   prof_mark(s, "k_seed_walk");
   // (the canonical bit-vector C was written in full by k_tile; global walks OR into it)
-  k_seed_walk<<<148 * 8, kSeedThreads, 0, s>>>(c->T, c->twin, c->next, c->F1, c->sdef, c->mids, c->C, c->len,
+  k_seed_walk<<<148 * 8, kSeedThreads, 0, s>>>(c->T, c->n_words, c->SDB, c->twin, c->next, c->F1, c->C, c->len,
                                                c->wlen, c->ctr);
   n += 3;
   prof_mark(s, "k_canon_scan");

@@ -6,10 +6,12 @@
 //   F0, F1, S, C, Bd : uint32 bit-vectors over the interior half-edges [0, 3T)
 //                      (frontier before/after repair, seed, canonical seed, unmatched)
 //   len              : int32 [3T]  loop length, written only at canonical seeds
-//   leftover keys/ids, global edge hash, border-vertex map vmap[V], tips, mids, scan sums,
+//   TB, SDB          : uint32 bit-vectors: barrier tips, seeds for the global seed walk
+//   leftover keys/ids (per-tile segments), global edge hash, border-vertex map vmap[V], tips, mids, scan sums,
 //   seeds/offsets/loops staging, input staging (run_host).
 #pragma once
 #include <cstdint>
+#include <type_traits>
 #include <cuda_runtime.h>
 
 #include "polylla.h"
@@ -41,7 +43,7 @@ struct DevCounters {
   int32_t n_f1;      // #interior F1 half-edges
   uint32_t hash_cap; // capacity (pow2 <= 2^31) of the leftover hash for this run
   int32_t n_def;     // half-edges deferred by k_tile to the label fixup
-  int32_t n_sdef;    // seeds deferred by k_tile to the global seed walk
+  int32_t n_sdef;    // seeds walked by k_seed_walk (deferred + repair halves)
   int32_t pad[5];
 };
 
@@ -55,12 +57,14 @@ struct Ctx {
   int32_t *origin, *twin, *next;
   uint8_t* lcode;
   uint32_t *F0, *F1, *S, *C, *Bd;
-  int32_t* len;
+  int32_t* len;     // [3T] loop length, at canonical seeds
   int32_t* wlen;    // [n_words] sum of loop lengths of the canonical seeds of each C word
   unsigned long long* left_key;
   int32_t* left_e;
-  int32_t* def_e;   // [3T] half-edges deferred by k_tile
-  int32_t* sdef;    // [T] seeds deferred by k_tile
+  int32_t* def_e;   // [3T] half-edges deferred by k_tile (per-tile segments at 3 * tile * 2048)
+  uint32_t* SDB;    // [n_words] seeds for the global seed walk (deferred by k_tile / the fixup, repair halves)
+  uint32_t* TB;     // [n_words] barrier tips (incoming frontier half-edge e, next[e] == twin[e])
+  int32_t* cnt_ld;  // [2 * tiles] per-tile leftover / deferred counts
   uint32_t* ehash;  // leftover-edge hash slots [hash_cap_max] (capacity chosen on device)
   int32_t* vmap;    // [V] border half-edge leaving each border vertex (written at border vertices only)
   int64_t hash_cap_max;
@@ -126,5 +130,64 @@ __device__ __forceinline__ uint32_t mix32(uint32_t a, uint32_t b) {
 constexpr uint32_t kEmpty = 0xFFFFFFFFu;   // empty hash slot
 constexpr uint32_t kPaired = 0x80000000u;  // flag in hash slots (slot values < 2^31 - 1)
 constexpr int kWalkBound = 1 << 16;      // rotation bound (vertex degree)
+constexpr int kBuildTileTris = 2048;     // triangles per k_tile tile (list segments are 3 * 2048 wide)
+
+// Set bits of a bit-vector, balanced over warps: warp g of the grid scans a contiguous
+// range of words and expands the set bits into its shared queue q (kBitQueue entries).
+// Each full (or final) batch is handed over either in warp-uniform rounds of 32,
+// f(e, valid) with all lanes present (f may use warp collectives; valid is false on the
+// padding lanes of the last round), or -- if `batch` is given -- whole, batch(fill), for
+// the caller to schedule freely.  Returns the number of set bits this warp saw.
+constexpr int kBitQueue = 128;  // small: the walks that follow live on L1 hits (shared memory shrinks L1)
+struct NoBatch {
+  __device__ void operator()(int) const {}
+};
+template <class F, class B = NoBatch>
+__device__ __forceinline__ int warp_foreach_bit(const uint32_t* __restrict__ bv, int64_t n_words, int32_t* q, F f,
+                                                B batch = B()) {
+  constexpr bool kBatch = !std::is_same<B, NoBatch>::value;
+  const int lane = threadIdx.x & 31;
+  const int64_t nwarps = (int64_t)gridDim.x * (blockDim.x >> 5);
+  const int64_t gwarp = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  const int64_t per = ((n_words + nwarps - 1) / nwarps + 31) & ~int64_t(31);
+  const int64_t wb = gwarp * per, we = wb + per < n_words ? wb + per : n_words;
+  int fill = 0, seen = 0;
+  auto flush = [&]() {
+    __syncwarp();
+    if constexpr (kBatch) {
+      batch(fill);
+    } else {
+      for (int base = 0; base < fill; base += 32) f(base + lane < fill ? q[base + lane] : -1, base + lane < fill);
+    }
+    __syncwarp();
+    fill = 0;
+  };
+  for (int64_t w0 = wb; w0 < we; w0 += 32) {
+    const int64_t w = w0 + lane;
+    uint32_t bits = w < we ? bv[w] : 0u;
+    while (__any_sync(0xffffffffu, bits != 0u)) {
+      const int c = __popc(bits);
+      int incl = c;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int a = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += a;
+      }
+      const int tot = __shfl_sync(0xffffffffu, incl, 31);
+      if (fill + tot > kBitQueue && fill > 0) flush();
+      // append as many bits as fit (a dense group may need several passes)
+      const int room = kBitQueue - fill, excl = incl - c;
+      int take = room - excl;
+      take = take < 0 ? 0 : (take > c ? c : take);
+      for (int p = fill + excl, k = 0; k < take; ++k, bits &= bits - 1) q[p++] = (int32_t)(w * 32 + __ffs(bits) - 1);
+      const int added = tot < room ? tot : room;
+      fill += added;
+      seen += added;
+      if (fill == kBitQueue) flush();
+    }
+  }
+  if (fill) flush();
+  return seen;
+}
 
 }  // namespace polylla

@@ -23,76 +23,70 @@ __device__ __forceinline__ bool is_longest(const uint8_t* __restrict__ lcode, in
 
 // One thread per half-edge deferred by k_tile (its twin, or a twin met by its rotation
 // walk, lies outside the build tile).  Same computation as k_tile's P4, on the global
-// arrays; bit-vector words are completed with atomicOr.
+// arrays; bit-vector words (F0, F1, S, and TB / SDB: tips and seeds for the generate
+// phase) are completed with atomicOr.  The deferred half-edges of tile t are entries
+// [3 * 2048 * t, + cnt_ld[2t + 1]) of def_e; one block per tile segment.
 __global__ void __launch_bounds__(kLabelThreads)
-    k_label_fixup(int64_t T, const int32_t* __restrict__ def_e, const int32_t* __restrict__ twin,
-                  const uint8_t* __restrict__ lcode, int32_t* __restrict__ next, uint32_t* __restrict__ F0,
-                  uint32_t* __restrict__ F1, uint32_t* __restrict__ S, int32_t* __restrict__ tips,
-                  int32_t* __restrict__ sdef, DevCounters* ctr) {
+    k_label_fixup(int64_t T, int64_t ntiles, const int32_t* __restrict__ cnt_ld, const int32_t* __restrict__ def_e,
+                  const int32_t* __restrict__ twin, const uint8_t* __restrict__ lcode, int32_t* __restrict__ next,
+                  uint32_t* __restrict__ F0, uint32_t* __restrict__ F1, uint32_t* __restrict__ S,
+                  uint32_t* __restrict__ TB, uint32_t* __restrict__ SDB, DevCounters* ctr) {
   if (ctr->status) return;
   const int64_t T3 = 3 * T;
-  const int32_t n = ctr->n_def;
   const int lane = threadIdx.x & 31;
-  for (int32_t base = blockIdx.x * kLabelThreads; base < n; base += gridDim.x * kLabelThreads) {
-    const int32_t i = base + threadIdx.x;
-    bool tip = false, walk_err = false, sd = false, fr = false;
-    int32_t e = -1;
-    if (i < n) {
-      e = def_e[i];
-      const int32_t t = twin[e];
-      const bool tb = t >= T3;
-      const bool Le = is_longest(lcode, e);
-      const bool Lt = !tb && is_longest(lcode, t);
-      fr = tb || (!Le && !Lt);
-      sd = Le && (tb || (Lt && e < t));
-      int32_t nx = next_in(e);
-      if (fr) {
-        int32_t x = nx;
-        for (int steps = 0;; ++steps) {
-          const int32_t tx = twin[x];
-          if (tx >= T3) break;                                         // border edge: frontier
-          if (!is_longest(lcode, x) && !is_longest(lcode, tx)) break;  // frontier edge
-          x = next_in(tx);                                             // cross the edge (sweep_out)
-          if (steps > kWalkBound) { walk_err = true; break; }
+  for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+    const int32_t n = cnt_ld[2 * tile + 1];
+    const int32_t seg = (int32_t)(3 * kBuildTileTris * tile);
+    for (int32_t base = 0; base < n; base += kLabelThreads) {  // warp-uniform trip count
+      const int32_t i = base + threadIdx.x;
+      bool tip = false, walk_err = false, sd = false, fr = false;
+      int32_t e = -1;
+      if (i < n) {
+        e = def_e[seg + i];
+        const int32_t t = twin[e];
+        const bool tb = t >= T3;
+        const bool Le = is_longest(lcode, e);
+        const bool Lt = !tb && is_longest(lcode, t);
+        fr = tb || (!Le && !Lt);
+        sd = Le && (tb || (Lt && e < t));
+        int32_t nx = next_in(e);
+        if (fr) {
+          int32_t x = nx;
+          for (int steps = 0;; ++steps) {
+            const int32_t tx = twin[x];
+            if (tx >= T3) break;                                         // border edge: frontier
+            if (!is_longest(lcode, x) && !is_longest(lcode, tx)) break;  // frontier edge
+            x = next_in(tx);                                             // cross the edge (sweep_out)
+            if (steps > kWalkBound) { walk_err = true; break; }
+          }
+          nx = x;
+          tip = (x == t);
         }
-        nx = x;
-        tip = (x == t);
+        next[e] = nx;
       }
-      next[e] = nx;
+      // bit-vector words: deferred entries are in ascending order per tile, so
+      // neighbouring lanes usually share a word -> one atomicOr per distinct word
+      const uint32_t word = e >= 0 ? (uint32_t)(e >> 5) : 0xFFFFFFFFu;
+      const uint32_t peers = __match_any_sync(0xffffffffu, word);
+      const uint32_t bit = e >= 0 ? 1u << (e & 31) : 0u;
+      const uint32_t fbits = __reduce_or_sync(peers, fr ? bit : 0u);
+      const uint32_t sbits = __reduce_or_sync(peers, sd ? bit : 0u);
+      const uint32_t tbits = __reduce_or_sync(peers, tip ? bit : 0u);
+      if (e >= 0 && lane == __ffs(peers) - 1) {
+        if (fbits) { atomicOr(&F0[word], fbits); atomicOr(&F1[word], fbits); }
+        if (sbits) { atomicOr(&S[word], sbits); atomicOr(&SDB[word], sbits); }  // seeds found here: global walk
+        if (tbits) atomicOr(&TB[word], tbits);
+      }
+      if (walk_err) raise_status(ctr, ST_WALK);
     }
-    // bit-vector words: deferred entries are appended in ascending order per tile, so
-    // neighbouring lanes usually share a word -> one atomicOr per distinct word
-    const uint32_t word = e >= 0 ? (uint32_t)(e >> 5) : 0xFFFFFFFFu;
-    const uint32_t peers = __match_any_sync(0xffffffffu, word);
-    const uint32_t bit = e >= 0 ? 1u << (e & 31) : 0u;
-    const uint32_t fbits = __reduce_or_sync(peers, fr ? bit : 0u);
-    const uint32_t sbits = __reduce_or_sync(peers, sd ? bit : 0u);
-    if (e >= 0 && lane == __ffs(peers) - 1) {
-      if (fbits) { atomicOr(&F0[word], fbits); atomicOr(&F1[word], fbits); }
-      if (sbits) atomicOr(&S[word], sbits);
-    }
-    const uint32_t tm = __ballot_sync(0xffffffffu, tip);
-    if (tm) {
-      int pos = 0;
-      if (lane == 0) pos = atomicAdd(&ctr->n_tips, __popc(tm));
-      pos = __shfl_sync(0xffffffffu, pos, 0) + __popc(tm & ((1u << lane) - 1));
-      if (tip) tips[pos] = e;
-    }
-    const uint32_t sm = __ballot_sync(0xffffffffu, sd);  // seeds found here go to the global seed walk
-    if (sm) {
-      int pos = 0;
-      if (lane == 0) pos = atomicAdd(&ctr->n_sdef, __popc(sm));
-      pos = __shfl_sync(0xffffffffu, pos, 0) + __popc(sm & ((1u << lane) - 1));
-      if (sd) sdef[pos] = e;
-    }
-    if (walk_err) raise_status(ctr, ST_WALK);
   }
 }
 
 int launch_label(Ctx* c, cudaStream_t s) {
+  const int64_t tiles = (c->T + kBuildTileTris - 1) / kBuildTileTris;
   prof_mark(s, "k_label_fixup");
-  k_label_fixup<<<148 * 16, kLabelThreads, 0, s>>>(c->T, c->def_e, c->twin, c->lcode, c->next, c->F0, c->F1, c->S,
-                                                   c->tips, c->sdef, c->ctr);
+  k_label_fixup<<<(unsigned)(tiles < 148 * 16 ? tiles : 148 * 16), kLabelThreads, 0, s>>>(
+      c->T, tiles, c->cnt_ld, c->def_e, c->twin, c->lcode, c->next, c->F0, c->F1, c->S, c->TB, c->SDB, c->ctr);
   prof_end(s);
   return cudaGetLastError() == cudaSuccess ? 1 : -1;
 }

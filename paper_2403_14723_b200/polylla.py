@@ -15,7 +15,7 @@ import numpy as np
 import torch
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libpolylla.so")
+LIB_PATH = os.environ.get("POLYLLA_LIB") or os.path.join(_HERE, "libpolylla.so")  # override: A/B experiments
 
 STATUS = {
     0: "OK", -1: "INVALID_ARGUMENT", -2: "DANGLING_INDEX", -3: "DEGENERATE_TRI",
