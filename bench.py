@@ -174,8 +174,9 @@ def alg_bytes(T, V, P, L):
         "pipeline": 60 * T + 16 * V + 12 * L + 4 * P,
         # tri in + xy once + origin/twin/next out + Lcode out + F0/F1/S/C bit-vectors out
         "k_tile": 12 * T + 16 * V + 36 * T + T + 4 * (3 * T) // 8,
-        # seeds + offsets in, next + origin along the loops, loops + offsets out
-        "k_extract": 4 * P + 4 * (P + 1) + 8 * L + 4 * L + 4 * (P + 1),
+        # k_emit (profile group "k_extract"): C bits + len at the canonical seeds in, next +
+        # origin along the loops, seeds + offsets + loops out
+        "k_extract": (3 * T) // 8 + 4 * P + 8 * L + 4 * P + 4 * (P + 1) + 4 * L,
     }
 
 

@@ -28,22 +28,33 @@ constexpr int kTileTris = kBuildTileTris;
 constexpr int kTileHE = 3 * kTileTris;   // 6144 half-edges = 192 bit-vector words (e order)
 constexpr int kTileQ = 4 * kTileTris;    // quad slots q = 4t + k (slot 3: copy of vertex 0 / unused)
 constexpr int kTileSlots = 8192;         // pow2 hash slots (load ~0.38: only the lo->hi halves insert)
-constexpr int kTileThreads = 768;
+#ifndef POLYLLA_TILE_THREADS
+#define POLYLLA_TILE_THREADS 768
+#endif
+constexpr int kTileThreads = POLYLLA_TILE_THREADS;
 constexpr int kTileWords = kTileHE / 32; // 192
-constexpr int kTriIters = (kTileTris + kTileThreads - 1) / kTileThreads;  // 3 (the third: threads < 512)
-constexpr int kHeIters = kTileHE / kTileThreads;                           // 8 exactly
-static_assert(kTileHE % kTileThreads == 0 && kTileThreads % 96 == 0, "j = tid + 768 i  <=>  q = q_of(tid) + 1024 i");
+constexpr int kTriIters = (kTileTris + kTileThreads - 1) / kTileThreads;  // 768: 3 (the third: threads < 512)
+constexpr int kHeIters = kTileHE / kTileThreads;                           // 768: 8 exactly
+static_assert(kTileHE % kTileThreads == 0 && kTileThreads % 3 != 2, "half-edge loops: q_step below");
 static_assert(kTileThreads % 32 == 0 && (kTileTris - 2 * kTileThreads) % 32 == 0, "warp-uniform third triangle");
+// quad of half-edge j + kTileThreads from the quad q of j (no division): 768 = 3 * 256
+// -> q + 1024; 1024 = 3 * 341 + 1 -> q + 1365, skipping the padding slot k = 3
+constexpr int kQStep = 4 * (kTileThreads / 3) + kTileThreads % 3;
+__device__ __forceinline__ int q_step(int q) {
+  q += kQStep;
+  if (kTileThreads % 3 == 1 && (q & 3) == 3) ++q;
+  return q;
+}
 // shared memory (bytes):
 //   tri_q int32[kTileQ]   32768  quad layout (v0, v1, v2, v0): half-edge q runs tri_q[q] -> tri_q[q+1]
 //   tw_s  int16[kTileQ]   16384  twin as a quad index, -1 = outside the tile
-//   slot  u32[kTileSlots] 32768  (dead after P2: reused for succ u16[kTileQ] | Lm, Dm, SDm u32[192] | scratch, offL, offD)
+//   slot  u32[kTileSlots] 32768  (dead after P2: reused for succ u16[kTileQ] | scratch, offL, offD)
 //   lc_s  u8[kTileTris]    2048
-//   nx_l  int16[kTileHE] 12288 | Sw, Cw, Wl u32[192] 2304 | slist int16[kTileTris] 4096   (P4-P6)
+//   nx_l  int16[kTileHE] 12288 | Sw, Cw, Wl, Lm, Dm, SDm u32[192] 4608 | slist int16[kTileTris] 4096   (P4-P6)
 //         (P0-P1: the raw triangle tile int32[kTileHE], 24576)
 constexpr size_t kOffTw = kTileQ * 4, kOffSlot = kOffTw + kTileQ * 2, kOffLc = kOffSlot + kTileSlots * 4,
                  kOffNx = kOffLc + kTileTris,
-                 kNxBytes = kTileHE * 2 + 3 * (kTileHE / 8) + kTileTris * 2,  // P4-P6 arrays (18,688 B)
+                 kNxBytes = kTileHE * 2 + 6 * (kTileHE / 8) + kTileTris * 2,  // P4-P6 arrays (20,992 B)
                  kRawBytes = kTileHE * 4,                                      // P0-P1 raw tile (24,576 B)
                  kTileSmem = kOffNx + (kNxBytes > kRawBytes ? kNxBytes : kRawBytes);  // 108,544 B -> 2 CTAs/SM
 static_assert(2 * (kTileSmem + 1024) <= 228 * 1024, "two tiles per SM");
@@ -185,9 +196,9 @@ template <bool FULL>
 __device__ __forceinline__ void tile_body(
     unsigned char* smem_tile, const double2* __restrict__ xy, const int32_t* __restrict__ tri, int64_t V, int64_t T,
     int32_t* __restrict__ origin, int32_t* __restrict__ twin, int32_t* __restrict__ next, uint8_t* __restrict__ lcode,
-    uint32_t* __restrict__ F0, uint32_t* __restrict__ F1, uint32_t* __restrict__ S, uint32_t* __restrict__ C,
+    uint32_t* __restrict__ F0, int64_t bv_stride, uint32_t* __restrict__ C,
     int32_t* __restrict__ len, int32_t* __restrict__ wlen, unsigned long long* __restrict__ left_key,
-    int32_t* __restrict__ left_e, int32_t* __restrict__ def_e, uint32_t* __restrict__ TB, uint32_t* __restrict__ SDB,
+    int32_t* __restrict__ left_e, int32_t* __restrict__ def_e, uint32_t* __restrict__ SDB,
     int32_t* __restrict__ cnt_ld, DevCounters* ctr, int64_t tile, int64_t tile_next) {
   int32_t* tri_q = reinterpret_cast<int32_t*>(smem_tile);
   int4* tri_q4 = reinterpret_cast<int4*>(smem_tile);
@@ -195,16 +206,17 @@ __device__ __forceinline__ void tile_body(
   uint32_t* slot = reinterpret_cast<uint32_t*>(smem_tile + kOffSlot);
   uint8_t* lc_s = smem_tile + kOffLc;
   int16_t* nx_l = reinterpret_cast<int16_t*>(smem_tile + kOffNx);               // local next, -1: not walkable
+  // six word arrays in a row (P4b stores word wl of array r at Sw + r * kTileWords + wl)
   uint32_t* Sw = reinterpret_cast<uint32_t*>(smem_tile + kOffNx + kTileHE * 2);  // seed bits (e order)
   uint32_t* Cw = Sw + kTileWords;                                                // canonical seed bits
   int32_t* Wl = reinterpret_cast<int32_t*>(Cw + kTileWords);                     // loop lengths per C word
-  int16_t* slist = reinterpret_cast<int16_t*>(Wl + kTileWords);                 // compacted seeds
+  uint32_t* Lm = reinterpret_cast<uint32_t*>(Wl + kTileWords);                   // leftover bits
+  uint32_t* Dm = Lm + kTileWords;                                                // deferred bits
+  uint32_t* SDm = Dm + kTileWords;                                               // deferred seed bits
+  int16_t* slist = reinterpret_cast<int16_t*>(SDm + kTileWords);                // compacted seeds
   // overlays of the slot area (after P2)
   uint16_t* succ = reinterpret_cast<uint16_t*>(slot);
-  uint32_t* Lm = slot + kTileQ / 2;
-  uint32_t* Dm = Lm + kTileWords;
-  uint32_t* SDm = Dm + kTileWords;
-  int* scan_sm = reinterpret_cast<int*>(SDm + kTileWords);  // 136 ints + offL/offD [2 x 192]
+  int* scan_sm = reinterpret_cast<int*>(slot + kTileQ / 2);  // 136 ints + offL/offD [2 x 192]
 
   const int64_t f0 = tile * kTileTris;
   const int64_t f0n = tile_next * kTileTris;  // this CTA's next tile (prefetched), if tile_next >= 0
@@ -212,7 +224,7 @@ __device__ __forceinline__ void tile_body(
   const int nhe = 3 * nt;
   const int64_t e0 = 3 * f0;
   const int tid = threadIdx.x, lane = tid & 31;
-  const int q0 = q_of(tid);  // quad of half-edge j = tid; j + 768 i -> q0 + 1024 i
+  const int q0 = q_of(tid);  // quad of half-edge j = tid (then q_step per kTileThreads)
 #ifdef POLYLLA_PHASE_TIMING
   long long t_phase_ = clock64();
 #endif
@@ -385,8 +397,8 @@ __device__ __forceinline__ void tile_body(
   //   succ[x] = next_q(twin x)  otherwise (cross the non-frontier edge: sweep_out)
   nm = 0;
 #pragma unroll 4
-  for (int i = 0; i < kHeIters; ++i) {
-    const int j = tid + i * kTileThreads, q = q0 + 4 * 256 * i;
+  for (int i = 0, q = q0; i < kHeIters; ++i, q = q_step(q)) {
+    const int j = tid + i * kTileThreads;
     if (!FULL && j >= nhe) break;
     const int k = q & 3, t = q >> 2;
     const int32_t tq = tw_s[q];
@@ -413,9 +425,9 @@ __device__ __forceinline__ void tile_body(
   for (int round = 0; round < kTileJumps; ++round) {
     const uint16_t* src = (round & 1) ? succ_b : succ;
     uint16_t* dst = (round & 1) ? succ : succ_b;
+    int q = q0;
 #pragma unroll
-    for (int i = 0; i < kHeIters; ++i) {
-      const int q = q0 + 4 * 256 * i;
+    for (int i = 0; i < kHeIters; ++i, q = q_step(q)) {
       if (!FULL && tid + i * kTileThreads >= nhe) break;
       const uint16_t sc = src[q];
       dst[q] = (sc & (kSuccFront | kSuccUnknown)) ? sc : src[sc];
@@ -427,8 +439,8 @@ __device__ __forceinline__ void tile_body(
 
   // ---- P4b: per half-edge (e order): F / S words (Alg. 8-9), next (Alg. 11), tips
 #pragma unroll 2
-  for (int i = 0; i < kHeIters; ++i) {
-    const int j = tid + i * kTileThreads, q = q0 + 4 * 256 * i;
+  for (int i = 0, q = q0; i < kHeIters; ++i, q = q_step(q)) {
+    const int j = tid + i * kTileThreads;
     bool fr = false, sd = false, tip = false, deferred = false, left = false;
     int32_t nl_j = -1;
     if (FULL || j < nhe) {
@@ -467,20 +479,12 @@ __device__ __forceinline__ void tile_body(
     const uint32_t tm = __ballot_sync(0xffffffffu, tip), dm = __ballot_sync(0xffffffffu, deferred),
                    lm = __ballot_sync(0xffffffffu, left);
     const int wl = (j - lane) >> 5;  // tile-local word of this warp
-    if (lane == 0) {
-      if (FULL || j < nhe) {
-        const int64_t w = (e0 >> 5) + wl;
-        F0[w] = fw;
-        F1[w] = fw;
-        S[w] = sw;
-        TB[w] = tm;
-      }
-      Lm[wl] = lm;
-      Dm[wl] = dm;
-      Sw[wl] = sw;
-      Cw[wl] = 0u;
-      Wl[wl] = 0;
-      SDm[wl] = 0u;
+    // one store per lane: lanes 0-5 the shared words Sw, Cw, Wl, Lm, Dm, SDm; lanes 8-11
+    // the global words F0, F1, S, TB (equally spaced in the workspace, bv_stride words)
+    if (lane < 6) {
+      Sw[lane * kTileWords + wl] = lane == 0 ? sw : lane == 3 ? lm : lane == 4 ? dm : 0u;
+    } else if (lane >= 8 && lane < 12 && (FULL || j - lane < nhe)) {
+      F0[(int64_t)(lane - 8) * bv_stride + (e0 >> 5) + wl] = lane == 10 ? sw : lane == 11 ? tm : fw;
     }
   }
   __syncthreads();
@@ -608,10 +612,9 @@ __device__ __forceinline__ void tile_body(
 __global__ void __launch_bounds__(kTileThreads, 2)
     k_tile(const double2* __restrict__ xy, const int32_t* __restrict__ tri, int64_t V, int64_t T,
            int32_t* __restrict__ origin, int32_t* __restrict__ twin, int32_t* __restrict__ next,
-           uint8_t* __restrict__ lcode, uint32_t* __restrict__ F0, uint32_t* __restrict__ F1,
-           uint32_t* __restrict__ S, uint32_t* __restrict__ C, int32_t* __restrict__ len, int32_t* __restrict__ wlen,
+           uint8_t* __restrict__ lcode, uint32_t* __restrict__ F0, int64_t bv_stride, uint32_t* __restrict__ C, int32_t* __restrict__ len, int32_t* __restrict__ wlen,
            unsigned long long* __restrict__ left_key, int32_t* __restrict__ left_e, int32_t* __restrict__ def_e,
-           uint32_t* __restrict__ TB, uint32_t* __restrict__ SDB, int32_t* __restrict__ cnt_ld, DevCounters* ctr,
+           uint32_t* __restrict__ SDB, int32_t* __restrict__ cnt_ld, DevCounters* ctr,
            int64_t prefetch_dist) {
   extern __shared__ __align__(16) unsigned char smem_tile[];
   const int64_t ntiles = (T + kTileTris - 1) / kTileTris;
@@ -620,11 +623,11 @@ __global__ void __launch_bounds__(kTileThreads, 2)
   // kResident at a time): its data is prefetched into L2, which every SM shares
   const int64_t nxt = tile + prefetch_dist < ntiles ? tile + prefetch_dist : -1;
   if ((tile + 1) * kTileTris <= T)
-    tile_body<true>(smem_tile, xy, tri, V, T, origin, twin, next, lcode, F0, F1, S, C, len, wlen, left_key, left_e,
-                    def_e, TB, SDB, cnt_ld, ctr, tile, nxt);
+    tile_body<true>(smem_tile, xy, tri, V, T, origin, twin, next, lcode, F0, bv_stride, C, len, wlen, left_key, left_e,
+                    def_e, SDB, cnt_ld, ctr, tile, nxt);
   else
-    tile_body<false>(smem_tile, xy, tri, V, T, origin, twin, next, lcode, F0, F1, S, C, len, wlen, left_key, left_e,
-                     def_e, TB, SDB, cnt_ld, ctr, tile, nxt);
+    tile_body<false>(smem_tile, xy, tri, V, T, origin, twin, next, lcode, F0, bv_stride, C, len, wlen, left_key, left_e,
+                     def_e, SDB, cnt_ld, ctr, tile, nxt);
 }
 
 #ifdef POLYLLA_PHASE_TIMING
@@ -779,10 +782,12 @@ int launch_build(Ctx* c, cudaStream_t s) {
     pf_dist = env ? std::atoll(env) : (int64_t)n_sm;
     if (pf_dist <= 0) pf_dist = int64_t(1) << 40;
   }
+  const int64_t bv_stride = c->F1 - c->F0;  // F0, F1, S, TB are equally spaced (capi.cu layout)
+  if (c->S - c->F1 != bv_stride || c->TB - c->S != bv_stride) return -1;
   k_tile<<<(unsigned)tiles, kTileThreads, kTileSmem, s>>>(reinterpret_cast<const double2*>(c->xy), c->tri, c->V, c->T,
-                                                          c->origin, c->twin, c->next, c->lcode, c->F0, c->F1, c->S,
-                                                          c->C, c->len, c->wlen, c->left_key, c->left_e, c->def_e, c->TB,
-                                                          c->SDB, c->cnt_ld, c->ctr, pf_dist);
+                                                          c->origin, c->twin, c->next, c->lcode, c->F0, bv_stride, c->C,
+                                                          c->len, c->wlen, c->left_key, c->left_e, c->def_e, c->SDB,
+                                                          c->cnt_ld, c->ctr, pf_dist);
   ++n;
   const int grid = 148 * 32;  // enough threads for ~1 leftover each on 10M-vertex meshes (latency-bound)
   prof_mark(s, "k_left_match");

@@ -39,7 +39,7 @@ static Layout layout(int64_t V, int64_t T) {
       (size_t)nw * 4,         // 4 F0
       (size_t)nw * 4,         // 5 F1
       (size_t)nw * 4,         // 6 S
-      (size_t)nw * 4,         // 7 C
+      (size_t)nw * 4,         // 7 TB: barrier tips (F0, F1, S, TB equally spaced: k_tile stores them by offset)
       (size_t)nw * 4,         // 8 Bd
       (size_t)(3 * T) * 4,    // 9 len
       (size_t)(3 * T) * 8,    // 10 left_key
@@ -62,8 +62,10 @@ static Layout layout(int64_t V, int64_t T) {
       (size_t)(3 * T) * 4,    // 27 deferred half-edges
       (size_t)nw * 4,         // 28 SDB: seeds for the global seed walk
       (size_t)nw * 4,         // 29 per-word loop lengths
-      (size_t)nw * 4,         // 30 TB: barrier tips
+      (size_t)nw * 4,         // 30 C
       (size_t)(2 * ((T + 2047) / 2048) + 2) * 4,  // 31 per-tile leftover / deferred counts
+      (size_t)(3 * ((T + 2047) / 2048) + 2) * 4,  // 32 per-tile canonical-seed sums
+      (size_t)(2 * ((T + 2047) / 2048) + 2) * 4,  // 33 per-tile polygon / loop-entry bases
   };
   Layout L{};
   static_assert(sizeof(sz) / sizeof(sz[0]) <= sizeof(L.off) / sizeof(L.off[0]), "Layout::off too small");
@@ -90,7 +92,7 @@ bool carve(Ctx* c, void* ws, size_t bytes) {
   c->F0 = reinterpret_cast<uint32_t*>(b + L.off[4]);
   c->F1 = reinterpret_cast<uint32_t*>(b + L.off[5]);
   c->S = reinterpret_cast<uint32_t*>(b + L.off[6]);
-  c->C = reinterpret_cast<uint32_t*>(b + L.off[7]);
+  c->TB = reinterpret_cast<uint32_t*>(b + L.off[7]);
   c->Bd = reinterpret_cast<uint32_t*>(b + L.off[8]);
   c->len = reinterpret_cast<int32_t*>(b + L.off[9]);
   c->left_key = reinterpret_cast<unsigned long long*>(b + L.off[10]);
@@ -112,8 +114,10 @@ bool carve(Ctx* c, void* ws, size_t bytes) {
   c->ctr = reinterpret_cast<DevCounters*>(b + L.off[26]);
   c->def_e = reinterpret_cast<int32_t*>(b + L.off[27]);
   c->SDB = reinterpret_cast<uint32_t*>(b + L.off[28]);
-  c->TB = reinterpret_cast<uint32_t*>(b + L.off[30]);
+  c->C = reinterpret_cast<uint32_t*>(b + L.off[30]);
   c->cnt_ld = reinterpret_cast<int32_t*>(b + L.off[31]);
+  c->tsum = reinterpret_cast<int32_t*>(b + L.off[32]);
+  c->tbase = reinterpret_cast<int32_t*>(b + L.off[33]);
   c->wlen = reinterpret_cast<int32_t*>(b + L.off[29]);
   c->n_words = (3 * c->T + 31) / 32;
   return true;
@@ -350,8 +354,7 @@ POLYLLA_API polylla_status polylla_run_host(const double* xy_host, int64_t V, co
     polylla_destroy(p);
     return POLYLLA_E_CAPACITY;
   }
-  // extraction into the workspace staging, then exact-size D2H copies
-  // (the offsets are already final in the workspace; only the loops are extracted)
+  // extraction into the workspace staging (offsets and loops), then exact-size D2H copies
   polylla_status out = POLYLLA_OK;
   if (launch_extract(c, nullptr, T + 1, c->loops, 3 * T, nullptr, s) < 0) out = POLYLLA_E_CUDA;
   if (cudaMemcpyAsync(offsets_host, c->offsets, (size_t)(P + 1) * 4, cudaMemcpyDeviceToHost, s) != cudaSuccess ||

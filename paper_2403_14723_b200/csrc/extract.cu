@@ -1,5 +1,7 @@
 // extract.cu -- polygon extraction ("the seed list is used to rebuild
-// each polygon of the output mesh using the next ... queries"), moved on-device:
+// each polygon of the output mesh using the next ... queries"), moved on-device and
+// fused with the last step of "Scan and compact":
+//   seeds[p] = p-th canonical seed, offsets[p] = sum of the earlier loop lengths,
 //   loops[offsets[p] + i] = origin[x_i], x_0 = seeds[p], x_{i+1} = next[x_i]   (CSR)
 // plus the optional prev array: the inverse of next on frontier and border
 // half-edges (their next is a permutation of them), prev_in on the others.
@@ -7,28 +9,121 @@
 
 namespace polylla {
 
-__global__ void k_extract(const int32_t* __restrict__ seeds, const int32_t* __restrict__ offs_in,
-                          const int32_t* __restrict__ origin, const int32_t* __restrict__ next,
-                          int32_t* __restrict__ offsets, int64_t offsets_cap, int32_t* __restrict__ loops,
-                          int64_t loops_cap, DevCounters* ctr) {
+// One CTA per build tile (kBuildTileTris triangles = 192 words of 32 half-edges):
+// warp 0 ranks the words' canonical seeds (C bits) on top of the tile base of
+// k_tiles_scan; the seeds are expanded in rank order into a shared queue with their
+// loop lengths (len), a block scan turns the lengths into offsets, and each thread then
+// walks one polygon: offsets/seeds at the polygon's rank, the loop's vertex ids from
+// its canonical seed (the tile's next/origin lines stay in L1 across the CTA's walks).
+// Polygons come out in ascending canonical-seed order.
+constexpr int kEmitWords = 3 * kBuildTileTris / 32;  // 192
+constexpr int kEmitThreads = 256;
+constexpr int kEmitQ = 2048;  // queue capacity (polygons per tile; a tile with more walks per word)
+
+__global__ void __launch_bounds__(kEmitThreads)
+    k_emit(int64_t T, int64_t n_words, const uint32_t* __restrict__ C, const int32_t* __restrict__ len,
+           const int32_t* __restrict__ tb, const int32_t* __restrict__ origin, const int32_t* __restrict__ next,
+           int32_t* __restrict__ seeds, int32_t* __restrict__ offsets, int64_t offsets_cap, int32_t* __restrict__ loops,
+           int64_t loops_cap, DevCounters* ctr) {
+  __shared__ int32_t qe[kEmitQ], qo[kEmitQ];
+  __shared__ int32_t wbase[kEmitWords];
+  __shared__ int32_t chunk[kEmitThreads / 32 + 1];
+  __shared__ int32_t npoly;
   if (ctr->status) return;
-  const int32_t P = ctr->P;
-  const int32_t L = ctr->L;
+  const int32_t P = ctr->P, L = ctr->L;
   if ((int64_t)P + 1 > offsets_cap || (int64_t)L > loops_cap) {
     if (blockIdx.x == 0 && threadIdx.x == 0) raise_status(ctr, ST_CAPACITY);
     return;
   }
-  for (int32_t p = blockIdx.x * blockDim.x + threadIdx.x; p <= P; p += gridDim.x * blockDim.x) {
-    const int32_t o = offs_in[p];
-    if (offsets) offsets[p] = o;
-    if (p == P) break;
-    const int32_t n = offs_in[p + 1] - o;
-    int32_t x = seeds[p];
-    for (int32_t i = 0; i < n; ++i) {
-      loops[o + i] = origin[x];
-      x = next[x];
+  const int64_t tile = blockIdx.x;
+  const int64_t wt = tile * kEmitWords;  // first word of the tile
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  if (warp == 0) {  // per-word exclusive prefix of the canonical-seed count
+    constexpr int kWPL = kEmitWords / 32;  // 6
+    int cp[kWPL], sp = 0;
+#pragma unroll
+    for (int k = 0; k < kWPL; ++k) {
+      const int64_t ww = wt + kWPL * lane + k;
+      cp[k] = ww < n_words ? __popc(C[ww]) : 0;
+      sp += cp[k];
+    }
+    int ip = sp;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int a = __shfl_up_sync(0xffffffffu, ip, o);
+      if (lane >= o) ip += a;
+    }
+    int bp = ip - sp;
+#pragma unroll
+    for (int k = 0; k < kWPL; ++k) {
+      wbase[kWPL * lane + k] = bp;
+      bp += cp[k];
+    }
+    if (lane == 31) npoly = ip;
+  }
+  __syncthreads();
+  const int np = npoly;
+  const int32_t rbase = tb[2 * tile], obase = tb[2 * tile + 1];
+  if (np > kEmitQ) {  // (dense tile) one thread per word walks its polygons in order
+    for (int wl = tid; wl < kEmitWords && wt + wl < n_words; wl += kEmitThreads) {
+      // offset of the word's first polygon: tile base + lengths of the earlier polygons
+      int32_t o = obase;
+      for (int64_t ww = wt; ww < wt + wl; ++ww)
+        for (uint32_t b = C[ww]; b; b &= b - 1) o += len[ww * 32 + __ffs(b) - 1];
+      int32_t r = rbase + wbase[wl];
+      for (uint32_t b = C[wt + wl]; b; b &= b - 1, ++r) {
+        const int32_t e = (int32_t)((wt + wl) * 32 + __ffs(b) - 1);
+        const int32_t n = len[e];
+        seeds[r] = e;
+        offsets[r] = o;
+        int32_t x = e;
+        for (int32_t i = 0; i < n; ++i, x = next[x]) loops[o + i] = origin[x];
+        o += n;
+      }
+    }
+  } else {
+    // expand the seeds into the queue (rank order) with their loop lengths
+    for (int wl = tid; wl < kEmitWords && wt + wl < n_words; wl += kEmitThreads) {
+      int p = wbase[wl];
+      for (uint32_t b = C[wt + wl]; b; b &= b - 1, ++p) {
+        const int32_t e = (int32_t)((wt + wl) * 32 + __ffs(b) - 1);
+        qe[p] = e;
+        qo[p] = len[e];
+      }
+    }
+    __syncthreads();
+    // exclusive scan of the lengths: thread t owns queue entries [t*per, (t+1)*per)
+    const int per = (np + kEmitThreads - 1) / kEmitThreads;
+    const int q0 = tid * per, q1 = min(q0 + per, np);
+    int sum = 0;
+    for (int i = q0; i < q1; ++i) sum += qo[i];
+    int inc = sum;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int a = __shfl_up_sync(0xffffffffu, inc, o);
+      if (lane >= o) inc += a;
+    }
+    if (lane == 31) chunk[warp] = inc;
+    __syncthreads();
+    if (tid == 0) {
+      int acc = 0;
+      for (int k = 0; k < kEmitThreads / 32; ++k) { const int v = chunk[k]; chunk[k] = acc; acc += v; }
+    }
+    __syncthreads();
+    int run = obase + chunk[warp] + inc - sum;
+    for (int i = q0; i < q1; ++i) { const int n = qo[i]; qo[i] = run; run += n; }
+    __syncthreads();
+    // one polygon per thread
+    for (int i = tid; i < np; i += kEmitThreads) {
+      const int32_t e = qe[i], o = qo[i];
+      const int32_t n = len[e];
+      seeds[rbase + i] = e;
+      offsets[rbase + i] = o;
+      int32_t x = e;
+      for (int32_t k = 0; k < n; ++k, x = next[x]) loops[o + k] = origin[x];
     }
   }
+  if (tile == gridDim.x - 1 && tid == 0) offsets[P] = L;
 }
 
 __global__ void k_prev(int64_t T, const int32_t* __restrict__ next, const uint32_t* __restrict__ F1,
@@ -47,8 +142,13 @@ int launch_extract(Ctx* c, int32_t* offsets, int64_t offsets_cap, int32_t* loops
                    int32_t* prev, cudaStream_t s) {
   int n = 0;
   prof_mark(s, "k_extract");
-  if (loops) k_extract<<<148 * 8, 256, 0, s>>>(c->seeds, c->offsets, c->origin, c->next, offsets, offsets_cap, loops, loops_cap,
-                                    c->ctr), ++n;
+  if (loops) {
+    const int64_t tiles = (c->T + kBuildTileTris - 1) / kBuildTileTris;
+    k_emit<<<(unsigned)tiles, kEmitThreads, 0, s>>>(c->T, c->n_words, c->C, c->len, c->tbase, c->origin, c->next,
+                                                   c->seeds, offsets ? offsets : c->offsets,
+                                                   offsets ? offsets_cap : c->T + 1, loops, loops_cap, c->ctr);
+    ++n;
+  }
   if (prev) {
     k_prev<<<148 * 16, 256, 0, s>>>(c->T, c->next, c->F1, prev, c->ctr);
     ++n;

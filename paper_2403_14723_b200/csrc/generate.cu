@@ -14,10 +14,10 @@
 //                    half-edge (Alg. 12), walk the polygon through next, keep the minimum
 //                    id as the canonical seed and its loop length (Overwrite seeds,
 //                    PAPER.md L816).  Duplicate walks of one polygon write the same values.
-//   canon scan       ascending canonical seeds -> seeds[P]; exclusive scan of lengths ->
-//                    offsets[P+1]; checks sum(len) == #interior F1 half-edges (R12).
+//   canon scan       per build tile: #canonical seeds, sum of their loop lengths, #F1;
+//                    one block scans the tiles (k_emit finishes ranks and offsets inside
+//                    each tile); checks sum(len) == #interior F1 half-edges (R12).
 #include "internal.cuh"
-#include "scan.cuh"
 
 namespace polylla {
 
@@ -133,31 +133,91 @@ __global__ void __launch_bounds__(kSeedThreads)
   if ((threadIdx.x & 31) == 0 && n) atomicAdd(&ctr->n_sdef, n);
 }
 
-struct CanonOp {
-  const uint32_t* C;
-  const uint32_t* F1;
-  const int32_t* len;
-  const int32_t* wlen;
-  int32_t* seeds;
-  int32_t* offsets;
-  DevCounters* ctr;
-  __device__ bool skip() const { return ctr->status != 0; }
-  __device__ uint32_t word(int64_t w) const { return C[w]; }
-  __device__ long long aux(int32_t e) const { return len[e]; }
-  __device__ long long word_aux(int64_t w, uint32_t) const { return wlen[w]; }  // dense per-word sums
-  __device__ long long extra(int64_t w) const { return __popc(F1[w]); }
-  __device__ void finish(long long P, long long L, long long nf1) const {
-    ctr->P = (int32_t)P;
-    ctr->L = (int32_t)L;
-    ctr->n_f1 = (int32_t)nf1;
-    if (L != nf1) raise_status(ctr, ST_UNSEEDED);  // R12: a frontier loop without a seed
-    offsets[P] = (int32_t)L;
+// "Scan and compact" at tile granularity: per build tile (192 words
+// of 32 half-edges) the number of canonical seeds, the sum of their loop lengths and
+// the number of interior F1 half-edges; then one block scans the tiles.  The
+// per-polygon ranks and offsets are finished inside the tile by k_emit (extract.cu).
+constexpr int kTileWordsG = 3 * kBuildTileTris / 32;  // 192
+
+__global__ void k_canon_tiles(int64_t n_words, int64_t ntiles, const uint32_t* __restrict__ C,
+                              const int32_t* __restrict__ wlen, const uint32_t* __restrict__ F1, int32_t* __restrict__ ts,
+                              DevCounters* ctr) {
+  if (ctr->status) return;
+  const int lane = threadIdx.x & 31;
+  const int64_t nwarps = (int64_t)gridDim.x * (blockDim.x >> 5);
+  for (int64_t tile = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); tile < ntiles; tile += nwarps) {
+    int p = 0, l = 0, f = 0;
+    for (int k = lane; k < kTileWordsG; k += 32) {
+      const int64_t w = tile * kTileWordsG + k;
+      if (w < n_words) {
+        p += __popc(C[w]);
+        l += wlen[w];
+        f += __popc(F1[w]);
+      }
+    }
+    p = __reduce_add_sync(0xffffffffu, p);
+    l = __reduce_add_sync(0xffffffffu, l);
+    f = __reduce_add_sync(0xffffffffu, f);
+    if (lane == 0) {
+      ts[3 * tile] = p;
+      ts[3 * tile + 1] = l;
+      ts[3 * tile + 2] = f;
+    }
   }
-  __device__ void emit(int32_t e, long long rank, long long pre) const {
-    seeds[rank] = e;
-    offsets[rank] = (int32_t)pre;
+}
+
+// one block of kTopThreads: thread t owns a contiguous run of tiles; exclusive prefixes
+// of (polygons, loop entries) per tile -> tb[2 * tile + {0, 1}]; totals -> P, L; the
+// R12 check sum(len) == #interior F1 half-edges
+constexpr int kTopThreads = 1024;
+__global__ void __launch_bounds__(kTopThreads)
+    k_tiles_scan(int64_t ntiles, const int32_t* __restrict__ ts, int32_t* __restrict__ tb, int32_t* __restrict__ offsets,
+                 DevCounters* ctr) {
+  __shared__ long long wsum[3][kTopThreads / 32];
+  if (ctr->status) return;
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  const int64_t per = (ntiles + kTopThreads - 1) / kTopThreads;
+  const int64_t t0 = tid * per, t1 = t0 + per < ntiles ? t0 + per : ntiles;
+  long long p = 0, l = 0, f = 0;
+  for (int64_t t = t0; t < t1; ++t) { p += ts[3 * t]; l += ts[3 * t + 1]; f += ts[3 * t + 2]; }
+  long long ip = p, il = l, iff = f;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const long long a = __shfl_up_sync(0xffffffffu, ip, o), b = __shfl_up_sync(0xffffffffu, il, o),
+                    c = __shfl_up_sync(0xffffffffu, iff, o);
+    if (lane >= o) { ip += a; il += b; iff += c; }
   }
-};
+  if (lane == 31) { wsum[0][wid] = ip; wsum[1][wid] = il; wsum[2][wid] = iff; }
+  __syncthreads();
+  if (wid == 0) {
+    long long a = wsum[0][lane], b = wsum[1][lane], c = wsum[2][lane];
+    long long ia = a, ib = b, ic = c;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const long long x = __shfl_up_sync(0xffffffffu, ia, o), y = __shfl_up_sync(0xffffffffu, ib, o),
+                      z = __shfl_up_sync(0xffffffffu, ic, o);
+      if (lane >= o) { ia += x; ib += y; ic += z; }
+    }
+    wsum[0][lane] = ia - a;
+    wsum[1][lane] = ib - b;
+    wsum[2][lane] = ic - c;
+    if (lane == 31) {
+      ctr->P = (int32_t)ia;
+      ctr->L = (int32_t)ib;
+      ctr->n_f1 = (int32_t)ic;
+      if (ib != ic) raise_status(ctr, ST_UNSEEDED);  // R12: a frontier loop without a seed
+      offsets[ia] = (int32_t)ib;
+    }
+  }
+  __syncthreads();
+  long long bp = wsum[0][wid] + ip - p, bl = wsum[1][wid] + il - l;
+  for (int64_t t = t0; t < t1; ++t) {
+    tb[2 * t] = (int32_t)bp;
+    tb[2 * t + 1] = (int32_t)bl;
+    bp += ts[3 * t];
+    bl += ts[3 * t + 1];
+  }
+}
 
 int launch_generate(Ctx* c, cudaStream_t s) {
   int n = 0;
@@ -171,10 +231,10 @@ int launch_generate(Ctx* c, cudaStream_t s) {
                                                c->wlen, c->ctr);
   n += 3;
   prof_mark(s, "k_canon_scan");
-  CanonOp op{c->C, c->F1, c->len, c->wlen, c->seeds, c->offsets, c->ctr};
-  const int r = launch_scan(op, c->n_words, c->scan_a, c->scan_b, c->scan_c, s);
-  if (r < 0) return -1;
-  n += r;
+  const int64_t tiles = (c->T + kBuildTileTris - 1) / kBuildTileTris;
+  k_canon_tiles<<<(unsigned)((tiles + 7) / 8), 256, 0, s>>>(c->n_words, tiles, c->C, c->wlen, c->F1, c->tsum, c->ctr);
+  k_tiles_scan<<<1, kTopThreads, 0, s>>>(tiles, c->tsum, c->tbase, c->offsets, c->ctr);
+  n += 2;
   prof_end(s);
   return cudaGetLastError() == cudaSuccess ? n : -1;
 }

@@ -65,6 +65,8 @@ struct Ctx {
   uint32_t* SDB;    // [n_words] seeds for the global seed walk (deferred by k_tile / the fixup, repair halves)
   uint32_t* TB;     // [n_words] barrier tips (incoming frontier half-edge e, next[e] == twin[e])
   int32_t* cnt_ld;  // [2 * tiles] per-tile leftover / deferred counts
+  int32_t* tsum;    // [3 * tiles] per-tile #canonical seeds, sum of loop lengths, #F1
+  int32_t* tbase;   // [2 * tiles] per-tile exclusive prefix of polygons / loop entries
   uint32_t* ehash;  // leftover-edge hash slots [hash_cap_max] (capacity chosen on device)
   int32_t* vmap;    // [V] border half-edge leaving each border vertex (written at border vertices only)
   int64_t hash_cap_max;

@@ -336,9 +336,10 @@ class HostPipeline:
     results, three-stage pipelined (the copies are ~90% of the
     end-to-end time and PCIe is full duplex):
 
-        up stream      H2D(xy_i, tri_i) ---------------------> H2D(xy_{i+1}, ...)
-        compute stream           build/label/generate/CSR(i)
+        up stream      H2D(xy_i, tri_i) ----------> H2D(xy_{i+1}, ...)
+        compute stream           build/label/generate/CSR(i)      CSR(i+1) ...
         down stream                                      D2H(CSR_i, origin/twin/next_i)
+                                                         (overlaps H2D(i+1))
 
     Two slots (workspace + device inputs + CSR staging) alternate; CUDA events order the
     reuse of a slot.  Every step still moves its own inputs up and its own results down
@@ -394,6 +395,11 @@ class HostPipeline:
                 sl["xy"][:V].copy_(xy_h, non_blocking=True)
                 sl["tri"][:T].copy_(tri_h, non_blocking=True)
                 sl["ev_up"].record(self.up)
+            # drain mesh i-1 before mesh i's kernels are queued: its counts sync waits for
+            # its own kernels only, and its D2H then runs while H2D(i) is in flight
+            if pending is not None:
+                drain(pending)
+                pending = None
             self.comp.wait_event(sl["ev_up"])
             if sl["used"]:
                 self.comp.wait_event(sl["ev_down"])  # its workspace was downloaded
@@ -403,8 +409,6 @@ class HostPipeline:
             get_polygons(ctx, sl["offsets"], sl["loops"], stream=self.comp)
             sl["ev_comp"].record(self.comp)
             sl["used"] = True
-            if pending is not None:
-                drain(pending)
             pending = (i, sl, ctx)
         if pending is not None:
             drain(pending)
