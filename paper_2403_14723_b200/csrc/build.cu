@@ -13,14 +13,13 @@
 //     - frontier/seed classification and the unlink rewire of every half-edge whose
 //       rotation walk stays inside the tile (label.cu completes the others);
 //     - half-edges whose twin is outside the tile are appended to a leftover list.
-//   k_left_insert / k_left_unmatched  -- global hash over the leftovers only;
-//   border scan (scan.cuh)             -- border ids 3T + rank(e) (R9), twin/origin of
-//                                         border half-edges, border-vertex hash;
+//   k_left_insert                      -- global hash over the leftovers only;
+//   k_border_rank / _scan / _emit      -- border ids 3T + rank(e) (R9), twin/origin of
+//                                         border half-edges, border-vertex map;
 //   k_border_next                      -- next(b) = border half-edge leaving target(b).
 #include <cstdlib>
 
 #include "internal.cuh"
-#include "scan.cuh"
 
 namespace polylla {
 
@@ -297,7 +296,31 @@ __device__ __forceinline__ void tile_body(
   __syncthreads();
   PHASE_MARK(1);
 
+  // L2 prefetch of the coordinates of the next tile's vertices (its triangles were
+  // bulk-prefetched in P0), so that tile's P1 gathers hit L2 instead of HBM: one triangle
+  // per thread per P2 pass, its ids loaded at the start of the pass and the prefetches
+  // issued at its end (the loads' latency hides behind the pass)
+  const int64_t nn_pf = tile_next >= 0 ? (T - f0n < kTileTris ? T - f0n : kTileTris) : 0;
+  int32_t pf_v[3];
+  bool pf_ok = false;
+  auto pf_load = [&](int i) {
+    const int t = tid + i * kTileThreads;
+    pf_ok = t < nn_pf;
+    if (pf_ok) {
+      const int32_t* src = tri + 3 * (f0n + t);
+      pf_v[0] = __ldg(src); pf_v[1] = __ldg(src + 1); pf_v[2] = __ldg(src + 2);
+    }
+  };
+  auto pf_issue = [&]() {
+    if (pf_ok) {
+#pragma unroll
+      for (int k = 0; k < 3; ++k)
+        if ((uint64_t)pf_v[k] < (uint64_t)V) asm volatile("prefetch.global.L2::evict_last [%0];" ::"l"(xy + pf_v[k]));
+    }
+  };
+
   // ---- P2a: the lo->hi halves claim their home slot with a plain store (last writer wins)
+  pf_load(0);
 #pragma unroll
   for (int i = 0; i < kTriIters; ++i) {
     const int t = tid + i * kTileThreads;
@@ -311,8 +334,10 @@ __device__ __forceinline__ void tile_body(
       if (o < tg) st_relaxed(&slot[tile_pos(h)], (h & ~kSlotQ) | (uint32_t)(4 * t + k));
     }
   }
+  pf_issue();
   __syncthreads();
   // ... the losers of a home slot insert with CAS + linear probing (one merged loop per lane)
+  pf_load(1);
   uint32_t nm = 0;
   {
     uint32_t pend = 0;
@@ -337,8 +362,10 @@ __device__ __forceinline__ void tile_body(
       nm |= tile_insert_probe(slot, tri_q, q, (uint32_t)tri_q[q], (uint32_t)tri_q[q + 1]);
     }
   }
+  pf_issue();
   __syncthreads();
   // ---- P2b: the hi->lo halves find their twin: home slot probed by every lane, misses loop
+  if (kTriIters > 2) pf_load(2);
   {
     uint32_t pend = 0;
 #pragma unroll
@@ -374,22 +401,10 @@ __device__ __forceinline__ void tile_body(
       }
     }
   }
+  if (kTriIters > 2) pf_issue();
   if (nm) raise_status(ctr, nm);
   __syncthreads();
   PHASE_MARK(2);
-
-  // ---- prefetch the coordinates of the next tile's vertices into L2 (its triangles were
-  // bulk-prefetched in P0), so that tile's P1 gathers hit L2 instead of HBM
-  if (tile_next >= 0) {
-    const int64_t nn = T - f0n < kTileTris ? T - f0n : kTileTris;
-    for (int t = tid; t < nn; t += kTileThreads) {
-      const int32_t* src = tri + 3 * (f0n + t);
-      const int32_t a = __ldg(src), b = __ldg(src + 1), c = __ldg(src + 2);
-      if ((uint64_t)a < (uint64_t)V) asm volatile("prefetch.global.L2::evict_last [%0];" ::"l"(xy + a));
-      if ((uint64_t)b < (uint64_t)V) asm volatile("prefetch.global.L2::evict_last [%0];" ::"l"(xy + b));
-      if ((uint64_t)c < (uint64_t)V) asm volatile("prefetch.global.L2::evict_last [%0];" ::"l"(xy + c));
-    }
-  }
 
   // ---- P3: origin/twin out (coalesced); rotation successors:
   //   succ[x] = x | FRONT   if x is a frontier half-edge (walk ends there)
@@ -698,47 +713,113 @@ __global__ void k_left_insert(DevCounters* ctr, int64_t ntiles, const int32_t* _
   }
 }
 
-// mark leftovers that found no partner: they lie on the domain boundary
-__global__ void k_left_unmatched(DevCounters* ctr, int64_t ntiles, const int32_t* __restrict__ cnt_ld,
-                                 const int32_t* __restrict__ left_e, const int32_t* __restrict__ twin, uint32_t* Bd) {
+// Leftovers that found no partner lie on the domain boundary.  Border ids follow R9:
+// b = 3T + rank(e) over the unmatched interior half-edges in ascending order.  Each tile
+// segment is in ascending e order, so the rank is (border half-edges of the earlier
+// tiles) + (rank inside the segment):
+//   k_border_rank  one block per tile segment: the unmatched leftovers in segment order
+//                  -> blist (the dead leftover-key storage), their count -> bcnt[tile]
+//   k_border_scan  one block: exclusive prefix of bcnt over the tiles, B = the total
+//   k_border_emit  one block per tile segment: b = 3T + base + rank; twin/origin of b and
+//                  vmap[origin(b)] = b (written only at border vertices: never cleared;
+//                  k_border_next reads it only at border vertices and verifies it)
+constexpr int kSegThreads = 256;
+
+__global__ void __launch_bounds__(kSegThreads)
+    k_border_rank(DevCounters* ctr, int64_t ntiles, const int32_t* __restrict__ cnt_ld,
+                  const int32_t* __restrict__ left_e, const int32_t* __restrict__ twin, int32_t* __restrict__ blist,
+                  int32_t* __restrict__ bcnt) {
+  __shared__ int32_t wtot[kSegThreads / 32];
   if (ctr->status) return;
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
     const int32_t n = cnt_ld[2 * tile];
     const int32_t base = (int32_t)(3 * kTileTris * tile);
-    for (int32_t k = threadIdx.x; k < n; k += blockDim.x) {
-      const int32_t e = left_e[base + k];
-      if (twin[e] < 0) atomicOr(&Bd[e >> 5], 1u << (e & 31));
+    int carry = 0;
+    for (int32_t k0 = 0; k0 < n; k0 += kSegThreads) {  // block-uniform trip count
+      const int32_t k = k0 + threadIdx.x;
+      const int32_t e = k < n ? left_e[base + k] : -1;
+      const bool un = e >= 0 && twin[e] < 0;
+      const uint32_t m = __ballot_sync(0xffffffffu, un);
+      if (lane == 0) wtot[wid] = __popc(m);
+      __syncthreads();
+      int pre = carry, tot = 0;
+      for (int w = 0; w < kSegThreads / 32; ++w) {
+        if (w < wid) pre += wtot[w];
+        tot += wtot[w];
+      }
+      if (un) blist[base + pre + __popc(m & ((1u << lane) - 1))] = e;  // segment-local rank order
+      carry += tot;
+      __syncthreads();
     }
+    if (threadIdx.x == 0) bcnt[tile] = carry;
   }
 }
 
-// border records: b = 3T + rank(e) over unmatched interior e (R9); vmap[origin(b)] = b
-// (written only at border vertices, so it needs no clearing: k_border_next reads it only
-// at border vertices and verifies what it reads)
-struct BorderOp {
-  const uint32_t* Bd;
-  int32_t *origin, *twin;
-  int32_t* vmap;
-  DevCounters* ctr;
-  int64_t T3;
-  __device__ bool skip() const { return ctr->status != 0; }
-  __device__ uint32_t word(int64_t w) const { return Bd[w]; }
-  __device__ long long aux(int32_t) const { return 0; }
-  __device__ long long word_aux(int64_t, uint32_t) const { return 0; }
-  __device__ long long extra(int64_t) const { return 0; }
-  __device__ void finish(long long cnt, long long, long long) const {
-    if (T3 + cnt > 0x7fffffffLL) raise_status(ctr, ST_OVERFLOW);
-    ctr->n_border = (int32_t)cnt;
+constexpr int kBorderScanThreads = 1024;
+__global__ void __launch_bounds__(kBorderScanThreads)
+    k_border_scan(DevCounters* ctr, int64_t ntiles, int64_t T3, int32_t* bcnt) {
+  constexpr int NW = kBorderScanThreads / 32;
+  __shared__ int32_t wsum[NW];
+  if (ctr->status) return;
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  const int64_t per = ((ntiles + NW - 1) / NW + 31) & ~int64_t(31);
+  const int64_t t0 = wid * per, t1 = t0 + per < ntiles ? t0 + per : ntiles;
+  int sum = 0;
+  for (int64_t t = t0 + lane; t < t1; t += 32) sum += bcnt[t];
+  sum = __reduce_add_sync(0xffffffffu, sum);
+  if (lane == 0) wsum[wid] = sum;
+  __syncthreads();
+  if (wid == 0) {
+    const int v = wsum[lane];
+    int inc = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int a = __shfl_up_sync(0xffffffffu, inc, o);
+      if (lane >= o) inc += a;
+    }
+    wsum[lane] = inc - v;
+    if (lane == 31) {
+      if (T3 + inc > 0x7fffffffLL) raise_status(ctr, ST_OVERFLOW);
+      ctr->n_border = inc;
+    }
   }
-  __device__ void emit(int32_t e, long long rank, long long) const {
-    const int32_t b = (int32_t)(T3 + rank);
-    const int32_t v = origin[next_in(e)];  // origin(b) = target(e)
-    twin[e] = b;
-    twin[b] = e;
-    origin[b] = v;
-    vmap[v] = b;
+  __syncthreads();
+  int carry = wsum[wid];
+  for (int64_t tb0 = t0; tb0 < t1; tb0 += 32) {
+    const int64_t t = tb0 + lane;
+    const int v = t < t1 ? bcnt[t] : 0;
+    int inc = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int a = __shfl_up_sync(0xffffffffu, inc, o);
+      if (lane >= o) inc += a;
+    }
+    if (t < t1) bcnt[t] = carry + inc - v;  // in place: the exclusive base of the tile
+    carry += __shfl_sync(0xffffffffu, inc, 31);
   }
-};
+}
+
+__global__ void __launch_bounds__(kSegThreads)
+    k_border_emit(DevCounters* ctr, int64_t ntiles, int64_t T3, const int32_t* __restrict__ blist,
+                  const int32_t* __restrict__ bbase, int32_t* origin, int32_t* twin, int32_t* vmap) {
+  if (ctr->status) return;
+  const int32_t nb = ctr->n_border;
+  for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+    const int32_t b0 = bbase[tile];
+    const int32_t n = (tile + 1 < ntiles ? bbase[tile + 1] : nb) - b0;
+    const int32_t base = (int32_t)(3 * kTileTris * tile);
+    for (int32_t k = threadIdx.x; k < n; k += kSegThreads) {
+      const int32_t e = blist[base + k];
+      const int32_t b = (int32_t)(T3 + b0 + k);
+      const int32_t v = origin[next_in(e)];  // origin(b) = target(e)
+      twin[e] = b;
+      twin[b] = e;
+      origin[b] = v;
+      vmap[v] = b;
+    }
+  }
+}
 
 // next(b) = the border half-edge whose origin is target(b) = origin(twin(b)).  A vertex
 // with two outgoing border half-edges keeps only one of them in vmap: the other fails
@@ -761,7 +842,6 @@ int launch_build(Ctx* c, cudaStream_t s) {
   int n = 0;
   const int64_t tiles = (c->T + kTileTris - 1) / kTileTris;
   cudaMemsetAsync(c->ctr, 0, sizeof(DevCounters), s);
-  cudaMemsetAsync(c->Bd, 0, (size_t)c->n_words * 4, s);
   static bool attr = false;
   if (!attr) {
     cudaFuncSetAttribute(k_tile, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kTileSmem);
@@ -795,13 +875,14 @@ int launch_build(Ctx* c, cudaStream_t s) {
   const unsigned seg_grid = (unsigned)(tiles < 148 * 16 ? tiles : 148 * 16);
   k_left_insert<<<seg_grid, 256, 0, s>>>(c->ctr, tiles, c->cnt_ld, c->left_key, c->left_e, c->origin, c->twin,
                                          c->ehash);
-  k_left_unmatched<<<seg_grid, 256, 0, s>>>(c->ctr, tiles, c->cnt_ld, c->left_e, c->twin, c->Bd);
+  int32_t* blist = reinterpret_cast<int32_t*>(c->left_key);  // dead after k_left_insert
+  k_border_rank<<<seg_grid, kSegThreads, 0, s>>>(c->ctr, tiles, c->cnt_ld, c->left_e, c->twin, blist, c->bcnt);
   n += 3;
   prof_mark(s, "k_border_scan");
-  BorderOp op{c->Bd, c->origin, c->twin, c->vmap, c->ctr, 3 * c->T};
-  const int r = launch_scan(op, c->n_words, c->scan_a, c->scan_b, c->scan_c, s);
-  if (r < 0) return -1;
-  n += r;
+  k_border_scan<<<1, kBorderScanThreads, 0, s>>>(c->ctr, tiles, 3 * c->T, c->bcnt);
+  k_border_emit<<<seg_grid, kSegThreads, 0, s>>>(c->ctr, tiles, 3 * c->T, blist, c->bcnt, c->origin, c->twin,
+                                                 c->vmap);
+  n += 2;
   prof_mark(s, "k_border_next");
   k_border_next<<<grid, 256, 0, s>>>(c->ctr, 3 * c->T, c->origin, c->twin, c->vmap, c->next);
   ++n;

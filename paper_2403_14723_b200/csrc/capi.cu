@@ -40,7 +40,7 @@ static Layout layout(int64_t V, int64_t T) {
       (size_t)nw * 4,         // 5 F1
       (size_t)nw * 4,         // 6 S
       (size_t)nw * 4,         // 7 TB: barrier tips (F0, F1, S, TB equally spaced: k_tile stores them by offset)
-      (size_t)nw * 4,         // 8 Bd
+      (size_t)((T + 2047) / 2048 + 1) * 4,  // 8 per-tile border counts / bases
       (size_t)(3 * T) * 4,    // 9 len
       (size_t)(3 * T) * 8,    // 10 left_key
       (size_t)(3 * T) * 4,    // 11 left_e
@@ -93,7 +93,7 @@ bool carve(Ctx* c, void* ws, size_t bytes) {
   c->F1 = reinterpret_cast<uint32_t*>(b + L.off[5]);
   c->S = reinterpret_cast<uint32_t*>(b + L.off[6]);
   c->TB = reinterpret_cast<uint32_t*>(b + L.off[7]);
-  c->Bd = reinterpret_cast<uint32_t*>(b + L.off[8]);
+  c->bcnt = reinterpret_cast<int32_t*>(b + L.off[8]);
   c->len = reinterpret_cast<int32_t*>(b + L.off[9]);
   c->left_key = reinterpret_cast<unsigned long long*>(b + L.off[10]);
   c->left_e = reinterpret_cast<int32_t*>(b + L.off[11]);

@@ -17,7 +17,10 @@ namespace polylla {
 // its canonical seed (the tile's next/origin lines stay in L1 across the CTA's walks).
 // Polygons come out in ascending canonical-seed order.
 constexpr int kEmitWords = 3 * kBuildTileTris / 32;  // 192
-constexpr int kEmitThreads = 256;
+#ifndef POLYLLA_EMIT_THREADS
+#define POLYLLA_EMIT_THREADS 384  // measured 256/384/512 on configs 3 and 5
+#endif
+constexpr int kEmitThreads = POLYLLA_EMIT_THREADS;
 constexpr int kEmitQ = 2048;  // queue capacity (polygons per tile; a tile with more walks per word)
 
 __global__ void __launch_bounds__(kEmitThreads)

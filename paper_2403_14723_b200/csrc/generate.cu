@@ -166,28 +166,29 @@ __global__ void k_canon_tiles(int64_t n_words, int64_t ntiles, const uint32_t* _
   }
 }
 
-// one block of kTopThreads: thread t owns a contiguous run of tiles; exclusive prefixes
-// of (polygons, loop entries) per tile -> tb[2 * tile + {0, 1}]; totals -> P, L; the
-// R12 check sum(len) == #interior F1 half-edges
+// one block of kTopThreads: warp w owns a contiguous run of tiles, read 32 at a time
+// (coalesced); pass 1 sums each warp's run, the warp totals are scanned, pass 2 rescans
+// the run with its carry and writes the exclusive prefixes of (polygons, loop entries)
+// per tile -> tb[2 * tile + {0, 1}]; totals -> P, L; the R12 check sum(len) == #F1
 constexpr int kTopThreads = 1024;
 __global__ void __launch_bounds__(kTopThreads)
     k_tiles_scan(int64_t ntiles, const int32_t* __restrict__ ts, int32_t* __restrict__ tb, int32_t* __restrict__ offsets,
                  DevCounters* ctr) {
-  __shared__ long long wsum[3][kTopThreads / 32];
+  constexpr int NW = kTopThreads / 32;
+  __shared__ long long wsum[3][NW];
   if (ctr->status) return;
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
-  const int64_t per = (ntiles + kTopThreads - 1) / kTopThreads;
-  const int64_t t0 = tid * per, t1 = t0 + per < ntiles ? t0 + per : ntiles;
+  const int64_t per = ((ntiles + NW - 1) / NW + 31) & ~int64_t(31);
+  const int64_t t0 = wid * per, t1 = t0 + per < ntiles ? t0 + per : ntiles;
   long long p = 0, l = 0, f = 0;
-  for (int64_t t = t0; t < t1; ++t) { p += ts[3 * t]; l += ts[3 * t + 1]; f += ts[3 * t + 2]; }
-  long long ip = p, il = l, iff = f;
+  for (int64_t t = t0 + lane; t < t1; t += 32) { p += ts[3 * t]; l += ts[3 * t + 1]; f += ts[3 * t + 2]; }
 #pragma unroll
-  for (int o = 1; o < 32; o <<= 1) {
-    const long long a = __shfl_up_sync(0xffffffffu, ip, o), b = __shfl_up_sync(0xffffffffu, il, o),
-                    c = __shfl_up_sync(0xffffffffu, iff, o);
-    if (lane >= o) { ip += a; il += b; iff += c; }
+  for (int o = 16; o; o >>= 1) {
+    p += __shfl_xor_sync(0xffffffffu, p, o);
+    l += __shfl_xor_sync(0xffffffffu, l, o);
+    f += __shfl_xor_sync(0xffffffffu, f, o);
   }
-  if (lane == 31) { wsum[0][wid] = ip; wsum[1][wid] = il; wsum[2][wid] = iff; }
+  if (lane == 0) { wsum[0][wid] = p; wsum[1][wid] = l; wsum[2][wid] = f; }
   __syncthreads();
   if (wid == 0) {
     long long a = wsum[0][lane], b = wsum[1][lane], c = wsum[2][lane];
@@ -200,7 +201,6 @@ __global__ void __launch_bounds__(kTopThreads)
     }
     wsum[0][lane] = ia - a;
     wsum[1][lane] = ib - b;
-    wsum[2][lane] = ic - c;
     if (lane == 31) {
       ctr->P = (int32_t)ia;
       ctr->L = (int32_t)ib;
@@ -210,12 +210,22 @@ __global__ void __launch_bounds__(kTopThreads)
     }
   }
   __syncthreads();
-  long long bp = wsum[0][wid] + ip - p, bl = wsum[1][wid] + il - l;
-  for (int64_t t = t0; t < t1; ++t) {
-    tb[2 * t] = (int32_t)bp;
-    tb[2 * t + 1] = (int32_t)bl;
-    bp += ts[3 * t];
-    bl += ts[3 * t + 1];
+  long long cp = wsum[0][wid], cl = wsum[1][wid];
+  for (int64_t tb0 = t0; tb0 < t1; tb0 += 32) {
+    const int64_t t = tb0 + lane;
+    const int vp = t < t1 ? ts[3 * t] : 0, vl = t < t1 ? ts[3 * t + 1] : 0;
+    int ip = vp, il = vl;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int x = __shfl_up_sync(0xffffffffu, ip, o), y = __shfl_up_sync(0xffffffffu, il, o);
+      if (lane >= o) { ip += x; il += y; }
+    }
+    if (t < t1) {
+      tb[2 * t] = (int32_t)(cp + ip - vp);
+      tb[2 * t + 1] = (int32_t)(cl + il - vl);
+    }
+    cp += __shfl_sync(0xffffffffu, ip, 31);
+    cl += __shfl_sync(0xffffffffu, il, 31);
   }
 }
 

@@ -3,8 +3,8 @@
 // Data layout in HBM (all inside the caller's workspace, see carve() in capi.cu):
 //   origin/twin/next : int32 SoA [H_max], H_max = 6T (worst case B = 3T)
 //   lcode            : uint8 [T]   k* of each triangle (longest half-edge 3f+k*)
-//   F0, F1, S, C, Bd : uint32 bit-vectors over the interior half-edges [0, 3T)
-//                      (frontier before/after repair, seed, canonical seed, unmatched)
+//   F0, F1, S, C     : uint32 bit-vectors over the interior half-edges [0, 3T)
+//                      (frontier before/after repair, seed, canonical seed)
 //   len              : int32 [3T]  loop length, written only at canonical seeds
 //   TB, SDB          : uint32 bit-vectors: barrier tips, seeds for the global seed walk
 //   leftover keys/ids (per-tile segments), global edge hash, border-vertex map vmap[V], tips, mids, scan sums,
@@ -56,7 +56,7 @@ struct Ctx {
   // workspace views
   int32_t *origin, *twin, *next;
   uint8_t* lcode;
-  uint32_t *F0, *F1, *S, *C, *Bd;
+  uint32_t *F0, *F1, *S, *C;
   int32_t* len;     // [3T] loop length, at canonical seeds
   int32_t* wlen;    // [n_words] sum of loop lengths of the canonical seeds of each C word
   unsigned long long* left_key;
@@ -67,6 +67,7 @@ struct Ctx {
   int32_t* cnt_ld;  // [2 * tiles] per-tile leftover / deferred counts
   int32_t* tsum;    // [3 * tiles] per-tile #canonical seeds, sum of loop lengths, #F1
   int32_t* tbase;   // [2 * tiles] per-tile exclusive prefix of polygons / loop entries
+  int32_t* bcnt;    // [tiles] per-tile border half-edge count, then (in place) its base
   uint32_t* ehash;  // leftover-edge hash slots [hash_cap_max] (capacity chosen on device)
   int32_t* vmap;    // [V] border half-edge leaving each border vertex (written at border vertices only)
   int64_t hash_cap_max;
@@ -134,8 +135,8 @@ constexpr uint32_t kPaired = 0x80000000u;  // flag in hash slots (slot values < 
 constexpr int kWalkBound = 1 << 16;      // rotation bound (vertex degree)
 constexpr int kBuildTileTris = 2048;     // triangles per k_tile tile (list segments are 3 * 2048 wide)
 
-// Set bits of a bit-vector, balanced over warps: warp g of the grid scans a contiguous
-// range of words and expands the set bits into its shared queue q (kBitQueue entries).
+// Set bits of a bit-vector, spread over warps: warp g of the grid scans 32-word chunks
+// g, g + G, ... and expands the set bits into its shared queue q (kBitQueue entries).
 // Each full (or final) batch is handed over either in warp-uniform rounds of 32,
 // f(e, valid) with all lanes present (f may use warp collectives; valid is false on the
 // padding lanes of the last round), or -- if `batch` is given -- whole, batch(fill), for
@@ -151,8 +152,6 @@ __device__ __forceinline__ int warp_foreach_bit(const uint32_t* __restrict__ bv,
   const int lane = threadIdx.x & 31;
   const int64_t nwarps = (int64_t)gridDim.x * (blockDim.x >> 5);
   const int64_t gwarp = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
-  const int64_t per = ((n_words + nwarps - 1) / nwarps + 31) & ~int64_t(31);
-  const int64_t wb = gwarp * per, we = wb + per < n_words ? wb + per : n_words;
   int fill = 0, seen = 0;
   auto flush = [&]() {
     __syncwarp();
@@ -164,9 +163,11 @@ __device__ __forceinline__ int warp_foreach_bit(const uint32_t* __restrict__ bv,
     __syncwarp();
     fill = 0;
   };
-  for (int64_t w0 = wb; w0 < we; w0 += 32) {
+  // interleaved 32-word chunks: at any time the grid works inside one window of the mesh
+  // (nwarps * 1024 half-edges), which keeps the walks' next/twin lines in L2
+  for (int64_t w0 = gwarp * 32; w0 < n_words; w0 += nwarps * 32) {
     const int64_t w = w0 + lane;
-    uint32_t bits = w < we ? bv[w] : 0u;
+    uint32_t bits = w < n_words ? bv[w] : 0u;
     while (__any_sync(0xffffffffu, bits != 0u)) {
       const int c = __popc(bits);
       int incl = c;
