@@ -57,10 +57,17 @@ constexpr size_t kOffTw = kTileQ * 4, kOffSlot = kOffTw + kTileQ * 2, kOffLc = k
                  kRawBytes = kTileHE * 4,                                      // P0-P1 raw tile (24,576 B)
                  kTileSmem = kOffNx + (kNxBytes > kRawBytes ? kNxBytes : kRawBytes);  // 108,544 B -> 2 CTAs/SM
 static_assert(2 * (kTileSmem + 1024) <= 228 * 1024, "two tiles per SM");
+constexpr unsigned long long kLeftDown = 1ull << 63;  // leftover key: set if origin > target
 constexpr uint32_t kSlotQ = (1u << 13) - 1;       // slot = fingerprint(19 bits) << 13 | quad index
 // rotation successors (P3/P4): quad index in the low 13 bits, terminal flags above
 constexpr uint16_t kSuccIdx = 0x1FFF, kSuccFront = 0x4000, kSuccUnknown = 0x8000;
-constexpr int kTileJumps = 4;            // pointer-jumping rounds: chains up to 2^4 steps resolved in-tile
+#ifndef POLYLLA_TILE_JUMPS
+#define POLYLLA_TILE_JUMPS 2  // measured 0 (walks) / 2 / 4 on configs 3 and 5
+#endif
+// pointer-jumping rounds (even: the result ends in succ); each use of a successor then
+// follows up to kTileHops more jumped pointers, so chains up to 16 steps resolve in-tile
+constexpr int kTileJumps = POLYLLA_TILE_JUMPS;
+constexpr int kTileHops = (16 >> kTileJumps) - 1;
 
 #ifdef POLYLLA_PHASE_TIMING
 __device__ unsigned long long g_phase_cycles[16];
@@ -181,8 +188,8 @@ __device__ __forceinline__ bool tri_ok(int i, int t, int nt) {
 //  P3 origin/twin written back coalesced; rotation successor of every half-edge: itself if it
 //     is a frontier edge (Alg. 8), else next_in(twin) (sweep_out, R1); a third copy of
 //     an edge breaks the twin involution
-//  P4 the unlink rewire (Alg. 11) by pointer jumping on the successors (lock-step, no
-//     divergent walks); frontier / seed bits (Alg. 8-9); tips (next == twin);
+//  P4 the unlink rewire (Alg. 11) by pointer jumping on the successors (2 lock-step
+//     rounds, then up to 3 jumped hops at each use: chains <= 16 steps); frontier / seed bits (Alg. 8-9); tips (next == twin);
 //     half-edges needing a twin outside the tile (or a longer rotation) are deferred
 //     to k_label_fixup (label phase)
 //  P5 the leftover and deferred lists as per-tile segments (one warp ranks the words)
@@ -433,8 +440,7 @@ __device__ __forceinline__ void tile_body(
   // ---- P4a: pointer jumping, double-buffered between succ and the (still unused) P4-P6
   // area: each round doubles the resolved chain length; an even number of rounds leaves
   // the result in succ.
-#ifndef POLYLLA_TILE_WALKS
-  static_assert(kTileJumps % 2 == 0, "result must end in succ");
+  static_assert(kTileJumps % 2 == 0 && kTileJumps <= 4, "result must end in succ");
   uint16_t* succ_b = reinterpret_cast<uint16_t*>(smem_tile + kOffNx);  // 16 KB <= the P4-P6 area
 #pragma unroll 1
   for (int round = 0; round < kTileJumps; ++round) {
@@ -449,7 +455,6 @@ __device__ __forceinline__ void tile_body(
     }
     __syncthreads();
   }
-#endif
   PHASE_MARK(4);
 
   // ---- P4b: per half-edge (e order): F / S words (Alg. 8-9), next (Alg. 11), tips
@@ -467,12 +472,8 @@ __device__ __forceinline__ void tile_body(
         sd = lc_s[q >> 2] == (q & 3) && lc_s[tq >> 2] == (tq & 3) && q < tq;  // terminal edge, smaller id
         int32_t nx = next_q(q);
         if (fr) {
-#ifdef POLYLLA_TILE_WALKS
-          uint16_t r = succ[nx];
-          for (int st = 0; !(r & (kSuccFront | kSuccUnknown)) && st < 15; ++st) r = succ[r];  // chains <= 16 (as the jumping)
-#else
-          const uint16_t r = succ[nx];  // first frontier half-edge about target(j), if reached
-#endif
+          uint16_t r = succ[nx];  // first frontier half-edge about target(j), if reached
+          for (int h = 0; h < kTileHops && !(r & (kSuccFront | kSuccUnknown)); ++h) r = succ[r];
           if (r & kSuccFront) {
             nx = r & kSuccIdx;
             tip = nx == tq;  // barrier tip: next == twin (R4)
@@ -565,7 +566,7 @@ __device__ __forceinline__ void tile_body(
       const int q = q_of(j);
       const int32_t o = tri_q[q], tg = tri_q[q + 1];
       const uint64_t lo = (uint32_t)min(o, tg), hi = (uint32_t)max(o, tg);
-      left_key[pl] = (lo << 32) | hi;
+      left_key[pl] = (lo << 32) | hi | (o > tg ? kLeftDown : 0ull);  // undirected key + direction bit
       left_e[pl++] = (int32_t)(e0 + j);
     }
     while (dw) {
@@ -583,12 +584,8 @@ __device__ __forceinline__ void tile_body(
     const int nseed = scan_sm[0];
     for (int i = tid; i < nseed; i += kTileThreads) {
       const int32_t sj = slist[i];
-#ifdef POLYLLA_TILE_WALKS
-      uint16_t r = succ[q_of(sj)];
-      for (int st = 0; !(r & (kSuccFront | kSuccUnknown)) && st < 15; ++st) r = succ[r];  // chains <= 16 (as the jumping)
-#else
-      const uint16_t r = succ[q_of(sj)];  // the frontier half-edge the rotation reaches, if resolved
-#endif
+      uint16_t r = succ[q_of(sj)];  // the frontier half-edge the rotation reaches, if resolved
+      for (int h = 0; h < kTileHops && !(r & (kSuccFront | kSuccUnknown)); ++h) r = succ[r];
       bool ok = (r & kSuccFront) != 0;
       int32_t mn = 0, n = 0;
       if (ok) {
@@ -679,7 +676,7 @@ __global__ void k_hash_clear(DevCounters* ctr, uint32_t* ehash, int64_t cap_max)
 // one block per tile segment (grid-stride over tiles).
 __global__ void k_left_insert(DevCounters* ctr, int64_t ntiles, const int32_t* __restrict__ cnt_ld,
                               const unsigned long long* __restrict__ left_key, const int32_t* __restrict__ left_e,
-                              const int32_t* __restrict__ origin, int32_t* twin, uint32_t* ehash) {
+                              int32_t* twin, uint32_t* ehash) {
   if (ctr->status) return;
   const uint32_t mask = (uint32_t)ctr->hash_cap - 1;
   for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
@@ -687,7 +684,8 @@ __global__ void k_left_insert(DevCounters* ctr, int64_t ntiles, const int32_t* _
     const int32_t base = (int32_t)(3 * kTileTris * tile);
     for (int32_t k = threadIdx.x; k < n; k += blockDim.x) {
       const int32_t i = base + k;
-      const unsigned long long key = left_key[i];
+      const unsigned long long kd = left_key[i], key = kd & ~kLeftDown;
+      const int32_t ei = left_e[i];
       uint32_t h = mix32((uint32_t)(key >> 32), (uint32_t)key) & mask;
       for (uint32_t probe = 0; probe <= mask; ++probe) {
         uint32_t s = ehash[h];
@@ -697,9 +695,11 @@ __global__ void k_left_insert(DevCounters* ctr, int64_t ntiles, const int32_t* _
           s = old;
         }
         const int32_t si = (int32_t)(s & ~kPaired);
-        if (left_key[si] == key) {
-          const int32_t ei = left_e[i], es = left_e[si];
-          if ((s & kPaired) || origin[ei] == origin[es] || atomicCAS(&ehash[h], s, s | kPaired) != s) {
+        const unsigned long long sd = left_key[si];
+        if ((sd & ~kLeftDown) == key) {
+          const int32_t es = left_e[si];
+          // a pair must run in opposite directions; a third copy finds the slot paired
+          if ((s & kPaired) || sd == kd || atomicCAS(&ehash[h], s, s | kPaired) != s) {
             raise_status(ctr, ST_NONMANIFOLD_EDGE);
             break;
           }
@@ -873,8 +873,7 @@ int launch_build(Ctx* c, cudaStream_t s) {
   prof_mark(s, "k_left_match");
   k_hash_clear<<<grid, 256, 0, s>>>(c->ctr, c->ehash, c->hash_cap_max);
   const unsigned seg_grid = (unsigned)(tiles < 148 * 16 ? tiles : 148 * 16);
-  k_left_insert<<<seg_grid, 256, 0, s>>>(c->ctr, tiles, c->cnt_ld, c->left_key, c->left_e, c->origin, c->twin,
-                                         c->ehash);
+  k_left_insert<<<seg_grid, 256, 0, s>>>(c->ctr, tiles, c->cnt_ld, c->left_key, c->left_e, c->twin, c->ehash);
   int32_t* blist = reinterpret_cast<int32_t*>(c->left_key);  // dead after k_left_insert
   k_border_rank<<<seg_grid, kSegThreads, 0, s>>>(c->ctr, tiles, c->cnt_ld, c->left_e, c->twin, blist, c->bcnt);
   n += 3;

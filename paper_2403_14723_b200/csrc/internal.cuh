@@ -135,13 +135,18 @@ constexpr uint32_t kPaired = 0x80000000u;  // flag in hash slots (slot values < 
 constexpr int kWalkBound = 1 << 16;      // rotation bound (vertex degree)
 constexpr int kBuildTileTris = 2048;     // triangles per k_tile tile (list segments are 3 * 2048 wide)
 
-// Set bits of a bit-vector, spread over warps: warp g of the grid scans 32-word chunks
-// g, g + G, ... and expands the set bits into its shared queue q (kBitQueue entries).
+// Set bits of a bit-vector, spread over warps: warp g of the grid scans kBitChunk-word
+// chunks g, g + G, ... and expands the set bits into its shared queue q (kBitQueue entries).
 // Each full (or final) batch is handed over either in warp-uniform rounds of 32,
 // f(e, valid) with all lanes present (f may use warp collectives; valid is false on the
 // padding lanes of the last round), or -- if `batch` is given -- whole, batch(fill), for
 // the caller to schedule freely.  Returns the number of set bits this warp saw.
 constexpr int kBitQueue = 128;  // small: the walks that follow live on L1 hits (shared memory shrinks L1)
+#ifndef POLYLLA_BIT_CHUNK
+#define POLYLLA_BIT_CHUNK 32
+#endif
+constexpr int kBitChunk = POLYLLA_BIT_CHUNK;  // words per warp chunk (<= 32)
+static_assert(kBitChunk >= 1 && kBitChunk <= 32, "one word per lane");
 struct NoBatch {
   __device__ void operator()(int) const {}
 };
@@ -163,11 +168,12 @@ __device__ __forceinline__ int warp_foreach_bit(const uint32_t* __restrict__ bv,
     __syncwarp();
     fill = 0;
   };
-  // interleaved 32-word chunks: at any time the grid works inside one window of the mesh
-  // (nwarps * 1024 half-edges), which keeps the walks' next/twin lines in L2
-  for (int64_t w0 = gwarp * 32; w0 < n_words; w0 += nwarps * 32) {
+  // interleaved kBitChunk-word chunks: at any time the grid works inside one window of
+  // the mesh (nwarps * kBitChunk * 32 half-edges), which keeps the walks' next/twin
+  // lines in L2
+  for (int64_t w0 = gwarp * kBitChunk; w0 < n_words; w0 += nwarps * kBitChunk) {
     const int64_t w = w0 + lane;
-    uint32_t bits = w < n_words ? bv[w] : 0u;
+    uint32_t bits = (lane < kBitChunk && w < n_words) ? bv[w] : 0u;
     while (__any_sync(0xffffffffu, bits != 0u)) {
       const int c = __popc(bits);
       int incl = c;
