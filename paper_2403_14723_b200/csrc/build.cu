@@ -313,9 +313,10 @@ __device__ __forceinline__ void tile_body(
   auto pf_load = [&](int i) {
     const int t = tid + i * kTileThreads;
     pf_ok = t < nn_pf;
-    if (pf_ok) {
+    if (pf_ok) {  // volatile: issued here, not sunk next to their use at the end of the pass
       const int32_t* src = tri + 3 * (f0n + t);
-      pf_v[0] = __ldg(src); pf_v[1] = __ldg(src + 1); pf_v[2] = __ldg(src + 2);
+      asm volatile("ld.global.nc.b32 %0, [%3];\n\tld.global.nc.b32 %1, [%3+4];\n\tld.global.nc.b32 %2, [%3+8];"
+                   : "=r"(pf_v[0]), "=r"(pf_v[1]), "=r"(pf_v[2]) : "l"(src));
     }
   };
   auto pf_issue = [&]() {
@@ -458,6 +459,11 @@ __device__ __forceinline__ void tile_body(
   PHASE_MARK(4);
 
   // ---- P4b: per half-edge (e order): F / S words (Alg. 8-9), next (Alg. 11), tips
+  // (per-lane word targets hoisted: lanes 0-5 the shared arrays Sw..SDm, lanes 8-11 the
+  // global F0, F1, S, TB)
+  const int s_off = lane < 6 ? lane * kTileWords : -1;
+  uint32_t* const g_word = F0 + (int64_t)(lane >= 8 && lane < 12 ? lane - 8 : 0) * bv_stride + (e0 >> 5);
+  const bool g_lane = lane >= 8 && lane < 12;
 #pragma unroll 2
   for (int i = 0, q = q0; i < kHeIters; ++i, q = q_step(q)) {
     const int j = tid + i * kTileThreads;
@@ -497,10 +503,10 @@ __device__ __forceinline__ void tile_body(
     const int wl = (j - lane) >> 5;  // tile-local word of this warp
     // one store per lane: lanes 0-5 the shared words Sw, Cw, Wl, Lm, Dm, SDm; lanes 8-11
     // the global words F0, F1, S, TB (equally spaced in the workspace, bv_stride words)
-    if (lane < 6) {
-      Sw[lane * kTileWords + wl] = lane == 0 ? sw : lane == 3 ? lm : lane == 4 ? dm : 0u;
-    } else if (lane >= 8 && lane < 12 && (FULL || j - lane < nhe)) {
-      F0[(int64_t)(lane - 8) * bv_stride + (e0 >> 5) + wl] = lane == 10 ? sw : lane == 11 ? tm : fw;
+    if (s_off >= 0) {
+      Sw[s_off + wl] = lane == 0 ? sw : lane == 3 ? lm : lane == 4 ? dm : 0u;
+    } else if (g_lane && (FULL || j - lane < nhe)) {
+      g_word[wl] = lane == 10 ? sw : lane == 11 ? tm : fw;
     }
   }
   __syncthreads();

@@ -85,15 +85,14 @@ __global__ void __launch_bounds__(kEmitThreads)
       }
     }
   } else {
-    // expand the seeds into the queue (rank order) with their loop lengths
+    // expand the seeds into the queue (rank order), then gather their loop lengths, one
+    // per thread (independent loads instead of a chain per word)
     for (int wl = tid; wl < kEmitWords && wt + wl < n_words; wl += kEmitThreads) {
       int p = wbase[wl];
-      for (uint32_t b = C[wt + wl]; b; b &= b - 1, ++p) {
-        const int32_t e = (int32_t)((wt + wl) * 32 + __ffs(b) - 1);
-        qe[p] = e;
-        qo[p] = len[e];
-      }
+      for (uint32_t b = C[wt + wl]; b; b &= b - 1, ++p) qe[p] = (int32_t)((wt + wl) * 32 + __ffs(b) - 1);
     }
+    __syncthreads();
+    for (int i = tid; i < np; i += kEmitThreads) qo[i] = len[qe[i]];
     __syncthreads();
     // exclusive scan of the lengths: thread t owns queue entries [t*per, (t+1)*per)
     const int per = (np + kEmitThreads - 1) / kEmitThreads;
@@ -115,11 +114,13 @@ __global__ void __launch_bounds__(kEmitThreads)
     __syncthreads();
     int run = obase + chunk[warp] + inc - sum;
     for (int i = q0; i < q1; ++i) { const int n = qo[i]; qo[i] = run; run += n; }
+    if (q1 == np && q0 < q1) chunk[kEmitThreads / 32] = run;  // end of the tile's last loop
     __syncthreads();
+    const int32_t run_end = chunk[kEmitThreads / 32];
     // one polygon per thread
     for (int i = tid; i < np; i += kEmitThreads) {
       const int32_t e = qe[i], o = qo[i];
-      const int32_t n = len[e];
+      const int32_t n = (i + 1 < np ? qo[i + 1] : run_end) - o;
       seeds[rbase + i] = e;
       offsets[rbase + i] = o;
       int32_t x = e;
