@@ -47,15 +47,13 @@ __device__ __forceinline__ int q_step(int q) {
 // shared memory (bytes):
 //   tri_q int32[kTileQ]   32768  quad layout (v0, v1, v2, v0): half-edge q runs tri_q[q] -> tri_q[q+1]
 //   tw_s  int16[kTileQ]   16384  twin as a quad index, -1 = outside the tile
-//   slot  u32[kTileSlots] 32768  (dead after P2: reused for succ u16[kTileQ] | scratch, offL, offD)
+//   slot  u32[kTileSlots] 32768  (dead after P2: reused for succ u16[kTileQ])
 //   lc_s  u8[kTileTris]    2048
-//   nx_l  int16[kTileHE] 12288 | Sw, Cw, Wl, Lm, Dm, SDm u32[192] 4608 | slist int16[kTileTris] 4096   (P4-P6)
-//         (P0-P1: the raw triangle tile int32[kTileHE], 24576)
+//   nx_l  int16[kTileHE] 12288 | Sw, Cw, Wl, Lm, Dm, SDm u32[192] 4608   (P4-P6)
 constexpr size_t kOffTw = kTileQ * 4, kOffSlot = kOffTw + kTileQ * 2, kOffLc = kOffSlot + kTileSlots * 4,
                  kOffNx = kOffLc + kTileTris,
-                 kNxBytes = kTileHE * 2 + 6 * (kTileHE / 8) + kTileTris * 2,  // P4-P6 arrays (20,992 B)
-                 kRawBytes = kTileHE * 4,                                      // P0-P1 raw tile (24,576 B)
-                 kTileSmem = kOffNx + (kNxBytes > kRawBytes ? kNxBytes : kRawBytes);  // 108,544 B -> 2 CTAs/SM
+                 kNxBytes = kTileHE * 2 + 6 * (kTileHE / 8),                   // P4-P6 arrays (16,896 B)
+                 kTileSmem = kOffNx + kNxBytes;                                // 100,864 B -> 2 CTAs/SM
 static_assert(2 * (kTileSmem + 1024) <= 228 * 1024, "two tiles per SM");
 constexpr unsigned long long kLeftDown = 1ull << 63;  // leftover key: set if origin > target
 constexpr uint32_t kSlotQ = (1u << 13) - 1;       // slot = fingerprint(19 bits) << 13 | quad index
@@ -178,7 +176,7 @@ __device__ __forceinline__ bool tri_ok(int i, int t, int nt) {
 }
 
 // One CTA per tile of kTileTris triangles.  Phases (PAPER.md section in brackets):
-//  P0 stage the triangle tile (coalesced, streaming)
+//  P0 clear the hash; bulk L2 prefetch of the tile that starts when this one ends
 //  P1 per triangle: checks, CCW orientation (R10), longest edge Lcode (Alg. 2/7); the
 //     oriented triangle goes to shared memory in quad layout
 //  P2 tile-local twin matching in a shared-memory hash on (min, max): the lo->hi halves
@@ -192,7 +190,7 @@ __device__ __forceinline__ bool tri_ok(int i, int t, int nt) {
 //     rounds, then up to 3 jumped hops at each use: chains <= 16 steps); frontier / seed bits (Alg. 8-9); tips (next == twin);
 //     half-edges needing a twin outside the tile (or a longer rotation) are deferred
 //     to k_label_fixup (label phase)
-//  P5 the leftover and deferred lists as per-tile segments (one warp ranks the words)
+//  P5 the leftover and deferred lists as per-tile segments (each word ranked by its warp)
 //  P6 seeds whose polygon closes inside the tile: landing + loop walk in shared memory
 //     -> canonical seed bits and loop lengths (others go to the global seed walk via the
 //     bit-vector SDB; tips go to the bit-vector TB)
@@ -219,10 +217,8 @@ __device__ __forceinline__ void tile_body(
   uint32_t* Lm = reinterpret_cast<uint32_t*>(Wl + kTileWords);                   // leftover bits
   uint32_t* Dm = Lm + kTileWords;                                                // deferred bits
   uint32_t* SDm = Dm + kTileWords;                                               // deferred seed bits
-  int16_t* slist = reinterpret_cast<int16_t*>(SDm + kTileWords);                // compacted seeds
   // overlays of the slot area (after P2)
   uint16_t* succ = reinterpret_cast<uint16_t*>(slot);
-  int* scan_sm = reinterpret_cast<int*>(slot + kTileQ / 2);  // 136 ints + offL/offD [2 x 192]
 
   const int64_t f0 = tile * kTileTris;
   const int64_t f0n = tile_next * kTileTris;  // this CTA's next tile (prefetched), if tile_next >= 0
@@ -235,20 +231,10 @@ __device__ __forceinline__ void tile_body(
   long long t_phase_ = clock64();
 #endif
 
-  // ---- P0: stage the raw triangle tile (coalesced 16-B streaming loads) in the P4-P6
-  // area (free until P4); clear the hash slots and the twins meanwhile
-  const int32_t* raw = reinterpret_cast<const int32_t*>(smem_tile + kOffNx);
-  {
-    int32_t* dst = reinterpret_cast<int32_t*>(smem_tile + kOffNx);
-    const int32_t* src = tri + e0;
-    if (FULL && ((reinterpret_cast<uintptr_t>(src) & 15) == 0)) {
-      const int4* s4 = reinterpret_cast<const int4*>(src);
-#pragma unroll
-      for (int i = tid; i < kTileHE / 4; i += kTileThreads) reinterpret_cast<int4*>(dst)[i] = __ldcs(s4 + i);
-    } else {
-      for (int i = tid; i < nhe; i += kTileThreads) dst[i] = __ldcs(src + i);
-    }
-  }
+  // ---- P0: clear the hash slots and the twins; P1 reads the raw triangles straight from
+  // global memory (the tile was bulk-prefetched into L2 by the CTA before; staging it in
+  // shared memory first measured 1% slower)
+  const int32_t* raw = tri + e0;
   for (int i = tid; i < kTileSlots / 4; i += kTileThreads)
     reinterpret_cast<uint4*>(slot)[i] = make_uint4(kEmpty, kEmpty, kEmpty, kEmpty);
   for (int i = tid; i < kTileQ / 2; i += kTileThreads) reinterpret_cast<uint32_t*>(tw_s)[i] = 0xFFFFFFFFu;
@@ -259,7 +245,6 @@ __device__ __forceinline__ void tile_body(
     if (bytes && (reinterpret_cast<uintptr_t>(pn) & 15) == 0)
       asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(pn), "r"(bytes) : "memory");
   }
-  __syncthreads();
   PHASE_MARK(0);
 
   // ---- P1: per triangle: checks, orientation, Lcode
@@ -464,6 +449,10 @@ __device__ __forceinline__ void tile_body(
   const int s_off = lane < 6 ? lane * kTileWords : -1;
   uint32_t* const g_word = F0 + (int64_t)(lane >= 8 && lane < 12 ? lane - 8 : 0) * bv_stride + (e0 >> 5);
   const bool g_lane = lane >= 8 && lane < 12;
+  // per-lane value masks (a select chain on the lane compiles to a divergent jump table)
+  const uint32_t m_s = 0u - (uint32_t)(lane == 0 || lane == 10), m_l = 0u - (uint32_t)(lane == 3),
+                 m_d = 0u - (uint32_t)(lane == 4), m_f = 0u - (uint32_t)(lane == 8 || lane == 9),
+                 m_t = 0u - (uint32_t)(lane == 11);
 #pragma unroll 2
   for (int i = 0, q = q0; i < kHeIters; ++i, q = q_step(q)) {
     const int j = tid + i * kTileThreads;
@@ -503,69 +492,39 @@ __device__ __forceinline__ void tile_body(
     const int wl = (j - lane) >> 5;  // tile-local word of this warp
     // one store per lane: lanes 0-5 the shared words Sw, Cw, Wl, Lm, Dm, SDm; lanes 8-11
     // the global words F0, F1, S, TB (equally spaced in the workspace, bv_stride words)
+    const uint32_t val = (sw & m_s) | (lm & m_l) | (dm & m_d) | (fw & m_f) | (tm & m_t);
     if (s_off >= 0) {
-      Sw[s_off + wl] = lane == 0 ? sw : lane == 3 ? lm : lane == 4 ? dm : 0u;
+      Sw[s_off + wl] = val;
     } else if (g_lane && (FULL || j - lane < nhe)) {
-      g_word[wl] = lane == 10 ? sw : lane == 11 ? tm : fw;
+      g_word[wl] = val;
     }
   }
   __syncthreads();
   PHASE_MARK(5);
 
-  // ---- P6 setup, one warp each (no block-wide scan, no global atomic): warp 0 lists the
-  // seed candidates of the tile (slist); warp 1 ranks the leftover and deferred half-edges
-  // of every word (their lists are per-tile segments at e0 of left_e/left_key/def_e, with
-  // the counts in cnt_ld[2 * tile + {0, 1}])
-  int* offL = scan_sm + 136;  // [kTileWords] exclusive prefix of leftovers per word
-  int* offD = offL + kTileWords;
-  {
-    constexpr int kWPL = kTileWords / 32;  // 6 words per lane
-    const int warp = tid >> 5;
-    if (warp < 2) {
-      const uint32_t* src0 = warp == 0 ? Sw : Lm;
-      uint32_t m0[kWPL], m1[kWPL];
-      int c0 = 0, c1 = 0;
-#pragma unroll
-      for (int k = 0; k < kWPL; ++k) {
-        m0[k] = src0[kWPL * lane + k];
-        m1[k] = warp == 0 ? 0u : Dm[kWPL * lane + k];
-        c0 += __popc(m0[k]);
-        c1 += __popc(m1[k]);
-      }
-      int i0 = c0, i1 = c1;
-#pragma unroll
-      for (int o = 1; o < 32; o <<= 1) {
-        const int a = __shfl_up_sync(0xffffffffu, i0, o), b = __shfl_up_sync(0xffffffffu, i1, o);
-        if (lane >= o) { i0 += a; i1 += b; }
-      }
-      int p0 = i0 - c0, p1 = i1 - c1;
-      if (warp == 0) {
-#pragma unroll
-        for (int k = 0; k < kWPL; ++k)
-          for (uint32_t b = m0[k]; b; b &= b - 1) slist[p0++] = (int16_t)((kWPL * lane + k) * 32 + __ffs(b) - 1);
-        if (lane == 31) scan_sm[0] = i0;  // number of seed candidates
-      } else {
-#pragma unroll
-        for (int k = 0; k < kWPL; ++k) {
-          offL[kWPL * lane + k] = p0;
-          offD[kWPL * lane + k] = p1;
-          p0 += __popc(m0[k]);
-          p1 += __popc(m1[k]);
-        }
-        if (lane == 31) {
-          reinterpret_cast<int2*>(cnt_ld)[tile] = make_int2(i0, i1);
-          if (i0) atomicAdd(&ctr->n_left, i0);  // totals (result unused: a reduction)
-          if (i1) atomicAdd(&ctr->n_def, i1);
-        }
-      }
-    }
-  }
-  __syncthreads();
-
-  // ---- P5: the leftover (key, id) and deferred lists, one word per thread
+  // ---- P5: the leftover (key, id) and deferred lists as per-tile segments at e0 of
+  // left_e/left_key/def_e (counts in cnt_ld[2 * tile + {0, 1}]), one word per thread of
+  // warps 0-5: a word's exclusive prefix is the warp's shuffle scan plus the popcounts of
+  // the earlier warps' words, which every lane sums itself (no barrier, no global atomic)
   if (tid < kTileWords) {
     uint32_t lw = Lm[tid], dw = Dm[tid];
-    int pl = (int)e0 + offL[tid], pd = (int)e0 + offD[tid];
+    const int cl = __popc(lw), cd = __popc(dw);
+    int il = cl, id = cd;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int a = __shfl_up_sync(0xffffffffu, il, o), b = __shfl_up_sync(0xffffffffu, id, o);
+      if (lane >= o) { il += a; id += b; }
+    }
+    int bl = 0, bd = 0;
+    for (int w = lane; w < (tid & ~31); w += 32) { bl += __popc(Lm[w]); bd += __popc(Dm[w]); }
+    bl = __reduce_add_sync(0xffffffffu, bl);
+    bd = __reduce_add_sync(0xffffffffu, bd);
+    if (tid == kTileWords - 1) {
+      reinterpret_cast<int2*>(cnt_ld)[tile] = make_int2(bl + il, bd + id);
+      if (bl + il) atomicAdd(&ctr->n_left, bl + il);  // totals (result unused: a reduction)
+      if (bd + id) atomicAdd(&ctr->n_def, bd + id);
+    }
+    int pl = (int)e0 + bl + il - cl, pd = (int)e0 + bd + id - cd;
     while (lw) {
       const int j = tid * 32 + __ffs(lw) - 1;
       lw &= lw - 1;
@@ -585,11 +544,16 @@ __device__ __forceinline__ void tile_body(
   // PAPER.md L778-849): land on a frontier half-edge by rotation (the resolved successor
   // chain), walk the loop on nx_l, keep the minimum id and the length.  Loops that touch
   // a deferred half-edge or a barrier tip (repaired later) are handed to the global
-  // seed walk (bit-vector SDB).
+  // seed walk (bit-vector SDB).  kSeedLanes threads per word take its seeds in turn.
   {
-    const int nseed = scan_sm[0];
-    for (int i = tid; i < nseed; i += kTileThreads) {
-      const int32_t sj = slist[i];
+    static_assert(kTileThreads % kTileWords == 0, "threads per word");
+    constexpr int kSeedLanes = kTileThreads / kTileWords;  // 4
+    const int wsd = tid / kSeedLanes, sub = tid % kSeedLanes;
+    uint32_t sb = Sw[wsd];
+    for (int k = 0; k < sub && sb; ++k) sb &= sb - 1;
+    while (sb) {
+      const int32_t sj = wsd * 32 + __ffs(sb) - 1;
+      for (int k = 0; k < kSeedLanes && sb; ++k) sb &= sb - 1;
       uint16_t r = succ[q_of(sj)];  // the frontier half-edge the rotation reaches, if resolved
       for (int h = 0; h < kTileHops && !(r & (kSuccFront | kSuccUnknown)); ++h) r = succ[r];
       bool ok = (r & kSuccFront) != 0;
