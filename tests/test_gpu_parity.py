@@ -151,6 +151,37 @@ def test_determinism_and_streams():
         assert torch.equal(a[k], b[k]), k
 
 
+def test_concurrent_meshes_on_two_streams():
+    """bench.py's batch path: independent meshes converted concurrently on two streams
+    (own workspace and outputs each) give the same CSR as one at a time."""
+    pp = _pp()
+    meshes = [synth.grid(300, 0.2, 7), synth.grid(300), synth.random_delaunay(60000, 9), synth.grid(250, 0.2, 3)]
+    ref = [gpu_run(xy, tri) for xy, tri in meshes]
+    Vm = max(xy.shape[0] for xy, _ in meshes)
+    Tm = max(tri.shape[0] for _, tri in meshes)
+    lanes = []
+    for _ in range(2):
+        lanes.append(dict(stream=torch.cuda.Stream(), ws=pp.alloc_workspace(Vm, Tm), out=[]))
+    dev = [(torch.from_numpy(xy).cuda(), torch.from_numpy(tri).cuda()) for xy, tri in meshes]
+    torch.cuda.synchronize()
+    for i, (xy_d, tri_d) in enumerate(dev):
+        ln = lanes[i % 2]
+        offs = torch.empty(Tm + 1, dtype=torch.int32, device="cuda")
+        loops = torch.empty(3 * Tm, dtype=torch.int32, device="cuda")
+        ctx = pp.build_halfedges(xy_d, tri_d, ln["ws"], ln["stream"])
+        pp.label(ctx, ln["stream"])
+        pp.generate(ctx, ln["stream"])
+        pp.get_polygons(ctx, offs, loops, stream=ln["stream"])
+        ln["out"].append((i, offs, loops))  # (a lane's next mesh reuses its workspace in stream order)
+        pp.destroy(ctx)
+    torch.cuda.synchronize()
+    for ln in lanes:
+        for i, offs, loops in ln["out"]:
+            P, L = ref[i]["P"], ref[i]["L"]
+            assert torch.equal(offs[:P + 1], ref[i]["offsets"]), i
+            assert torch.equal(loops[:L], ref[i]["loops"]), i
+
+
 def test_run_host_e2e_matches_device():
     pp = _pp()
     xy, tri = synth.random_delaunay(30000, 12)
