@@ -148,7 +148,8 @@ POLYLLA_API polylla_status polylla_get_polygons(polylla_ctx* ctx, int32_t* offse
  * Any pointer argument may be NULL.  Sizes: origin/twin/next [H]; lcode [T] (k* of
  * each triangle); frontier0 / frontier1 / seed_bits: bit-vectors of uint32 words
  * over the interior half-edges [0, 3T) (bit e%32 of word e/32; border half-edges
- * are frontier by definition); seeds [P]. */
+ * are frontier by definition); seeds [P] (canonical seed of each polygon, written by
+ * polylla_get_polygons). */
 typedef struct {
   const int32_t* origin;
   const int32_t* twin;

@@ -479,7 +479,7 @@ __device__ __forceinline__ void tile_body(
         if (!deferred) {
           nx = j_of(nx);
           __stcs(next + e0 + j, (int32_t)(e0 + nx));
-          if (!tip) nl_j = nx;
+          nl_j = tip ? -2 : nx;  // -2: a barrier tip (the loop will be split by the repair)
         } else {
           fr = sd = false;  // the fixup sets every bit of a deferred half-edge
         }
@@ -556,7 +556,7 @@ __device__ __forceinline__ void tile_body(
       for (int k = 0; k < kSeedLanes && sb; ++k) sb &= sb - 1;
       uint16_t r = succ[q_of(sj)];  // the frontier half-edge the rotation reaches, if resolved
       for (int h = 0; h < kTileHops && !(r & (kSuccFront | kSuccUnknown)); ++h) r = succ[r];
-      bool ok = (r & kSuccFront) != 0;
+      bool ok = (r & kSuccFront) != 0, tipped = false;
       int32_t mn = 0, n = 0;
       if (ok) {
         const int32_t x = j_of(r & kSuccIdx);
@@ -566,14 +566,16 @@ __device__ __forceinline__ void tile_body(
           mn = min(mn, y);
           ++n;
           y = nx_l[y];
-          if (y < 0 || n > 1024) { ok = false; break; }  // deferred / barrier-tip loop
+          if (y < 0 || n > 1024) { ok = false; tipped = y == -2; break; }  // deferred / barrier-tip loop
         } while (y != x);
       }
       if (ok) {
         len[e0 + mn] = n;
         const uint32_t bit = 1u << (mn & 31);
         if (!(atomicOr(&Cw[mn >> 5], bit) & bit)) atomicAdd(&Wl[mn >> 5], n);  // first setter only
-      } else {
+      } else if (!tipped) {
+        // (a loop through a barrier tip is split by the repair, and every piece borders a
+        // middle edge whose two halves k_repair_mid seeds: this seed would add nothing)
         atomicOr(&SDm[sj >> 5], 1u << (sj & 31));
       }
     }
