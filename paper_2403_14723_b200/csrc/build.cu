@@ -638,9 +638,10 @@ __global__ void k_hash_clear(DevCounters* ctr, uint32_t* ehash, int64_t cap_max)
     return;
   }
   if (blockIdx.x == 0 && threadIdx.x == 0) ctr->hash_cap = (uint32_t)cap;
-  for (uint64_t i = blockIdx.x * blockDim.x + threadIdx.x; i < cap; i += gridDim.x * blockDim.x) {
-    ehash[i] = kEmpty;
-  }
+  // cap is a power of two >= 1024 and ehash is 256-B aligned: 16-B stores
+  uint4* h4 = reinterpret_cast<uint4*>(ehash);
+  for (uint64_t i = blockIdx.x * blockDim.x + threadIdx.x; i < cap / 4; i += gridDim.x * blockDim.x)
+    h4[i] = make_uint4(kEmpty, kEmpty, kEmpty, kEmpty);
 }
 
 // global hash over leftover half-edges: pair the two halves of each cross-tile edge.

@@ -11,7 +11,6 @@
 //   seeds/offsets/loops staging, input staging (run_host).
 #pragma once
 #include <cstdint>
-#include <type_traits>
 #include <cuda_runtime.h>
 
 #include "polylla.h"
@@ -136,35 +135,25 @@ constexpr int kWalkBound = 1 << 16;      // rotation bound (vertex degree)
 constexpr int kBuildTileTris = 2048;     // triangles per k_tile tile (list segments are 3 * 2048 wide)
 
 // Set bits of a bit-vector, spread over warps: warp g of the grid scans kBitChunk-word
-// chunks g, g + G, ... and expands the set bits into its shared queue q (kBitQueue entries).
-// Each full (or final) batch is handed over either in warp-uniform rounds of 32,
-// f(e, valid) with all lanes present (f may use warp collectives; valid is false on the
-// padding lanes of the last round), or -- if `batch` is given -- whole, batch(fill), for
-// the caller to schedule freely.  Returns the number of set bits this warp saw.
+// chunks g, g + G, ... and expands the set bits into its shared queue q (kBitQueue
+// entries); each full (or final) queue is handed to f(e, valid) in warp-uniform rounds of
+// 32 (all lanes present, so f may use warp collectives; valid is false on the padding
+// lanes of the last round).  Returns the number of set bits this warp saw.
 constexpr int kBitQueue = 128;  // small: the walks that follow live on L1 hits (shared memory shrinks L1)
 #ifndef POLYLLA_BIT_CHUNK
 #define POLYLLA_BIT_CHUNK 32
 #endif
-constexpr int kBitChunk = POLYLLA_BIT_CHUNK;  // words per warp chunk (<= 32)
+constexpr int kBitChunk = POLYLLA_BIT_CHUNK;  // words per warp chunk (<= 32; 8 and 4 measured slower)
 static_assert(kBitChunk >= 1 && kBitChunk <= 32, "one word per lane");
-struct NoBatch {
-  __device__ void operator()(int) const {}
-};
-template <class F, class B = NoBatch>
-__device__ __forceinline__ int warp_foreach_bit(const uint32_t* __restrict__ bv, int64_t n_words, int32_t* q, F f,
-                                                B batch = B()) {
-  constexpr bool kBatch = !std::is_same<B, NoBatch>::value;
+template <class F>
+__device__ __forceinline__ int warp_foreach_bit(const uint32_t* __restrict__ bv, int64_t n_words, int32_t* q, F f) {
   const int lane = threadIdx.x & 31;
   const int64_t nwarps = (int64_t)gridDim.x * (blockDim.x >> 5);
   const int64_t gwarp = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   int fill = 0, seen = 0;
   auto flush = [&]() {
     __syncwarp();
-    if constexpr (kBatch) {
-      batch(fill);
-    } else {
-      for (int base = 0; base < fill; base += 32) f(base + lane < fill ? q[base + lane] : -1, base + lane < fill);
-    }
+    for (int base = 0; base < fill; base += 32) f(base + lane < fill ? q[base + lane] : -1, base + lane < fill);
     __syncwarp();
     fill = 0;
   };
