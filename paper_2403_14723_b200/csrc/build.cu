@@ -340,13 +340,17 @@ __device__ __forceinline__ void tile_body(
       if (!tri_ok<FULL>(i, t, nt)) continue;
       const int4 v = tri_q4[t];
       const int32_t vs[4] = {v.x, v.y, v.z, v.w};
+      uint32_t got[3], mine[3];
 #pragma unroll
-      for (int k = 0; k < 3; ++k) {
+      for (int k = 0; k < 3; ++k) {  // the three re-reads issued together
         const uint32_t o = (uint32_t)vs[k], tg = (uint32_t)vs[k + 1];
         const uint32_t h = tile_hash(min(o, tg), max(o, tg));
-        if (o < tg && ld_relaxed(&slot[tile_pos(h)]) != ((h & ~kSlotQ) | (uint32_t)(4 * t + k)))
-          pend |= 1u << (4 * i + k);
+        mine[k] = (h & ~kSlotQ) | (uint32_t)(4 * t + k);
+        got[k] = o < tg ? ld_relaxed(&slot[tile_pos(h)]) : mine[k];
       }
+#pragma unroll
+      for (int k = 0; k < 3; ++k)
+        if (got[k] != mine[k]) pend |= 1u << (4 * i + k);
     }
     while (pend) {
       const int b = __ffs(pend) - 1;
@@ -367,19 +371,35 @@ __device__ __forceinline__ void tile_body(
       if (!tri_ok<FULL>(i, t, nt)) continue;
       const int4 v = tri_q4[t];
       const int32_t vs[4] = {v.x, v.y, v.z, v.w};
+      // the three half-edges' probes issued together (predicated loads, no branch
+      // between them): home slots, then the candidates' vertices, then the decisions
+      uint32_t w[3], fp[3];
+      bool look[3];
 #pragma unroll
       for (int k = 0; k < 3; ++k) {
         const uint32_t o = (uint32_t)vs[k], tg = (uint32_t)vs[k + 1];
-        if (o > tg) {
-          const uint32_t h = tile_hash(tg, o);
-          const uint32_t w = slot[tile_pos(h)];
-          if (slot_is(w, h & ~kSlotQ, tri_q, tg, o)) {
-            const int32_t sq = (int32_t)(w & kSlotQ);
-            tw_s[4 * t + k] = (int16_t)sq;
-            tw_s[sq] = (int16_t)(4 * t + k);
-          } else if (w != kEmpty) {
-            pend |= 1u << (4 * i + k);
-          }
+        look[k] = o > tg;
+        const uint32_t h = tile_hash(tg, o);
+        fp[k] = h & ~kSlotQ;
+        w[k] = look[k] ? slot[tile_pos(h)] : kEmpty;
+      }
+      int32_t ca[3], cb[3];
+#pragma unroll
+      for (int k = 0; k < 3; ++k) {
+        const bool f = w[k] != kEmpty && (w[k] & ~kSlotQ) == fp[k];
+        const int32_t sq = (int32_t)(w[k] & kSlotQ);
+        ca[k] = f ? tri_q[sq] : -1;
+        cb[k] = f ? tri_q[sq + 1] : -1;
+      }
+#pragma unroll
+      for (int k = 0; k < 3; ++k) {
+        const bool hit = look[k] && ca[k] == vs[k + 1] && cb[k] == vs[k];
+        if (hit) {
+          const int32_t sq = (int32_t)(w[k] & kSlotQ);
+          tw_s[4 * t + k] = (int16_t)sq;
+          tw_s[sq] = (int16_t)(4 * t + k);
+        } else if (look[k] && w[k] != kEmpty) {
+          pend |= 1u << (4 * i + k);
         }
       }
     }
