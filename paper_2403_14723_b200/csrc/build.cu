@@ -429,15 +429,18 @@ __device__ __forceinline__ void tile_body(
     const int j = tid + i * kTileThreads;
     if (!FULL && j >= nhe) break;
     const int k = q & 3, t = q >> 2;
+    // loads issued together: own twin / vertex / Lcode, then the twin's back-pointer and Lcode
     const int32_t tq = tw_s[q];
-    if (tq >= 0 && tw_s[tq] != q) nm = ST_NONMANIFOLD_EDGE;  // twin claimed twice (edge in > 2 triangles)
-    __stcs(origin + e0 + j, tri_q[q]);
+    const int32_t org = tri_q[q];
+    const uint8_t lq = lc_s[t];
+    const int32_t tqs = tq < 0 ? q : tq;
+    const int32_t back = tw_s[tqs];
+    const uint8_t lt = lc_s[tqs >> 2];
+    if (tq >= 0 && back != q) nm = ST_NONMANIFOLD_EDGE;  // twin claimed twice (edge in > 2 triangles)
+    __stcs(origin + e0 + j, org);
     __stcs(twin + e0 + j, tq >= 0 ? (int32_t)(e0 + j_of(tq)) : -1);
-    uint16_t sc;
-    if (tq < 0) sc = (uint16_t)(q | kSuccUnknown);
-    else if (lc_s[t] != k && lc_s[tq >> 2] != (tq & 3)) sc = (uint16_t)(q | kSuccFront);  // neither half longest
-    else sc = (uint16_t)next_q(tq);
-    succ[q] = sc;
+    const bool front = lq != k && lt != (tq & 3);  // neither half the longest edge of its triangle
+    succ[q] = (uint16_t)(tq < 0 ? (q | kSuccUnknown) : front ? (q | kSuccFront) : next_q(tq));
   }
   if (nm) raise_status(ctr, nm);
   __syncthreads();
