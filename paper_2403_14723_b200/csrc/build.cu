@@ -65,6 +65,10 @@ constexpr uint16_t kSuccIdx = 0x1FFF, kSuccFront = 0x4000, kSuccUnknown = 0x8000
 // pointer-jumping rounds (even: the result ends in succ); each use of a successor then
 // follows up to kTileHops more jumped pointers, so chains up to 16 steps resolve in-tile
 constexpr int kTileJumps = POLYLLA_TILE_JUMPS;
+#ifndef POLYLLA_P4B_UNROLL
+#define POLYLLA_P4B_UNROLL 2
+#endif
+constexpr int kP4bUnroll = POLYLLA_P4B_UNROLL;  // P4b loop unroll (1 / 2 / 4 measured: 2 best)
 constexpr int kTileHops = (16 >> kTileJumps) - 1;
 
 #ifdef POLYLLA_PHASE_TIMING
@@ -476,7 +480,7 @@ __device__ __forceinline__ void tile_body(
   const uint32_t m_s = 0u - (uint32_t)(lane == 0 || lane == 10), m_l = 0u - (uint32_t)(lane == 3),
                  m_d = 0u - (uint32_t)(lane == 4), m_f = 0u - (uint32_t)(lane == 8 || lane == 9),
                  m_t = 0u - (uint32_t)(lane == 11);
-#pragma unroll 2
+#pragma unroll kP4bUnroll
   for (int i = 0, q = q0; i < kHeIters; ++i, q = q_step(q)) {
     const int j = tid + i * kTileThreads;
     bool fr = false, sd = false, tip = false, deferred = false, left = false;
