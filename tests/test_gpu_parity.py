@@ -140,6 +140,53 @@ def test_config5_grid_full():
     assert res["P"] == 3_996_001 and res["L"] == 15_984_004
 
 
+def _grid_with_holes(s=60, seed=11):
+    """Jittered grid minus the triangles with a vertex strictly inside three discs: four
+    boundary loops (the outer one and three holes), polygons that touch the holes."""
+    xy, tri = synth.grid(s, 0.2, seed)
+    bad = np.zeros(tri.shape[0], bool)
+    for cx, cy, r in ((0.25 * s, 0.26 * s, 0.10 * s), (0.67 * s, 0.37 * s, 0.085 * s), (0.5 * s, 0.76 * s, 0.12 * s)):
+        bad |= (np.hypot(xy[:, 0] - cx, xy[:, 1] - cy) < r)[tri].any(axis=1)
+    return xy, np.ascontiguousarray(tri[~bad])
+
+
+def _wheels(k=300, seed=5):
+    """k disjoint wheels (a centre vertex with 20-60 spokes each): rotation chains far
+    longer than the 16 steps k_tile resolves in shared memory, so the label fixup walks
+    them; several tiles."""
+    rng = np.random.default_rng(seed)
+    pts, tris, off = [], [], 0
+    for w in range(k):
+        n = int(rng.integers(20, 61))
+        ang = np.sort(rng.random(n)) * 2 * np.pi
+        rr = 1.0 + 0.4 * rng.random(n)
+        c = np.array([3.0 * (w % 20), 3.0 * (w // 20)])
+        pts.append(np.vstack([c, c + np.c_[rr * np.cos(ang), rr * np.sin(ang)]]))
+        tris.append(np.array([[off, off + 1 + i, off + 1 + (i + 1) % n] for i in range(n)], np.int32))
+        off += n + 1
+    return np.vstack(pts), np.vstack(tris)
+
+
+def test_mesh_with_holes():
+    xy, tri = _grid_with_holes()
+    res, ref = assert_parity(xy, tri)
+    assert ref["B"] > 4 * 59  # outer boundary plus the three holes
+
+
+def test_disconnected_components():
+    xy1, tri1 = synth.grid(60, 0.2, 11)
+    xy2, tri2 = synth.random_delaunay(5000, 12)
+    xy = np.vstack([xy1, xy2 * 50.0 + np.array([100.0, 0.0])])
+    tri = np.vstack([tri1, tri2 + xy1.shape[0]]).astype(np.int32)
+    assert_parity(xy, tri)
+
+
+def test_high_degree_wheels():
+    xy, tri = _wheels()
+    res, ref = assert_parity(xy, tri)
+    assert res["n_deferred"] > 0
+
+
 def test_determinism_and_streams():
     xy, tri = synth.random_delaunay(20000, 8)
     a = gpu_run(xy, tri)
