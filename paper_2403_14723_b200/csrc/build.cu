@@ -584,9 +584,10 @@ __device__ __forceinline__ void tile_body(
       uint16_t r = succ[q_of(sj)];  // the frontier half-edge the rotation reaches, if resolved
       for (int h = 0; h < kTileHops && !(r & (kSuccFront | kSuccUnknown)); ++h) r = succ[r];
       bool ok = (r & kSuccFront) != 0, tipped = false;
-      int32_t mn = 0, n = 0;
+      const bool landed = ok;
+      int32_t mn = 0, n = 0, x = sj;
       if (ok) {
-        const int32_t x = j_of(r & kSuccIdx);
+        x = j_of(r & kSuccIdx);
         int32_t y = x;
         mn = x;
         do {
@@ -602,8 +603,12 @@ __device__ __forceinline__ void tile_body(
         if (!(atomicOr(&Cw[mn >> 5], bit) & bit)) atomicAdd(&Wl[mn >> 5], n);  // first setter only
       } else if (!tipped) {
         // (a loop through a barrier tip is split by the repair, and every piece borders a
-        // middle edge whose two halves k_repair_mid seeds: this seed would add nothing)
-        atomicOr(&SDm[sj >> 5], 1u << (sj & 31));
+        // middle edge whose two halves k_repair_mid seeds: this seed would add nothing).
+        // The global walk starts from the frontier half-edge the seed landed on when the
+        // landing stayed in the tile (the same loop: F1 adds frontier edges only to
+        // repaired loops, whose pieces the middle-edge halves seed anyway), else from the seed.
+        const int32_t g = landed ? x : sj;
+        atomicOr(&SDm[g >> 5], 1u << (g & 31));
       }
     }
   }
