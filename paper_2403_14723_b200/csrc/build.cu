@@ -12,7 +12,9 @@
 //       key (min, max) -- Morton-ordered meshes keep ~96% of twins inside a tile;
 //     - frontier/seed classification and the unlink rewire of every half-edge whose
 //       rotation walk stays inside the tile (label.cu completes the others);
-//     - half-edges whose twin is outside the tile are appended to a leftover list.
+//     - polygons that close inside the tile: canonical seed and loop length;
+//     - half-edges whose twin is outside the tile go to the tile's leftover segment,
+//       those whose rotation leaves it to its deferred segment.
 //   k_left_insert                      -- global hash over the leftovers only;
 //   k_border_rank / _scan / _emit      -- border ids 3T + rank(e) (R9), twin/origin of
 //                                         border half-edges, border-vertex map;
