@@ -1,3 +1,4 @@
 mkdir -p gpurun_out
-L=$PWD/paper_2403_14723_b200
-timeout 600 python tools/kernel_times.py 3 40 $L/libpolylla.so $L/libpolylla_p6f.so $L/libpolylla.so $L/libpolylla_p6f.so 2>&1 | grep -v Warn
+for c in -1 0 10 25 50 100; do
+POLYLLA_EMIT_CARVEOUT=$c timeout 600 python tools/kernel_times.py 3 30 2>&1 | grep -v Warn | sed "s/^/carve $c: /"
+done
