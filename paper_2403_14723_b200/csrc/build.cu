@@ -879,8 +879,12 @@ int launch_build(Ctx* c, cudaStream_t s) {
   const int grid = 148 * 32;  // enough threads for ~1 leftover each on 10M-vertex meshes (latency-bound)
   prof_mark(s, "k_left_match");
   k_hash_clear<<<grid, 256, 0, s>>>(c->ctr, c->ehash, c->hash_cap_max);
+#ifndef POLYLLA_LEFT_THREADS
+#define POLYLLA_LEFT_THREADS 256  // 128 / 256 / 384 / 512 measured: 128-256 best
+#endif
   const unsigned seg_grid = (unsigned)(tiles < 148 * 16 ? tiles : 148 * 16);
-  k_left_insert<<<seg_grid, 256, 0, s>>>(c->ctr, tiles, c->cnt_ld, c->left_key, c->left_e, c->twin, c->ehash);
+  const unsigned left_grid = (unsigned)(tiles < 148 * (4096 / POLYLLA_LEFT_THREADS) ? tiles : 148 * (4096 / POLYLLA_LEFT_THREADS));
+  k_left_insert<<<left_grid, POLYLLA_LEFT_THREADS, 0, s>>>(c->ctr, tiles, c->cnt_ld, c->left_key, c->left_e, c->twin, c->ehash);
   int32_t* blist = reinterpret_cast<int32_t*>(c->left_key);  // dead after k_left_insert
   k_border_rank<<<seg_grid, kSegThreads, 0, s>>>(c->ctr, tiles, c->cnt_ld, c->left_e, c->twin, blist, c->bcnt);
   n += 3;

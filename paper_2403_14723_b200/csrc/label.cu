@@ -14,7 +14,10 @@
 
 namespace polylla {
 
-constexpr int kLabelThreads = 256;
+#ifndef POLYLLA_FIX_THREADS
+#define POLYLLA_FIX_THREADS 384  // 128 / 256 / 384 / 512 measured: 384 best on config 3
+#endif
+constexpr int kLabelThreads = POLYLLA_FIX_THREADS;
 
 __device__ __forceinline__ bool is_longest(const uint8_t* __restrict__ lcode, int32_t x) {
   const int32_t f = x / 3;
@@ -82,10 +85,12 @@ __global__ void __launch_bounds__(kLabelThreads)
   }
 }
 
+constexpr int kFixBlocksPerSM = 4096 / kLabelThreads;  // a grid of 2 resident waves
+
 int launch_label(Ctx* c, cudaStream_t s) {
   const int64_t tiles = (c->T + kBuildTileTris - 1) / kBuildTileTris;
   prof_mark(s, "k_label_fixup");
-  k_label_fixup<<<(unsigned)(tiles < 148 * 16 ? tiles : 148 * 16), kLabelThreads, 0, s>>>(
+  k_label_fixup<<<(unsigned)(tiles < 148 * kFixBlocksPerSM ? tiles : 148 * kFixBlocksPerSM), kLabelThreads, 0, s>>>(
       c->T, tiles, c->cnt_ld, c->def_e, c->twin, c->lcode, c->next, c->F0, c->F1, c->S, c->TB, c->SDB, c->ctr);
   prof_end(s);
   return cudaGetLastError() == cudaSuccess ? 1 : -1;
