@@ -27,7 +27,10 @@ __device__ __forceinline__ bool f1_of(const uint32_t* __restrict__ F1, int64_t T
 
 // The tips of the bit-vector TB (set by k_tile and the label fixup), balanced over warps
 // (warp_foreach_bit) and compacted (one atomic per round of 32) into tips[] / aff[].
-constexpr int kRepairThreads = 128;
+#ifndef POLYLLA_REPAIR_THREADS
+#define POLYLLA_REPAIR_THREADS 128
+#endif
+constexpr int kRepairThreads = POLYLLA_REPAIR_THREADS;
 __global__ void __launch_bounds__(kRepairThreads)
     k_repair_mid(int64_t T, int64_t n_words, const uint32_t* __restrict__ TB, const int32_t* __restrict__ twin,
                  uint32_t* F1, uint32_t* SDB, int32_t* __restrict__ tips, int32_t* __restrict__ aff, DevCounters* ctr) {
@@ -93,7 +96,10 @@ __global__ void k_repair_rewire(int64_t T, const int32_t* __restrict__ twin, con
   }
 }
 
-constexpr int kSeedThreads = 256;
+#ifndef POLYLLA_SEED_THREADS
+#define POLYLLA_SEED_THREADS 256
+#endif
+constexpr int kSeedThreads = POLYLLA_SEED_THREADS;
 
 __device__ __forceinline__ void process_seed(int32_t s, int64_t T3, int64_t H, const int32_t* __restrict__ twin,
                                              const int32_t* __restrict__ next, const uint32_t* __restrict__ F1,
@@ -233,11 +239,11 @@ int launch_generate(Ctx* c, cudaStream_t s) {
   int n = 0;
   if (c->next_pre) cudaMemcpyAsync(c->next_pre, c->next, (size_t)c->Hmax * 4, cudaMemcpyDeviceToDevice, s);
   prof_mark(s, "k_repair");
-  k_repair_mid<<<148 * 12, kRepairThreads, 0, s>>>(c->T, c->n_words, c->TB, c->twin, c->F1, c->SDB, c->tips, c->aff, c->ctr);
-  k_repair_rewire<<<148 * 32, 128, 0, s>>>(c->T, c->twin, c->F1, c->aff, c->next, c->ctr);
+  k_repair_mid<<<148 * (1536 / kRepairThreads), kRepairThreads, 0, s>>>(c->T, c->n_words, c->TB, c->twin, c->F1, c->SDB, c->tips, c->aff, c->ctr);
+  k_repair_rewire<<<148 * (4096 / kRepairThreads), kRepairThreads, 0, s>>>(c->T, c->twin, c->F1, c->aff, c->next, c->ctr);
   prof_mark(s, "k_seed_walk");
   // (the canonical bit-vector C was written in full by k_tile; global walks OR into it)
-  k_seed_walk<<<148 * 8, kSeedThreads, 0, s>>>(c->T, c->n_words, c->SDB, c->twin, c->next, c->F1, c->C, c->len,
+  k_seed_walk<<<148 * (2048 / kSeedThreads), kSeedThreads, 0, s>>>(c->T, c->n_words, c->SDB, c->twin, c->next, c->F1, c->C, c->len,
                                                c->wlen, c->ctr);
   n += 3;
   prof_mark(s, "k_canon_scan");
