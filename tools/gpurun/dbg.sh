@@ -1,0 +1,1 @@
+timeout 600 python -m pytest tests -m gpu -x -q 2>&1 | grep -v "^\s*$" | tail -25
