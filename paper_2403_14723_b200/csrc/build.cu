@@ -615,6 +615,7 @@ __device__ __forceinline__ void tile_body(
     }
   }
   __syncthreads();
+  PHASE_MARK(6);
   if (tid * 32 < nhe) {
     const int64_t w = (e0 >> 5) + tid;
     C[w] = Cw[tid];

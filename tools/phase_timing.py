@@ -37,7 +37,8 @@ for r in range(reps + 1):
 torch.cuda.synchronize()
 L.polylla_debug_phase_cycles(buf.ctypes.data, 0)
 tiles = (tri.shape[0] + 2047) // 2048
-names = ["P0 clear", "P1 orient/lcode", "P2 hash", "P3 succ/out", "P4a jump", "P4b label/next", "-", "P5+P6 lists/seeds"]
+names = ["P0 clear", "P1 orient/lcode", "P2 hash", "P3 succ/out", "P4a jump", "P4b label/next", "P5+P6 lists/seeds",
+         "out (word stores)"]
 tot = buf[:8].sum()
 for i, nme in enumerate(names):
     print(f"{nme:18s} {buf[i] / (reps * tiles):10.0f} cycles/tile  {100 * buf[i] / tot:5.1f}%")
