@@ -144,6 +144,17 @@ POLYLLA_API polylla_status polylla_get_polygons(polylla_ctx* ctx, int32_t* offse
                                                 int32_t* loops, int64_t loops_cap, int32_t* origin, int32_t* twin,
                                                 int32_t* next, int32_t* prev, polylla_stream stream);
 
+/* Per-triangle polygon ids (the output polygons as unions of triangles: the terminal-edge
+ * regions of PAPER.md L76-L128 after the barrier repair):
+ *   poly_of_tri[t] = the index, in polylla_get_polygons' order, of the polygon whose loop
+ *   bounds the piece of t -- the triangles connected to t across non-frontier (F1 = 0)
+ *   edges; where several loops bound one piece (around a hole of the mesh), the smallest.
+ * poly_of_tri: device int32 [T], written by the caller-owned pointer; -1 is never written
+ * for a valid conversion.  Needs a previous polylla_get_polygons with offsets/loops on this
+ * ctx (it reads the polygon seeds; same stream, or synchronise), else E_CALL_ORDER.  Uses
+ * dead workspace scratch; asynchronous (4 launches). */
+POLYLLA_API polylla_status polylla_get_triangle_polygons(polylla_ctx* ctx, int32_t* poly_of_tri, polylla_stream stream);
+
 /* Device views into the workspace (valid until polylla_destroy / workspace reuse).
  * Any pointer argument may be NULL.  Sizes: origin/twin/next [H]; lcode [T] (k* of
  * each triangle); frontier0 / frontier1 / seed_bits: bit-vectors of uint32 words

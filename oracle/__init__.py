@@ -120,3 +120,35 @@ def run(xy: np.ndarray, tri: np.ndarray):
         times=dict(zip(PHASES, list(io.times))),
     )
     return out
+
+
+def triangle_polygons(ref: dict):
+    """Per-triangle polygon id, from a ``run`` result, by the
+    definition: the output polygons are unions of triangles (the terminal-edge regions of
+    PAPER.md L76-L128, split by the repair's middle edges).  A piece is a
+    connected component of the triangles joined across interior non-frontier (F1 = 0)
+    edges (library routine: scipy's connected_components); polygon p bounds the pieces of
+    the triangles of its loop's half-edges (walked from seeds[p] along next, PAPER.md L315);
+    poly_of_tri[t] = the smallest p bounding t's piece (several loops bound one piece only
+    around a hole).  Python loop over the loop entries: small and medium meshes only."""
+    import scipy.sparse as sp
+    from scipy.sparse.csgraph import connected_components
+
+    T = ref["T"]
+    e = np.arange(3 * T)
+    tw = ref["twin"][:3 * T].astype(np.int64)
+    m = (ref["frontier1"][:3 * T] == 0) & (tw < 3 * T) & (e < tw)
+    g = sp.coo_matrix((np.ones(int(m.sum())), (e[m] // 3, tw[m] // 3)), shape=(T, T))
+    _, comp = connected_components(g, directed=False)
+    best = np.full(comp.max() + 1, -1, np.int64)
+    nxt = ref["next"]
+    for p, s in enumerate(ref["seeds"].tolist()):
+        x = s
+        while True:
+            c = comp[x // 3]
+            if best[c] < 0:  # p ascends: the first polygon to reach a piece is its smallest
+                best[c] = p
+            x = int(nxt[x])
+            if x == s:
+                break
+    return best[comp].astype(np.int32)

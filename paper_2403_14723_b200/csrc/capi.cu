@@ -280,6 +280,7 @@ POLYLLA_API polylla_status polylla_get_polygons(polylla_ctx* p, int32_t* offsets
     const int n = launch_extract(c, offsets, offsets_cap, loops, loops_cap, prev, S(stream));
     if (n < 0) return POLYLLA_E_CUDA;
     c->launches += n;
+    c->extracted = true;
   } else if (offsets || loops) {
     return POLYLLA_E_INVALID_ARGUMENT;
   } else if (prev) {
@@ -294,6 +295,16 @@ POLYLLA_API polylla_status polylla_get_polygons(polylla_ctx* p, int32_t* offsets
     return POLYLLA_E_CUDA;
   if (next && cudaMemcpyAsync(next, c->next, hb, cudaMemcpyDefault, S(stream)) != cudaSuccess)
     return POLYLLA_E_CUDA;
+  return POLYLLA_OK;
+}
+
+POLYLLA_API polylla_status polylla_get_triangle_polygons(polylla_ctx* p, int32_t* poly_of_tri, polylla_stream stream) {
+  if (!p || !poly_of_tri) return POLYLLA_E_INVALID_ARGUMENT;
+  Ctx* c = &p->c;
+  if (!c->extracted) return POLYLLA_E_CALL_ORDER;
+  const int n = launch_regions(c, poly_of_tri, S(stream));
+  if (n < 0) return POLYLLA_E_CUDA;
+  c->launches += n;
   return POLYLLA_OK;
 }
 

@@ -85,6 +85,7 @@ struct Ctx {
   int32_t* next_pre;  // optional debug copy
   // host state
   int stage;          // 1 built, 2 labelled, 3 generated, 4 counted
+  bool extracted;     // polylla_get_polygons wrote the polygon seeds
   int64_t launches;
   polylla_counts host_counts;
   int64_t n_words;    // ceil(3T/32)
@@ -105,6 +106,7 @@ int launch_label(Ctx* c, cudaStream_t s);
 int launch_generate(Ctx* c, cudaStream_t s);
 int launch_extract(Ctx* c, int32_t* offsets, int64_t offsets_cap, int32_t* loops, int64_t loops_cap,
                    int32_t* prev, cudaStream_t s);
+int launch_regions(Ctx* c, int32_t* poly_of_tri, cudaStream_t s);
 
 // ------------------------------------------------------------------ device helpers
 __device__ __forceinline__ int32_t next_in(int32_t e) {  // 3f + (k+1)%3

@@ -28,7 +28,7 @@ EXPORTS = (
     "polylla_workspace_bytes", "polylla_build_halfedges", "polylla_label", "polylla_generate",
     "polylla_get_counts", "polylla_get_polygons", "polylla_get_views", "polylla_set_debug",
     "polylla_run_host", "polylla_destroy", "polylla_status_string", "polylla_launch_count",
-    "polylla_profile_enable", "polylla_profile_read",
+    "polylla_profile_enable", "polylla_profile_read", "polylla_get_triangle_polygons",
 )
 
 
@@ -74,6 +74,8 @@ def lib():
         L.polylla_get_counts.argtypes = [vp, vp, ctypes.POINTER(Counts)]
         L.polylla_get_polygons.restype = ctypes.c_int
         L.polylla_get_polygons.argtypes = [vp, i32p, i64, i32p, i64, i32p, i32p, i32p, i32p, vp]
+        L.polylla_get_triangle_polygons.restype = ctypes.c_int
+        L.polylla_get_triangle_polygons.argtypes = [vp, i32p, vp]
         L.polylla_get_views.restype = ctypes.c_int
         L.polylla_get_views.argtypes = [vp, ctypes.POINTER(Views)]
         L.polylla_set_debug.restype = ctypes.c_int
@@ -168,6 +170,13 @@ def get_polygons(ctx: Context, offsets, loops, origin=None, twin=None, next=None
     _check(rc, "polylla_get_polygons")
 
 
+def get_triangle_polygons(ctx: Context, poly_of_tri: torch.Tensor, stream=None) -> None:
+    """poly_of_tri (device int32 [T]) = index of the polygon containing each triangle;
+    after get_polygons (it needs the polygon seeds)."""
+    _check(lib().polylla_get_triangle_polygons(ctx.handle, _ptr(poly_of_tri), _stream(stream)),
+           "polylla_get_triangle_polygons")
+
+
 def set_debug(ctx: Context, next_pre: torch.Tensor | None) -> None:
     _check(lib().polylla_set_debug(ctx.handle, _ptr(next_pre)), "polylla_set_debug")
 
@@ -217,7 +226,8 @@ def status_string(code: int) -> str:
 
 # ----------------------------------------------------------------------- conveniences
 
-def run(xy: torch.Tensor, tri: torch.Tensor, stream=None, arrays=True, prev=False, debug=False) -> dict:
+def run(xy: torch.Tensor, tri: torch.Tensor, stream=None, arrays=True, prev=False, debug=False,
+        regions=False) -> dict:
     """build -> label -> generate -> get_counts -> get_polygons on device tensors.
     Returns a dict of torch tensors (offsets, loops, seeds, [origin, twin, next, prev],
     [lcode, frontier0, frontier1, seed_bits, next_pre]) plus the counts."""
@@ -244,6 +254,9 @@ def run(xy: torch.Tensor, tri: torch.Tensor, stream=None, arrays=True, prev=Fals
     if prev:
         out["prev"] = kw["prev"] = torch.empty(H, dtype=torch.int32, device=dev)
     get_polygons(ctx, out["offsets"], out["loops"], stream=stream, **kw)
+    if regions:
+        out["poly_of_tri"] = torch.empty(T, dtype=torch.int32, device=dev)
+        get_triangle_polygons(ctx, out["poly_of_tri"], stream)
     c2 = get_counts(ctx, stream)  # synchronises; surfaces a capacity error
     out["loops"] = out["loops"][:L]
     v = get_views(ctx)

@@ -18,9 +18,10 @@ cases = [synth.fixture_square(), synth.fixture_fan(), synth.fixture_tie_lattice(
 xy, tri = synth.random_delaunay(3000, 6)
 cases.append((xy, tri[np.random.default_rng(0).permutation(tri.shape[0])]))
 for xy, tri in cases:
-    r = pp.run(torch.from_numpy(xy).cuda(), torch.from_numpy(tri).cuda(), prev=True)
+    r = pp.run(torch.from_numpy(xy).cuda(), torch.from_numpy(tri).cuda(), prev=True, regions=True)
     o = oracle.run(xy, tri)
     for k in ("origin", "twin", "next", "prev"):
         assert np.array_equal(r[k].cpu().numpy(), o[k]), k
     assert np.array_equal(r["loops"].cpu().numpy(), o["loops"])
+    assert np.array_equal(r["poly_of_tri"].cpu().numpy(), oracle.triangle_polygons(o))
 print("sanitize cases ok", len(cases))

@@ -187,6 +187,37 @@ def test_high_degree_wheels():
     assert res["n_deferred"] > 0
 
 
+def _regions_case(name):
+    if name == "square":
+        return synth.fixture_square()
+    if name == "fan":
+        return synth.fixture_fan()
+    if name == "tie":
+        return synth.fixture_tie_lattice()
+    if name == "grid":
+        return synth.grid(64)
+    if name == "jittered":
+        return synth.grid(150, 0.2, 3)
+    if name == "random":
+        return synth.random_delaunay(200000, 6)
+    if name == "holes":
+        return _grid_with_holes()
+    if name == "wheels":
+        return _wheels()
+    xy, tri = synth.random_delaunay(30000, 9)  # shuffled: the global leftover path
+    return xy, np.ascontiguousarray(tri[np.random.default_rng(1).permutation(tri.shape[0])])
+
+
+@pytest.mark.parametrize("name", ["square", "fan", "tie", "grid", "jittered", "random", "holes", "wheels", "shuffled"])
+def test_triangle_polygons(name):
+    """polylla_get_triangle_polygons against the oracle's flood
+    definition, element by element (holes: several loops per piece -> the smallest)."""
+    xy, tri = _regions_case(name)
+    ref = oracle.run(xy, tri)
+    res = gpu_run(xy, tri, regions=True)
+    np.testing.assert_array_equal(res["poly_of_tri"].cpu().numpy(), oracle.triangle_polygons(ref))
+
+
 def test_determinism_and_streams():
     xy, tri = synth.random_delaunay(20000, 8)
     a = gpu_run(xy, tri)
@@ -273,6 +304,9 @@ def test_call_order_and_workspace_errors():
     ctx = pp.build_halfedges(xy, tri, ws)
     with pytest.raises(pp.PolyllaError) as ei:
         pp.generate(ctx)
+    assert pp.STATUS[ei.value.code] == "CALL_ORDER"
+    with pytest.raises(pp.PolyllaError) as ei:  # needs the polygon seeds of get_polygons
+        pp.get_triangle_polygons(ctx, torch.empty(2, dtype=torch.int32, device="cuda"))
     assert pp.STATUS[ei.value.code] == "CALL_ORDER"
     pp.destroy(ctx)
 

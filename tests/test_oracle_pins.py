@@ -246,3 +246,48 @@ def test_errors():
     assert _err([[0, 0], [1, 0], [0.5, 1], [0.5, 2]], [[0, 1, 2], [0, 1, 3]]) == "NON_MANIFOLD_EDGE"
     # bow-tie: two triangles sharing only vertex 0
     assert _err([[0, 0], [1, 0], [1, 1], [-1, 0], [-1, -1]], [[0, 1, 2], [0, 3, 4]]) == "NON_MANIFOLD_VERTEX"
+
+
+# ---- per-triangle polygon ids (oracle.triangle_polygons)
+
+def _signed_area2(xy, a, b, c):
+    return (xy[b, 0] - xy[a, 0]) * (xy[c, 1] - xy[a, 1]) - (xy[b, 1] - xy[a, 1]) * (xy[c, 0] - xy[a, 0])
+
+
+@pytest.mark.parametrize("s", [2, 3, 10])
+def test_triangle_polygons_grid_closed_form(s):
+    # Alg. 13 emits the two triangles of each cell together; every cell is one quad
+    # (closed form of test_grid_closed_forms), so triangle t lies in polygon t // 2
+    xy, tri = synth.grid(s)
+    o = oracle.triangle_polygons(oracle.run(xy, tri))
+    np.testing.assert_array_equal(o, np.arange(tri.shape[0]) // 2)
+
+
+def test_triangle_polygons_fixtures():
+    # square (Fig. 5): one polygon; fan F4: loops (0,1,2,3,4) <- triangles
+    # (0,1,2),(0,2,3),(0,3,4) and (0,4,5,1) <- (0,4,5),(0,5,1)
+    np.testing.assert_array_equal(oracle.triangle_polygons(oracle.run(*synth.fixture_square())), [0, 0])
+    np.testing.assert_array_equal(oracle.triangle_polygons(oracle.run(*synth.fixture_fan())), [0, 0, 0, 1, 1])
+    np.testing.assert_array_equal(oracle.triangle_polygons(oracle.run(*synth.fixture_triangle())), [0])
+
+
+@pytest.mark.parametrize("kind,arg,seed", [("random", 3000, 4), ("jittered", 40, 2)])
+def test_triangle_polygons_areas(kind, arg, seed):
+    # every polygon's loop area (shoelace) = the summed area of the triangles assigned to it,
+    # and every polygon owns at least one triangle (no holes: one loop per piece)
+    xy, tri = synth.random_delaunay(arg, seed) if kind == "random" else synth.grid(arg, 0.2, seed)
+    r = oracle.run(xy, tri)
+    o = oracle.triangle_polygons(r)
+    P = r["P"]
+    assert o.min() == 0 and o.max() == P - 1 and len(np.unique(o)) == P
+    t = r["origin"][:3 * r["T"]].reshape(-1, 3)
+    ta = _signed_area2(xy, t[:, 0], t[:, 1], t[:, 2])
+    assert (ta > 0).all()
+    tri_sum = np.bincount(o, weights=ta, minlength=P)
+    off, lp = r["offsets"], r["loops"]
+    nxt_idx = np.arange(len(lp)) + 1
+    poly_of_entry = np.repeat(np.arange(P), np.diff(off))
+    nxt_idx[off[1:] - 1] = off[:-1]  # wrap each loop
+    a, b = lp, lp[nxt_idx]
+    shoe = np.bincount(poly_of_entry, weights=xy[a, 0] * xy[b, 1] - xy[b, 0] * xy[a, 1], minlength=P)
+    np.testing.assert_allclose(shoe, tri_sum, rtol=1e-9, atol=1e-12 * np.abs(ta).max())
