@@ -5,7 +5,7 @@
 //   poly_of_tri[t] = min { p : the loop of polygon p bounds the piece of t }
 // (a piece has several loops only around a hole of the mesh).
 // GPU: lock-free union-find over the non-frontier interior edges (hook the larger root
-// under the smaller with CAS, path halving in find), then every polygon's canonical seed
+// under the smaller with CAS, path halving in find; per tile in shared memory first), then every polygon's canonical seed
 // (an interior half-edge of its loop, whose triangle lies in the piece) takes the min over
 // its root, and every triangle reads its root's value.
 #include "internal.cuh"
@@ -25,27 +25,76 @@ __device__ __forceinline__ int32_t uf_find(int32_t* parent, int32_t x) {
   }
 }
 
-__global__ void k_uf_init(int64_t T, int32_t* __restrict__ parent, int32_t* __restrict__ slot) {
-  for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < T; t += (int64_t)gridDim.x * blockDim.x) {
-    parent[t] = (int32_t)t;
-    slot[t] = INT32_MAX;
+__device__ __forceinline__ int32_t uf_find_s(volatile int32_t* p, int32_t x) {
+  while (true) {
+    const int32_t q = p[x];
+    if (q == x) return x;
+    const int32_t g = p[q];
+    if (q == g) return q;
+    p[x] = g;
+    x = g;
   }
 }
 
-// one thread per word of 32 interior half-edges: every non-frontier e < twin(e) unites
-// its two triangles (a non-frontier edge is interior on both sides)
-__global__ void k_uf_hook(int64_t T, int64_t n_words, const int32_t* __restrict__ twin, const uint32_t* __restrict__ F1,
-                          int32_t* parent, const DevCounters* ctr) {
+// One block per build tile of kBuildTileTris triangles: the unions whose two triangles lie
+// in the tile (most of them: triangles come in spatial order) in shared memory, then the
+// tile's forest goes out as the initial global parents (a local root keeps the smallest id
+// of its set, so parents still only decrease).
+constexpr int kUfTile = kBuildTileTris, kUfThreads = 512;
+__global__ void __launch_bounds__(kUfThreads) k_uf_local(int64_t T, const int32_t* __restrict__ twin,
+                                                  const uint32_t* __restrict__ F1, int32_t* __restrict__ parent,
+                                                  int32_t* __restrict__ slot) {
+  __shared__ int32_t p[kUfTile];
+  const int64_t t0 = (int64_t)blockIdx.x * kUfTile;
+  const int nt = T - t0 < kUfTile ? (int)(T - t0) : kUfTile;
+  for (int i = threadIdx.x; i < nt; i += blockDim.x) p[i] = i;
+  __syncthreads();
+  volatile int32_t* vp = p;
+  const int32_t e0 = (int32_t)(3 * t0);
+  constexpr int kIt = 3 * kUfTile / kUfThreads;
+  int32_t tws[kIt];
+#pragma unroll
+  // a thread takes kIt consecutive half-edges (4 triangles): neighbouring lanes then unite
+  // different pieces (interleaved lanes all hook the same few roots and retry their CAS)
+  for (int k = 0; k < kIt; ++k) {  // all of the thread's loads first (independent)
+    const int j = threadIdx.x * kIt + k;
+    tws[k] = j < 3 * nt && !bit_of(F1, e0 + j) ? __ldcs(twin + e0 + j) : -1;
+  }
+#pragma unroll
+  for (int k = 0; k < kIt; ++k) {
+    const int j = threadIdx.x * kIt + k;
+    const int32_t e = e0 + j, tw = tws[k];
+    if (tw < e || tw >= e0 + 3 * nt) continue;  // frontier; once per pair; cross-tile pairs: k_uf_hook
+    int32_t a = j / 3, b = (tw - e0) / 3;
+    while (true) {
+      a = uf_find_s(vp, a);
+      b = uf_find_s(vp, b);
+      if (a == b) break;
+      if (a < b) { const int32_t s = a; a = b; b = s; }
+      if (atomicCAS(p + a, a, b) == a) break;
+    }
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < nt; i += blockDim.x) {
+    parent[t0 + i] = (int32_t)t0 + uf_find_s(vp, i);
+    slot[t0 + i] = INT32_MAX;
+  }
+}
+
+// the cross-tile pairs: both halves of each are in k_tile's leftover lists (tile t:
+// entries [3 * kBuildTileTris * t, + cnt_ld[2t]) of left_e); one block per tile segment
+__global__ void k_uf_hook(int64_t ntiles, const int32_t* __restrict__ cnt_ld, const int32_t* __restrict__ left_e,
+                          const int32_t* __restrict__ twin, const uint32_t* __restrict__ F1, int32_t* parent,
+                          const DevCounters* ctr) {
   if (ctr->status) return;
-  const int64_t T3 = 3 * T;
-  for (int64_t w = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; w < n_words; w += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t e0 = w * 32;
-    uint32_t m = ~F1[w];
-    if (T3 - e0 < 32) m &= (1u << (T3 - e0)) - 1u;
-    for (; m; m &= m - 1) {
-      const int32_t e = (int32_t)(e0 + __ffs(m) - 1);
+  for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+    const int32_t n = cnt_ld[2 * tile];
+    const int64_t base = 3 * (int64_t)kBuildTileTris * tile;
+    for (int32_t k = threadIdx.x; k < n; k += blockDim.x) {
+      const int32_t e = left_e[base + k];
+      if (bit_of(F1, e)) continue;  // frontier (incl. the border ones)
       const int32_t tw = twin[e];
-      if (tw < e) continue;  // the pair is united once, from its lower half
+      if (tw < e) continue;  // once per pair, from its lower half
       int32_t a = e / 3, b = tw / 3;
       while (true) {
         a = uf_find(parent, a);
@@ -81,8 +130,9 @@ int launch_regions(Ctx* c, int32_t* poly_of_tri, cudaStream_t s) {
   int32_t* slot = parent + c->T;
   const unsigned g = 148 * 8;
   prof_mark(s, "k_regions");
-  k_uf_init<<<g, 256, 0, s>>>(c->T, parent, slot);
-  k_uf_hook<<<g, 256, 0, s>>>(c->T, c->n_words, c->twin, c->F1, parent, c->ctr);
+  k_uf_local<<<(unsigned)((c->T + kUfTile - 1) / kUfTile), kUfThreads, 0, s>>>(c->T, c->twin, c->F1, parent, slot);
+  const int64_t tiles = (c->T + kUfTile - 1) / kUfTile;
+  k_uf_hook<<<(unsigned)tiles, 256, 0, s>>>(tiles, c->cnt_ld, c->left_e, c->twin, c->F1, parent, c->ctr);
   k_uf_seed<<<g, 256, 0, s>>>(c->seeds, parent, slot, c->ctr);
   k_uf_out<<<g, 256, 0, s>>>(c->T, parent, slot, poly_of_tri, c->ctr);
   prof_end(s);
