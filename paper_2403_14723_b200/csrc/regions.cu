@@ -12,26 +12,47 @@
 
 namespace polylla {
 
+// global parents: relaxed GPU-scope atomic loads/stores (served by L2, like ld.cg)
+__device__ __forceinline__ int32_t ld_rlx_g(const int32_t* p) {
+  int32_t v;
+  asm volatile("ld.relaxed.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(p));
+  return v;
+}
+__device__ __forceinline__ void st_rlx_g(int32_t* p, int32_t v) {
+  asm volatile("st.relaxed.gpu.global.s32 [%0], %1;" ::"l"(p), "r"(v));
+}
+
 __device__ __forceinline__ int32_t uf_find(int32_t* parent, int32_t x) {
   // path halving; parents only ever decrease (a root is hooked under a smaller root), so a
   // racy halving store still points into the same tree
   while (true) {
-    const int32_t p = __ldcg(parent + x);
+    const int32_t p = ld_rlx_g(parent + x);
     if (p == x) return x;
-    const int32_t g = __ldcg(parent + p);
+    const int32_t g = ld_rlx_g(parent + p);
     if (p == g) return p;
-    __stcg(parent + x, g);
+    st_rlx_g(parent + x, g);
     x = g;
   }
 }
 
-__device__ __forceinline__ int32_t uf_find_s(volatile int32_t* p, int32_t x) {
+// shared-memory parents: relaxed CTA-scope atomic loads/stores (plain LDS/STS in SASS; the
+// halving stores race with the hooks' CAS by design, so they are atomics in the PTX memory
+// model, not data races)
+__device__ __forceinline__ int32_t ld_rlx_s(const int32_t* p) {
+  int32_t v;
+  asm volatile("ld.relaxed.cta.shared.s32 %0, [%1];" : "=r"(v) : "r"((uint32_t)__cvta_generic_to_shared(p)));
+  return v;
+}
+__device__ __forceinline__ void st_rlx_s(int32_t* p, int32_t v) {
+  asm volatile("st.relaxed.cta.shared.s32 [%0], %1;" ::"r"((uint32_t)__cvta_generic_to_shared(p)), "r"(v));
+}
+__device__ __forceinline__ int32_t uf_find_s(int32_t* p, int32_t x) {
   while (true) {
-    const int32_t q = p[x];
+    const int32_t q = ld_rlx_s(p + x);
     if (q == x) return x;
-    const int32_t g = p[q];
+    const int32_t g = ld_rlx_s(p + q);
     if (q == g) return q;
-    p[x] = g;
+    st_rlx_s(p + x, g);
     x = g;
   }
 }
@@ -49,7 +70,6 @@ __global__ void __launch_bounds__(kUfThreads) k_uf_local(int64_t T, const int32_
   const int nt = T - t0 < kUfTile ? (int)(T - t0) : kUfTile;
   for (int i = threadIdx.x; i < nt; i += blockDim.x) p[i] = i;
   __syncthreads();
-  volatile int32_t* vp = p;
   const int32_t e0 = (int32_t)(3 * t0);
   constexpr int kIt = 3 * kUfTile / kUfThreads;
   int32_t tws[kIt];
@@ -67,8 +87,8 @@ __global__ void __launch_bounds__(kUfThreads) k_uf_local(int64_t T, const int32_
     if (tw < e || tw >= e0 + 3 * nt) continue;  // frontier; once per pair; cross-tile pairs: k_uf_hook
     int32_t a = j / 3, b = (tw - e0) / 3;
     while (true) {
-      a = uf_find_s(vp, a);
-      b = uf_find_s(vp, b);
+      a = uf_find_s(p, a);
+      b = uf_find_s(p, b);
       if (a == b) break;
       if (a < b) { const int32_t s = a; a = b; b = s; }
       if (atomicCAS(p + a, a, b) == a) break;
@@ -76,7 +96,7 @@ __global__ void __launch_bounds__(kUfThreads) k_uf_local(int64_t T, const int32_
   }
   __syncthreads();
   for (int i = threadIdx.x; i < nt; i += blockDim.x) {
-    parent[t0 + i] = (int32_t)t0 + uf_find_s(vp, i);
+    parent[t0 + i] = (int32_t)t0 + uf_find_s(p, i);
     slot[t0 + i] = INT32_MAX;
   }
 }
