@@ -124,7 +124,8 @@ class Context:
     workspace: torch.Tensor
 
     def __del__(self):
-        destroy(self)
+        if destroy is not None:  # (module globals are already cleared at interpreter exit)
+            destroy(self)
 
 
 def workspace_bytes(n_vertices: int, n_triangles: int) -> int:
