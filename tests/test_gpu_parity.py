@@ -320,6 +320,33 @@ def test_config3_full():
 
 
 @pytest.mark.slow
+def test_config3_triangle_polygons_areas():
+    """Per-triangle polygon ids at the config-3 size, by properties that hold at any size
+    (device-side): ids in [0, P), every polygon owns a triangle, and each polygon's loop
+    area (shoelace over its CSR loop) equals the summed area of its triangles (rel 1e-9)."""
+    xy, tri = synth.random_delaunay(10_000_000, 3)
+    res = gpu_run(xy, tri, arrays=True, regions=True)
+    P = res["P"]
+    o = res["poly_of_tri"].long()
+    assert int(o.min()) == 0 and int(o.max()) == P - 1
+    xy_d = torch.from_numpy(xy).cuda()
+    t = res["origin"][:3 * tri.shape[0]].long().view(-1, 3)
+    a, b, c = xy_d[t[:, 0]], xy_d[t[:, 1]], xy_d[t[:, 2]]
+    ta = (b[:, 0] - a[:, 0]) * (c[:, 1] - a[:, 1]) - (b[:, 1] - a[:, 1]) * (c[:, 0] - a[:, 0])
+    tri_sum = torch.zeros(P, dtype=torch.float64, device="cuda").index_add_(0, o, ta)
+    off = res["offsets"].long()
+    lp = res["loops"].long()
+    nxt = torch.arange(1, lp.numel() + 1, device="cuda")
+    nxt[off[1:] - 1] = off[:-1]
+    pe = torch.repeat_interleave(torch.arange(P, device="cuda"), off[1:] - off[:-1])
+    base = xy_d[lp[off[:-1]]][pe]  # each loop relative to its first vertex (no cancellation)
+    u, v = xy_d[lp] - base, xy_d[lp[nxt]] - base
+    shoe = torch.zeros(P, dtype=torch.float64, device="cuda").index_add_(0, pe, u[:, 0] * v[:, 1] - v[:, 0] * u[:, 1])
+    assert bool((tri_sum > 0).all())
+    assert float(((shoe - tri_sum).abs() / tri_sum).max()) < 1e-9
+
+
+@pytest.mark.slow
 def test_config5_jittered_full():
     """A config-5 jittered mesh at full size (s = 2000, a = 0.2, seed 1000)."""
     xy, tri = synth.grid(2000, 0.2, 1000)
