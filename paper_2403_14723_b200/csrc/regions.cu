@@ -61,7 +61,11 @@ __device__ __forceinline__ int32_t uf_find_s(int32_t* p, int32_t x) {
 // in the tile (most of them: triangles come in spatial order) in shared memory, then the
 // tile's forest goes out as the initial global parents (a local root keeps the smallest id
 // of its set, so parents still only decrease).
-constexpr int kUfTile = kBuildTileTris, kUfThreads = 512;
+#ifndef POLYLLA_UF_THREADS
+#define POLYLLA_UF_THREADS 512  // measured 256 / 384 / 512 / 1024 on config 3: 512 best (0.46 ms)
+#endif
+constexpr int kUfTile = kBuildTileTris, kUfThreads = POLYLLA_UF_THREADS;
+static_assert(3 * kUfTile % kUfThreads == 0, "half-edges per thread");
 __global__ void __launch_bounds__(kUfThreads) k_uf_local(int64_t T, const int32_t* __restrict__ twin,
                                                   const uint32_t* __restrict__ F1, int32_t* __restrict__ parent,
                                                   int32_t* __restrict__ slot) {
