@@ -56,6 +56,9 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-graph", action="store_true", help="launch the C-ABI calls eagerly instead of a CUDA graph")
+    ap.add_argument("--order", default="morton", choices=["morton", "shuffled"],
+                    help="triangle order of configs 2/3 (sensitivity rows): generator Morton order or shuffled")
+    ap.add_argument("--no-pcie", action="store_true")
     return ap.parse_args()
 
 
@@ -72,7 +75,7 @@ def dist_setup():
     return ws, rank, local
 
 
-def workload(cfg: int, rank: int, world: int, device):
+def workload(cfg: int, rank: int, world: int, device, order: str = "morton"):
     """Synthetic input of BASELINE config `cfg` for this rank (recipes: DESIGN.md 'Input
     recipe').  Returns (description, scaling, [mesh dicts with xy/tri device tensors and,
     for the e2e leg, a host generator])."""
@@ -82,8 +85,10 @@ def workload(cfg: int, rank: int, world: int, device):
             name = "config1: jittered 32x32 grid (a=0.2), 1 mesh per GPU"
         else:
             n = 1_000_000 if cfg == 2 else 10_000_000
-            fn = lambda: synth.random_delaunay(n, cfg + 1000 * rank)  # noqa: E731
-            name = f"config{cfg}: {n // 1_000_000}M random points, Delaunay (Morton-ordered triangles), 1 mesh per GPU"
+            fn = lambda: (lambda xy, tri: (xy, reorder(tri, order)))(*synth.random_delaunay(n, cfg + 1000 * rank))  # noqa: E731
+            name = (f"config{cfg}: {n // 1_000_000}M random points, Delaunay ({order}-ordered triangles: "
+                    f"{'centroid Morton order of the generator' if order == 'morton' else 'seeded random permutation'})"
+                    f", 1 mesh per GPU")
         xy, tri = fn()
         m = dict(xy=torch.from_numpy(xy).to(device), tri=torch.from_numpy(tri).to(device), host=lambda: (xy, tri),
                  xy_np=xy, tri_np=tri)
@@ -168,76 +173,204 @@ class ClockSampler:
                 "reasons": sorted(self.reasons), "samples": len(self.samples)}
 
 
-def alg_bytes(T, V, P, L):
-    """Algorithmic bytes: the method's compulsory HBM traffic."""
+def alg_bytes(T, V, P, L, c=None):
+    """Algorithmic bytes per launch of each kernel group (DESIGN.md section 6 states each
+    model).  "pipeline" is SURVEY.md 8(d)'s B_alg = 60T + 16V + 12L + 4P, the method's
+    compulsory HBM traffic for one mesh; the group models split the same accounting over
+    the kernels (what each must read or write once), plus the FP32 coordinate copy that
+    this design adds (k_xy32, not part of B_alg).  c: the mesh's polylla counts."""
+    c = c or {}
+    n_left, n_def = c.get("n_leftover", 0), c.get("n_deferred", 0)
+    n_sdef, tips, B = c.get("n_seed_deferred", 0), c.get("n_tips", 0), c.get("n_border", 0)
+    tiles = (T + 2047) // 2048
+    mean_loop = L / P if P else 0.0
     return {
         "pipeline": 60 * T + 16 * V + 12 * L + 4 * P,
-        # tri in + xy once + origin/twin/next out + Lcode out + F0/F1/S/C bit-vectors out
-        "k_tile": 12 * T + 16 * V + 36 * T + T + 4 * (3 * T) // 8,
-        # k_emit (profile group "k_extract"): C bits + len at the canonical seeds in, next +
-        # origin along the loops, seeds + offsets + loops out
+        # 16 B per vertex in, 8 B out
+        "k_xy32": 24 * V,
+        # B_alg's build rows: tri in (12T), origin/twin/next out (36T), the coordinates once
+        # (the 8-B FP32 copy; the FP64 array is read only for the few undecided triangles)
+        "k_tile": 48 * T + 8 * V,
+        # per leftover: key + id in (12 B), twin out (4 B), border ranking re-reads id + twin (8 B)
+        "k_left_match": 24 * n_left,
+        # per border half-edge: blist, twin[e], origin[target] in; twin[e], twin[b], origin[b], vmap out
+        "k_border_scan": 28 * B + 8 * tiles,
+        # per border half-edge: origin[b], twin[b], origin[twin], vmap x2, origin[nx] in; next out
+        "k_border_next": 28 * B,
+        # per deferred half-edge: id, twin, Lcode x2 in, next out, + one rotation step (twin, Lcode x2)
+        "k_label_fixup": 22 * n_def,
+        # per tip: the degree walk about v (~6 twins) + middle-edge steps, F1/SDB words, and the
+        # re-rewire of the two touched vertices (~2 x 6 x (twin + F1 + next))
+        "k_repair": 96 * tips,
+        # per global seed: F1 word + landing, then the loop walk (next per step), len/C/wlen out
+        "k_seed_walk": int(n_sdef * (16 + 4 * mean_loop)),
+        # C, wlen and F1 words in (12 B per 32 half-edges), per-tile sums
+        "k_canon_scan": (12 * 3 * T) // 32 + 24 * tiles,
+        # C bits + len at the canonical seeds in, next + origin along the loops, seeds +
+        # offsets + loops out
         "k_extract": (3 * T) // 8 + 4 * P + 8 * L + 4 * P + 4 * (P + 1) + 4 * L,
     }
 
 
+def src_hash():
+    """Hash of the CUDA sources: ties a committed ncu traffic figure to this build."""
+    import hashlib
+    h = hashlib.sha256()
+    d = os.path.join(ROOT, "paper_2403_14723_b200", "csrc")
+    for f in sorted(os.listdir(d)):
+        if f.endswith((".cu", ".cuh")):
+            h.update(open(os.path.join(d, f), "rb").read())
+    h.update(open(os.path.join(ROOT, "include", "polylla.h"), "rb").read())
+    return h.hexdigest()[:16]
+
+
 def ncu_traffic(kernel: str, cfg: int):
-    """dram__bytes_read+write per launch of `kernel` from the committed ncu summary."""
+    """dram__bytes_read + write per launch of `kernel`, from the committed `ncu --set full`
+    capture of this build (profiles/ncu_traffic.json, written by
+    profiles/tools/ncu_traffic.py with the source hash it was captured on); None if the
+    capture is of other sources."""
     p = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     try:
         with open(p) as f:
             d = json.load(f)
+        if d.get("src_hash") != src_hash():
+            return None
         return d.get(f"config{cfg}", {}).get(kernel)
     except Exception:
         return None
 
 
+def host_cpu():
+    model = "?"
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                model = line.split(":", 1)[1].strip()
+                break
+    except OSError:
+        pass
+    return {"model": model, "logical_cpus": os.cpu_count()}
+
+
+def _pinned_one_core(fn):
+    """Run fn() with this thread pinned to one CPU (the taskset -c of SURVEY.md 8(d))."""
+    try:
+        old = os.sched_getaffinity(0)
+        cpu = min(old)
+        os.sched_setaffinity(0, {cpu})
+    except (AttributeError, OSError):
+        old, cpu = None, None
+    try:
+        return fn(), cpu
+    finally:
+        if old is not None:
+            os.sched_setaffinity(0, old)
+
+
 def cpu_oracle_baseline(xy, tri):
-    """Time the CPU oracle on a bounded sample of the workload (rank 0, N = 1)."""
+    """Time the CPU oracle (built on this host with -O3 -march=native -ffp-contract=off,
+    one thread pinned to one core) on a bounded sample of the workload (rank 0, N = 1)."""
     import oracle
+    oracle.use_native()
     T = tri.shape[0]
     if T <= 25_000_000:
         sample_xy, sample_tri, what = xy, tri, f"the full bench mesh ({T} triangles), 1 run"
     else:
-        sample_xy, sample_tri = synth.random_delaunay(2_000_000, 99)
-        what = f"a 2M-point random Delaunay mesh of the same recipe ({sample_tri.shape[0]} triangles), 1 run"
+        n = 2_000_000
+        sample_xy, sample_tri = xy, np.ascontiguousarray(tri[:n])
+        what = f"the first {n} triangles of the bench mesh (a contiguous block of it), 1 run"
     t0 = time.perf_counter()
-    o = oracle.run(sample_xy, sample_tri)
+    o, cpu = _pinned_one_core(lambda: oracle.run(sample_xy, sample_tri))
     dt = time.perf_counter() - t0
     return {"value": sample_tri.shape[0] / dt, "unit": "triangles/s", "cores": 1, "kind": "oracle",
-            "sample": what, "seconds": dt, "phases_s": o["times"]}
+            "sample": what, "seconds": dt, "phases_s": o["times"], "pinned_cpu": cpu,
+            "build": "gcc -O3 -march=native -ffp-contract=off (on this host)", "host": host_cpu()}
 
 
 def reference_arm(args, ws, rank):
-    """--impl reference: the CPU oracle, unmodified, as the reference arm."""
+    """--impl reference: the CPU oracle, unmodified, as the reference arm: each step runs
+    the oracle (one thread pinned to one core, -O3 -march=native) on a bounded sample of
+    the SAME workload -- the first n triangles of the bench mesh (triangles come in Morton
+    order, so this is a compact block of the mesh), n sized so the run ends in ~3 min."""
     if rank != 0:
         return
     import oracle
+    oracle.use_native()
     steps, warm = args.steps, args.warmup
-    # calibrate: oracle throughput on a small mesh of the same recipe
-    cxy, ctri = synth.random_delaunay(100_000, 7)
+    name, xy, tri = host_workload(args.config, args.order)
+    # calibrate on a small block of the same mesh
+    nc = min(tri.shape[0], 200_000)
     t0 = time.perf_counter()
-    oracle.run(cxy, ctri)
-    rate = ctri.shape[0] / (time.perf_counter() - t0)
-    budget = 150.0 / max(1, steps + warm)  # seconds per step so the run ends in ~2.5 min
-    n = int(min(10_000_000, max(2_000, 0.5 * rate * budget)))
-    sxy, stri = synth.random_delaunay(n, 3)
+    _pinned_one_core(lambda: oracle.run(xy, np.ascontiguousarray(tri[:nc])))
+    rate = nc / (time.perf_counter() - t0)
+    budget = 150.0 / max(1, steps + warm)  # seconds per step
+    n = int(min(tri.shape[0], max(2_000, 0.7 * rate * budget)))
+    stri = np.ascontiguousarray(tri[:n])
     for _ in range(warm):
-        oracle.run(sxy, stri)
+        _pinned_one_core(lambda: oracle.run(xy, stri))
     t0 = time.perf_counter()
     for _ in range(steps):
-        oracle.run(sxy, stri)
+        _, cpu = _pinned_one_core(lambda: oracle.run(xy, stri))
     dt = time.perf_counter() - t0
-    T = stri.shape[0]
-    v = T * steps / dt
-    what = f"{n}-point random Delaunay mesh (config-{args.config} recipe, {T} triangles) per step"
+    v = n * steps / dt
+    what = (f"the first {n} of the {tri.shape[0]} triangles of the bench mesh ({name}) per step"
+            if n < tri.shape[0] else f"the full bench mesh ({name}) per step")
     print(json.dumps({
         "impl": "reference", "metric": METRIC, "value": v, "unit": "triangles/s", "n_gpus": ws,
         "steps": steps, "warmup": warm, "ms_per_step": 1e3 * dt / steps, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "f64/i32", "data": "synthetic",
-        "config": {"workload": what},
-        "cpu_baseline": {"value": v, "unit": "triangles/s", "cores": 1, "kind": "oracle", "sample": what},
+        "config": {"workload": name, "sample": what},
+        "cpu_baseline": {"value": v, "unit": "triangles/s", "cores": 1, "kind": "oracle", "sample": what,
+                         "pinned_cpu": cpu, "build": "gcc -O3 -march=native -ffp-contract=off",
+                         "host": host_cpu()},
         "e2e": {"value": v, "unit": "triangles/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }), flush=True)
+
+
+def host_workload(cfg: int, order: str = "morton"):
+    """The host copy of a single-mesh workload (configs 1-3; 4 and 5 use a 2000-grid)."""
+    if cfg == 1:
+        xy, tri = synth.grid(32, 0.2, 1)
+        return "config1: jittered 32x32 grid (a=0.2)", xy, tri
+    if cfg in (2, 3):
+        n = 1_000_000 if cfg == 2 else 10_000_000
+        xy, tri = synth.random_delaunay(n, cfg)
+        tri = reorder(tri, order)
+        return f"config{cfg}: {n // 1_000_000}M random points, Delaunay ({order} triangle order)", xy, tri
+    xy, tri = synth.grid(2000, 0.2, 1000)
+    return "config5 mesh 0: jittered 2000x2000 grid (a=0.2)", xy, tri
+
+
+def reorder(tri, order: str):
+    """Triangle order of the input (a sensitivity row of SURVEY.md 8(d)): "morton" is the
+    generator's order (centroid Morton code); "shuffled" a seeded random permutation (the
+    worst case for tile-local twin matching: almost every twin crosses tiles)."""
+    if order == "morton":
+        return tri
+    perm = np.random.default_rng(12345).permutation(tri.shape[0])
+    return np.ascontiguousarray(tri[perm])
+
+
+def pcie_bandwidth(dev, nbytes=256 << 20, reps=5):
+    """Pinned host <-> device copy bandwidth (GB/s), each direction alone (CUDA events)."""
+    h = torch.empty(nbytes, dtype=torch.uint8, pin_memory=True)
+    d = torch.empty(nbytes, dtype=torch.uint8, device=dev)
+    out = {}
+    for name, (dst, src) in (("h2d_gbs", (d, h)), ("d2h_gbs", (h, d))):
+        dst.copy_(src, non_blocking=True)
+        torch.cuda.synchronize(dev)
+        best = None
+        for _ in range(reps):
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            dst.copy_(src, non_blocking=True)
+            e1.record()
+            e1.synchronize()
+            ms = e0.elapsed_time(e1)
+            best = ms if best is None else min(best, ms)
+        out[name] = nbytes / (best * 1e-3) / 1e9
+    out["bytes_per_copy"] = nbytes
+    return out
 
 
 def main():
@@ -255,7 +388,7 @@ def main():
     dev = torch.device("cuda", local if ws > 1 else 0)
     if ws > 1:
         import torch.distributed as dist
-    name, scaling, meshes = workload(args.config, rank, ws, dev)
+    name, scaling, meshes = workload(args.config, rank, ws, dev, args.order)
     Vmax = max(m["xy"].shape[0] for m in meshes)
     Tmax = max(m["tri"].shape[0] for m in meshes)
     wsp = pp.alloc_workspace(Vmax, Tmax, dev)
@@ -380,15 +513,22 @@ def main():
     prof_step_ms = sum(ms for ms, _ in prof.values()) / prof_steps
     nm = len(meshes)
     # algorithmic bytes per launch (one mesh per launch; meshes of a batch have equal size)
-    ab = alg_bytes(local_T // nm, local_V // nm, local_P // nm, local_L // nm)
+    ab = alg_bytes(local_T // nm, local_V // nm, local_P // nm, local_L // nm, meshes[0]["counts"])
     peak, peak_src = load_peaks()
-    top = max((k for k in per_launch if k in ab), key=lambda k: per_launch[k])
+    # the dominant kernel group: the largest share of the step (every group has a byte model)
+    groups = {k: v for k, v in per_launch.items() if k in ab}
+    missing = sorted(k for k in per_launch if k not in ab)
+    top = max(groups, key=lambda k: groups[k] * prof[k][1])
     achieved = ab[top] / (per_launch[top] * 1e-3) / 1e9
     traffic = ncu_traffic(top, args.config)
     roof = {"bound": "hbm", "kernel": top, "achieved": achieved, "peak": peak, "unit": "GB/s",
             "frac": achieved / peak, "traffic": traffic, "alg_bytes_per_launch": ab[top],
-            "kernel_ms": per_launch[top], "share_of_step": per_launch[top] * nm / prof_step_ms,
-            "peak_source": peak_src}
+            "kernel_ms": per_launch[top], "share_of_step": per_launch[top] * prof[top][1] / prof_steps / prof_step_ms,
+            "peak_source": peak_src, "traffic_source": "profiles/ncu_traffic.json (ncu --set full capture of this "
+                                                        "source hash)" if traffic else "no capture of this build",
+            "groups_without_model": missing}
+    group_roof = {k: {"ms": per_launch[k] * prof[k][1] / prof_steps, "alg_bytes": ab[k],
+                      "frac": ab[k] / (per_launch[k] * 1e-3) / 1e9 / peak} for k in groups}
     pipe_gbs = ab["pipeline"] * nm / (ms_step * 1e-3) / 1e9  # per GPU
     pipeline_roof = {"alg_bytes_per_step_per_gpu": ab["pipeline"] * nm, "achieved": pipe_gbs, "peak": peak,
                      "frac": pipe_gbs / peak, "frac_of_8TBs_nominal": pipe_gbs / 8000.0}
@@ -434,6 +574,11 @@ def main():
         e2e["single_call_ms"] = 1e3 * (time.perf_counter() - t0) / 3
         assert cnts[-1]["n_polygons"] == meshes[(len(inputs) - 1) % len(meshes)]["counts"]["n_polygons"]
 
+    if e2e is not None and not args.no_pcie:
+        e2e["pcie"] = pcie_bandwidth(dev)
+        e2e["pcie"]["copy_bound_ms_per_step"] = 1e3 * max(e2e["h2d_bytes_per_step"] / (e2e["pcie"]["h2d_gbs"] * 1e9),
+                                                            e2e["d2h_bytes_per_step"] / (e2e["pcie"]["d2h_gbs"] * 1e9))
+
     cpu = None
     if rank == 0 and ws == 1 and not args.no_cpu_baseline:
         if meshes[0].get("host") is not None:
@@ -457,7 +602,7 @@ def main():
                        "l2": "no flush: per-step inputs and working set exceed the 126 MB L2" if args.config >= 3
                              else "small working set: L2-resident between steps (reported, not the headline)"},
             "polygons_per_s": all_P * args.steps / (ms_total / 1e3),
-            "roofline": roof, "pipeline_roofline": pipeline_roof,
+            "roofline": roof, "pipeline_roofline": pipeline_roof, "group_roofline": group_roof,
             "kernels_ms_per_step": {k: ms / prof_steps for k, (ms, _) in prof.items()},
             "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches[0] * args.steps,
             "launch_mode": ("cuda_graph (one graph launch per step)" if graphs else

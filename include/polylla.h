@@ -110,6 +110,18 @@ POLYLLA_API polylla_status polylla_build_halfedges(const double* xy, int64_t n_v
                                                    int64_t n_triangles, void* workspace, size_t workspace_bytes,
                                                    polylla_stream stream, polylla_ctx** ctx_out);
 
+/* Exact non-manifold-edge check (SPEC.md L49 NonManifoldEdge), opt-in.  The build
+ * detects an edge in more than two triangles (or twice in one direction) when all of
+ * its copies fall in one 2,048-triangle build tile or all of them cross tiles; a copy
+ * that pairs inside its tile while a further copy lies in another tile is seen only by
+ * this pass (R20).  Every interior half-edge looks its undirected key up in a
+ * global hash (dead workspace scratch); a second copy in the same direction, or a third
+ * copy, ORs POLYLLA_E_NON_MANIFOLD_EDGE into the device status (returned by the next
+ * polylla_get_counts).  Call after polylla_build_halfedges and before
+ * polylla_get_triangle_polygons / a host-pointer prev (which reuse the same scratch);
+ * asynchronous (2 launches). */
+POLYLLA_API polylla_status polylla_check_manifold(polylla_ctx* ctx, polylla_stream stream);
+
 /* Label phase (Alg. 8-9): frontier bits F[e] = border(e) or
  * border(twin e) or (not L[e] and not L[twin e]); seed bits for terminal and
  * terminal-border edges on the smaller interior half-edge.  Fused with the unlink
@@ -137,8 +149,11 @@ POLYLLA_API polylla_status polylla_get_counts(polylla_ctx* ctx, polylla_stream s
  * polygon p is loops[offsets[p] .. offsets[p+1]) = origin[x0], origin[x1], ... with
  * x0 = seeds[p] (ascending canonical seeds) and x_{i+1} = next[x_i].  origin, twin,
  * next, prev: optional [H] outputs (NULL to skip; device or host pointers; copied
- * with cudaMemcpyAsync).  prev is the inverse of next on frontier and border
- * half-edges and prev_in elsewhere.  Asynchronous; a too-small capacity sets
+ * with cudaMemcpyAsync -- origin/twin/next and a host prev need polylla_get_counts
+ * first, for H).  prev is the inverse of next on frontier and border half-edges and
+ * prev_in elsewhere; it is built on the device (into the caller's array when that is
+ * device memory, else into workspace scratch that is then copied out).  offsets and
+ * loops are both given or both NULL.  Asynchronous; a too-small capacity sets
  * POLYLLA_E_CAPACITY in the device status. */
 POLYLLA_API polylla_status polylla_get_polygons(polylla_ctx* ctx, int32_t* offsets, int64_t offsets_cap,
                                                 int32_t* loops, int64_t loops_cap, int32_t* origin, int32_t* twin,
@@ -151,8 +166,10 @@ POLYLLA_API polylla_status polylla_get_polygons(polylla_ctx* ctx, int32_t* offse
  *   edges; where several loops bound one piece (around a hole of the mesh), the smallest.
  * poly_of_tri: device int32 [T], written by the caller-owned pointer; -1 is never written
  * for a valid conversion.  Needs a previous polylla_get_polygons with offsets/loops on this
- * ctx (it reads the polygon seeds; same stream, or synchronise), else E_CALL_ORDER.  Uses
- * dead workspace scratch; asynchronous (4 launches). */
+ * ctx (it reads the polygon seeds; same stream, or synchronise), else E_CALL_ORDER.  The
+ * ids are valid only if a later polylla_get_counts returns POLYLLA_OK: when the device
+ * status is set (e.g. a capacity error in get_polygons, so no seeds were written) every
+ * entry is -1.  Uses dead workspace scratch; asynchronous (4 launches). */
 POLYLLA_API polylla_status polylla_get_triangle_polygons(polylla_ctx* ctx, int32_t* poly_of_tri, polylla_stream stream);
 
 /* Device views into the workspace (valid until polylla_destroy / workspace reuse).

@@ -48,13 +48,34 @@ class _IO(ctypes.Structure):
         ("offsets", ctypes.c_void_p), ("loops", ctypes.c_void_p),
         ("tips", ctypes.c_void_p),
         ("counts", ctypes.c_int64 * 10), ("times", ctypes.c_double * 8),
+        ("hcap", ctypes.c_int64),
     ]
+
+
+_PATH = os.path.join(_HERE, "liboracle.so")
+
+
+def use_native() -> str:
+    """Switch to a copy of the oracle compiled on THIS host with -O3 -march=native
+    -ffp-contract=off (the timing build of SURVEY.md 8(d); no FMA, so bit-identical
+    results), cached in a temporary directory.  Returns its path."""
+    global _LIB, _PATH
+    import subprocess
+    import tempfile
+    src = os.path.join(_HERE, "polylla_oracle.c")
+    out = os.path.join(tempfile.gettempdir(), f"liboracle_native_{os.getuid()}_{int(os.path.getmtime(src))}.so")
+    if not os.path.exists(out):
+        subprocess.run(["gcc", "-O3", "-march=native", "-std=c11", "-ffp-contract=off", "-fPIC", "-shared",
+                        "-o", out + ".tmp", src], check=True)
+        os.replace(out + ".tmp", out)
+    _PATH, _LIB = out, None
+    return out
 
 
 def _lib():
     global _LIB
     if _LIB is None:
-        path = os.path.join(_HERE, "liboracle.so")
+        path = _PATH
         if not os.path.exists(path):
             raise RuntimeError(f"{path} missing: run __graft_entry__.build()")
         lib = ctypes.CDLL(path)
@@ -86,12 +107,14 @@ def build(xy: np.ndarray, tri: np.ndarray):
                 flips=int(hb[2]))
 
 
-def run(xy: np.ndarray, tri: np.ndarray):
-    """Full sequential Polylla (Alg. 1).  Returns a dict of numpy arrays + counts + times."""
+def run(xy: np.ndarray, tri: np.ndarray, hcap: int | None = None):
+    """Full sequential Polylla (Alg. 1).  Returns a dict of numpy arrays + counts + times.
+    hcap: capacity of the [H] arrays when the caller knows a bound on H = 3T + B (the
+    default 6T covers any mesh; huge meshes pass a tight bound to fit host memory)."""
     xy = np.ascontiguousarray(xy, dtype=np.float64)
     tri = np.ascontiguousarray(tri, dtype=np.int32)
     V, T = xy.shape[0], tri.shape[0]
-    H = 6 * max(T, 1)
+    H = int(hcap) if hcap else 6 * max(T, 1)
     a = dict(
         origin=np.empty(H, np.int32), twin=np.empty(H, np.int32), next=np.empty(H, np.int32),
         prev=np.empty(H, np.int32), next_pre=np.empty(H, np.int32),
@@ -103,6 +126,7 @@ def run(xy: np.ndarray, tri: np.ndarray):
     )
     io = _IO()
     io.T, io.V = T, V
+    io.hcap = H
     io.xy, io.tri = xy.ctypes.data, tri.ctypes.data
     for k, v in a.items():
         setattr(io, k, v.ctypes.data)

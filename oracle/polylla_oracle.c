@@ -46,6 +46,7 @@ enum {
 /* ---------------------------------------------------------------- half-edge mesh */
 typedef struct {
   int64_t T, H, B, V;
+  int64_t Hcap; /* capacity of origin/twin/next/prev (the build returns NOMEM if H exceeds it) */
   const double* xy;
   int32_t* origin; /* [H] */
   int32_t* twin;   /* [H] */
@@ -136,6 +137,7 @@ static int build(mesh* m, const int32_t* tri, int64_t* flips_out) {
     if (m->twin[e] < 0) ++B;
   if (3 * T + B > INT32_MAX) return OR_E_INDEX_OVERFLOW;
   const int64_t H = 3 * T + B;
+  if (H > m->Hcap) return OR_E_NOMEM;
   m->B = B;
   m->H = H;
   int64_t b = 3 * T;
@@ -308,6 +310,7 @@ typedef struct {
   int32_t *tips;         /* [<=V] barrier tips found (vertex ids, discovery order) */
   int64_t counts[10];    /* H, B, flips, n_seeds0, P, L, n_tips, n_mid_edges, rot_steps, 0 */
   double times[8];       /* Build, LM, LF, LS, Trav, Rep, Extract, total (seconds) */
+  int64_t hcap;          /* capacity of the [H] arrays if > 0 (else 6T); memory only, not arithmetic */
 } oracle_io;
 
 /* Alg. 1: Label (Alg. 2-4) -> Traversal (Alg. 5 per seed) ->
@@ -317,11 +320,11 @@ int oracle_run(oracle_io* io) {
   const double t_start = now_s();
   const int64_t T = io->T;
   if (T < 1 || io->V < 3 || !io->xy || !io->tri) return OR_E_INVALID_ARGUMENT;
-  mesh M = {T, 0, 0, io->V, io->xy, io->origin, io->twin, NULL, NULL, NULL};
+  /* mesh_input next/prev live in scratch; io->next/prev are mesh_output */
+  const int64_t Hcap = io->hcap > 0 ? io->hcap : 6 * T;
+  mesh M = {T, 0, 0, io->V, Hcap, io->xy, io->origin, io->twin, NULL, NULL, NULL};
   M.incident = (int32_t*)malloc((size_t)io->V * sizeof(int32_t));
   if (!M.incident) return OR_E_NOMEM;
-  /* mesh_input next/prev live in scratch; io->next/prev are mesh_output */
-  const int64_t Hcap = 6 * T;
   M.next = (int32_t*)malloc((size_t)Hcap * sizeof(int32_t));
   M.prev = (int32_t*)malloc((size_t)Hcap * sizeof(int32_t));
   if (!M.next || !M.prev) return OR_E_NOMEM;
@@ -455,7 +458,7 @@ int oracle_run(oracle_io* io) {
 /* Stand-alone build for the mesh-core pins. */
 int oracle_build(int64_t V, const double* xy, int64_t T, const int32_t* tri, int32_t* origin,
                  int32_t* twin, int32_t* next, int32_t* prev, int64_t* HB_flips) {
-  mesh M = {T, 0, 0, V, xy, origin, twin, next, prev, NULL};
+  mesh M = {T, 0, 0, V, 6 * T, xy, origin, twin, next, prev, NULL};
   int64_t flips = 0;
   const int rc = build(&M, tri, &flips);
   HB_flips[0] = M.H; HB_flips[1] = M.B; HB_flips[2] = flips;

@@ -20,6 +20,7 @@
 //                                         border half-edges, border-vertex map;
 //   k_border_next                      -- next(b) = border half-edge leaving target(b).
 #include <cstdlib>
+#include <mutex>
 
 #include "internal.cuh"
 
@@ -37,7 +38,9 @@ constexpr int kTileWords = kTileHE / 32; // 192
 constexpr int kTriIters = (kTileTris + kTileThreads - 1) / kTileThreads;  // 768: 3 (the third: threads < 512)
 constexpr int kHeIters = kTileHE / kTileThreads;                           // 768: 8 exactly
 static_assert(kTileHE % kTileThreads == 0 && kTileThreads % 3 != 2, "half-edge loops: q_step below");
-static_assert(kTileThreads % 32 == 0 && (kTileTris - 2 * kTileThreads) % 32 == 0, "warp-uniform third triangle");
+static_assert(kTileThreads % 32 == 0 && (kTileTris - (kTriIters - 1) * kTileThreads) % 32 == 0,
+              "warp-uniform last triangle iteration");
+static_assert(4 * kTriIters <= 32, "per-lane pending bit masks");
 // quad of half-edge j + kTileThreads from the quad q of j (no division): 768 = 3 * 256
 // -> q + 1024; 1024 = 3 * 341 + 1 -> q + 1365, skipping the padding slot k = 3
 constexpr int kQStep = 4 * (kTileThreads / 3) + kTileThreads % 3;
@@ -72,6 +75,10 @@ constexpr int kTileJumps = POLYLLA_TILE_JUMPS;
 #endif
 constexpr int kP4bUnroll = POLYLLA_P4B_UNROLL;  // P4b loop unroll (1 / 2 / 4 measured: 2 best)
 constexpr int kTileHops = (16 >> kTileJumps) - 1;
+#ifndef POLYLLA_P6_MAXLEN
+#define POLYLLA_P6_MAXLEN 1024  // (a test variant sets it tiny to force the global seed walk)
+#endif
+constexpr int kP6MaxLen = POLYLLA_P6_MAXLEN;  // in-tile loop walks longer than this go to k_seed_walk
 
 #ifdef POLYLLA_PHASE_TIMING
 __device__ unsigned long long g_phase_cycles[16];
@@ -175,10 +182,11 @@ __device__ __noinline__ int32_t tile_lookup_probe(const uint32_t* slot, const in
 }
 
 // is triangle slot i (t = tid + 768 i) of this thread inside the tile?  For a full tile
-// this is compile-time true for i < 2 and warp-uniform for i = 2 (threads < 512).
+// this is compile-time true for all but the last iteration and warp-uniform for the last
+// (768 threads: i < 2 always, i = 2 for threads < 512).
 template <bool FULL>
 __device__ __forceinline__ bool tri_ok(int i, int t, int nt) {
-  return FULL ? (i < 2 || threadIdx.x < kTileTris - 2 * kTileThreads) : t < nt;
+  return FULL ? (i < kTriIters - 1 || threadIdx.x < kTileTris - (kTriIters - 1) * kTileThreads) : t < nt;
 }
 
 // One CTA per tile of kTileTris triangles.  Phases (PAPER.md section in brackets):
@@ -257,10 +265,8 @@ __device__ __forceinline__ void tile_body(
   const uint64_t pol = policy_evict_last();
   uint32_t bad = 0;
   int flips = 0;
-#pragma unroll
-  for (int i = 0; i < kTriIters; ++i) {
-    const int t = tid + i * kTileThreads;
-    if (!tri_ok<FULL>(i, t, nt)) continue;
+  // the FP64 decisions (R11: IEEE RN, no FMA)
+  auto orient_tri = [&](int t) {
     int32_t a = raw[3 * t], b = raw[3 * t + 1], c = raw[3 * t + 2];
     if ((uint64_t)a >= (uint64_t)V || (uint64_t)b >= (uint64_t)V || (uint64_t)c >= (uint64_t)V) {
       bad |= ST_DANGLING;
@@ -284,6 +290,12 @@ __device__ __forceinline__ void tile_body(
     lc_s[t] = (uint8_t)k;
     lcode[f0 + t] = (uint8_t)k;
     tri_q4[t] = make_int4(a, b, c, a);
+  };
+#pragma unroll
+  for (int i = 0; i < kTriIters; ++i) {
+    const int t = tid + i * kTileThreads;
+    if (!tri_ok<FULL>(i, t, nt)) continue;
+    orient_tri(t);
   }
   flips = __reduce_add_sync(0xffffffffu, flips);
   bad = __reduce_or_sync(0xffffffffu, bad);
@@ -596,7 +608,7 @@ __device__ __forceinline__ void tile_body(
           mn = min(mn, y);
           ++n;
           y = nx_l[y];
-          if (y < 0 || n > 1024) { ok = false; tipped = y == -2; break; }  // deferred / barrier-tip loop
+          if (y < 0 || n > kP6MaxLen) { ok = false; tipped = y == -2; break; }  // deferred / barrier-tip / long loop
         } while (y != x);
       }
       if (ok) {
@@ -637,7 +649,7 @@ __global__ void __launch_bounds__(kTileThreads, 2)
            int64_t prefetch_dist) {
   extern __shared__ __align__(16) unsigned char smem_tile[];
   const int64_t ntiles = (T + kTileTris - 1) / kTileTris;
-  const int64_t tile = blockIdx.x;
+  const int64_t tile = sched_tile(blockIdx.x, ntiles);
   // the tile that starts about when this one ends (blocks are dispatched in index order,
   // kResident at a time): its data is prefetched into L2, which every SM shares
   const int64_t nxt = tile + prefetch_dist < ntiles ? tile + prefetch_dist : -1;
@@ -687,7 +699,8 @@ __global__ void k_left_insert(DevCounters* ctr, int64_t ntiles, const int32_t* _
                               int32_t* twin, uint32_t* ehash) {
   if (ctr->status) return;
   const uint32_t mask = (uint32_t)ctr->hash_cap - 1;
-  for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+  for (int64_t it = blockIdx.x; it < ntiles; it += gridDim.x) {
+    const int64_t tile = sched_tile(it, ntiles);
     const int32_t n = cnt_ld[2 * tile];
     const int32_t base = (int32_t)(3 * kTileTris * tile);
     for (int32_t k = threadIdx.x; k < n; k += blockDim.x) {
@@ -740,7 +753,8 @@ __global__ void __launch_bounds__(kSegThreads)
   __shared__ int32_t wtot[kSegThreads / 32];
   if (ctr->status) return;
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+  for (int64_t it = blockIdx.x; it < ntiles; it += gridDim.x) {
+    const int64_t tile = sched_tile(it, ntiles);
     const int32_t n = cnt_ld[2 * tile];
     const int32_t base = (int32_t)(3 * kTileTris * tile);
     int carry = 0;
@@ -813,7 +827,8 @@ __global__ void __launch_bounds__(kSegThreads)
                   const int32_t* __restrict__ bbase, int32_t* origin, int32_t* twin, int32_t* vmap) {
   if (ctr->status) return;
   const int32_t nb = ctr->n_border;
-  for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+  for (int64_t it = blockIdx.x; it < ntiles; it += gridDim.x) {
+    const int64_t tile = sched_tile(it, ntiles);
     const int32_t b0 = bbase[tile];
     const int32_t n = (tile + 1 < ntiles ? bbase[tile + 1] : nb) - b0;
     const int32_t base = (int32_t)(3 * kTileTris * tile);
@@ -846,32 +861,47 @@ __global__ void k_border_next(DevCounters* ctr, int64_t T3, const int32_t* __res
   }
 }
 
+// Per-device launch setup: the dynamic shared-memory attribute of k_tile belongs to each
+// device's context, so it is set once per device id (a relaxed bit-set under a mutex;
+// the SM count is cached next to it).
+static std::mutex g_dev_mu;
+static uint64_t g_dev_ready = 0;  // bit d: device d configured
+static int g_dev_sms[64];
+
+static int device_setup(int* n_sm) {
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return -1;
+  std::lock_guard<std::mutex> lk(g_dev_mu);
+  if (dev >= 64 || !((g_dev_ready >> dev) & 1)) {
+    if (cudaFuncSetAttribute(k_tile, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kTileSmem) != cudaSuccess)
+      return -1;
+    int sms = 0;
+    if (cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess) return -1;
+    if (dev >= 64) { *n_sm = sms; return 0; }  // (not cached)
+    g_dev_sms[dev] = sms;
+    g_dev_ready |= uint64_t(1) << dev;
+  }
+  *n_sm = g_dev_sms[dev];
+  return 0;
+}
+
 int launch_build(Ctx* c, cudaStream_t s) {
   int n = 0;
   const int64_t tiles = (c->T + kTileTris - 1) / kTileTris;
   cudaMemsetAsync(c->ctr, 0, sizeof(DevCounters), s);
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(k_tile, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kTileSmem);
-    attr = true;
-  }
-  prof_mark(s, "k_tile");
-  static int n_sm = 0;
-  if (!n_sm) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, dev);
-  }
+  int n_sm = 0;
+  if (device_setup(&n_sm) != 0) return -1;
   // L2 prefetch distance in tiles (default: one per SM, measured best of {0, 148, 296, 444, 592} on config 3);
   // POLYLLA_PREFETCH_DIST overrides it (<= 0 disables the prefetch) for experiments
-  static int64_t pf_dist = -1;
-  if (pf_dist < 0) {
+  static const int64_t pf_env = [] {
     const char* env = std::getenv("POLYLLA_PREFETCH_DIST");
-    pf_dist = env ? std::atoll(env) : (int64_t)n_sm;
-    if (pf_dist <= 0) pf_dist = int64_t(1) << 40;
-  }
+    // INT64_MIN: unset (one tile per SM); <= 0: no prefetch
+    return env ? (int64_t)std::atoll(env) : INT64_MIN;
+  }();
+  const int64_t pf_dist = pf_env == INT64_MIN ? (int64_t)n_sm : pf_env <= 0 ? int64_t(1) << 40 : pf_env;
   const int64_t bv_stride = c->F1 - c->F0;  // F0, F1, S, TB are equally spaced (capi.cu layout)
   if (c->S - c->F1 != bv_stride || c->TB - c->S != bv_stride) return -1;
+  prof_mark(s, "k_tile");
   k_tile<<<(unsigned)tiles, kTileThreads, kTileSmem, s>>>(reinterpret_cast<const double2*>(c->xy), c->tri, c->V, c->T,
                                                           c->origin, c->twin, c->next, c->lcode, c->F0, bv_stride, c->C,
                                                           c->len, c->wlen, c->left_key, c->left_e, c->def_e, c->SDB,

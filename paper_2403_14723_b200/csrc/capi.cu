@@ -222,6 +222,15 @@ POLYLLA_API polylla_status polylla_build_halfedges(const double* xy, int64_t V, 
   return POLYLLA_OK;
 }
 
+POLYLLA_API polylla_status polylla_check_manifold(polylla_ctx* p, polylla_stream stream) {
+  if (!p) return POLYLLA_E_INVALID_ARGUMENT;
+  if (p->c.stage < 1) return POLYLLA_E_CALL_ORDER;
+  const int n = launch_check_manifold(&p->c, S(stream));
+  if (n < 0) return POLYLLA_E_CUDA;
+  p->c.launches += n;
+  return POLYLLA_OK;
+}
+
 POLYLLA_API polylla_status polylla_label(polylla_ctx* p, polylla_stream stream) {
   if (!p) return POLYLLA_E_INVALID_ARGUMENT;
   if (p->c.stage != 1) return POLYLLA_E_CALL_ORDER;
@@ -276,19 +285,30 @@ POLYLLA_API polylla_status polylla_get_polygons(polylla_ctx* p, int32_t* offsets
   Ctx* c = &p->c;
   if (c->stage < 3) return POLYLLA_E_CALL_ORDER;
   if ((origin || twin || next) && c->stage < 4) return POLYLLA_E_CALL_ORDER;  // H needs get_counts
-  if (offsets && loops) {
-    const int n = launch_extract(c, offsets, offsets_cap, loops, loops_cap, prev, S(stream));
-    if (n < 0) return POLYLLA_E_CUDA;
-    c->launches += n;
-    c->extracted = true;
-  } else if (offsets || loops) {
-    return POLYLLA_E_INVALID_ARGUMENT;
-  } else if (prev) {
-    const int n = launch_extract(c, nullptr, -1, nullptr, -1, prev, S(stream));
-    if (n < 0) return POLYLLA_E_CUDA;
-    c->launches += n;
+  if ((offsets != nullptr) != (loops != nullptr)) return POLYLLA_E_INVALID_ARGUMENT;
+  // prev is built by a scatter kernel (prev[next[e]] = e): into the caller's array when it
+  // is device memory, else into dead workspace scratch (the leftover-key region, 24T bytes
+  // >= 4H) and copied out like origin/twin/next -- a kernel must never store to a host
+  // pointer
+  int32_t* prev_dev = nullptr;
+  if (prev) {
+    cudaPointerAttributes pa{};
+    const bool on_dev = cudaPointerGetAttributes(&pa, prev) == cudaSuccess &&
+                        (pa.type == cudaMemoryTypeDevice || pa.type == cudaMemoryTypeManaged);
+    cudaGetLastError();  // (clear a failed query of an unregistered host pointer)
+    prev_dev = on_dev ? prev : reinterpret_cast<int32_t*>(c->left_key);
+    if (!on_dev && c->stage < 4) return POLYLLA_E_CALL_ORDER;  // the copy-out needs H (get_counts)
   }
   const size_t hb = (size_t)c->host_counts.n_halfedges * 4;
+  if (offsets || prev_dev) {
+    const int n = launch_extract(c, offsets, offsets ? offsets_cap : -1, loops, loops ? loops_cap : -1, prev_dev,
+                                 S(stream));
+    if (n < 0) return POLYLLA_E_CUDA;
+    c->launches += n;
+    if (offsets) c->extracted = true;
+  }
+  if (prev && prev_dev != prev && cudaMemcpyAsync(prev, prev_dev, hb, cudaMemcpyDefault, S(stream)) != cudaSuccess)
+    return POLYLLA_E_CUDA;
   if (origin && cudaMemcpyAsync(origin, c->origin, hb, cudaMemcpyDefault, S(stream)) != cudaSuccess)
     return POLYLLA_E_CUDA;
   if (twin && cudaMemcpyAsync(twin, c->twin, hb, cudaMemcpyDefault, S(stream)) != cudaSuccess)

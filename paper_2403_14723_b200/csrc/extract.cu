@@ -21,7 +21,10 @@ constexpr int kEmitWords = 3 * kBuildTileTris / 32;  // 192
 #define POLYLLA_EMIT_THREADS 384  // measured 256/384/512 on configs 3 and 5
 #endif
 constexpr int kEmitThreads = POLYLLA_EMIT_THREADS;
-constexpr int kEmitQ = 2048;  // queue capacity (polygons per tile; a tile with more walks per word)
+#ifndef POLYLLA_EMIT_Q
+#define POLYLLA_EMIT_Q 2048  // (a test variant sets it tiny to force the dense-tile branch)
+#endif
+constexpr int kEmitQ = POLYLLA_EMIT_Q;  // queue capacity (polygons per tile; a tile with more walks per word)
 
 __global__ void __launch_bounds__(kEmitThreads)
     k_emit(int64_t T, int64_t n_words, const uint32_t* __restrict__ C, const int32_t* __restrict__ len,
@@ -38,7 +41,7 @@ __global__ void __launch_bounds__(kEmitThreads)
     if (blockIdx.x == 0 && threadIdx.x == 0) raise_status(ctr, ST_CAPACITY);
     return;
   }
-  const int64_t tile = blockIdx.x;
+  const int64_t tile = sched_tile(blockIdx.x, gridDim.x);
   const int64_t wt = tile * kEmitWords;  // first word of the tile
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   if (warp == 0) {  // per-word exclusive prefix of the canonical-seed count
@@ -127,7 +130,7 @@ __global__ void __launch_bounds__(kEmitThreads)
       for (int32_t k = 0; k < n; ++k, x = next[x]) loops[o + k] = origin[x];
     }
   }
-  if (tile == gridDim.x - 1 && tid == 0) offsets[P] = L;
+  if (tile == (int64_t)gridDim.x - 1 && tid == 0) offsets[P] = L;
 }
 
 __global__ void k_prev(int64_t T, const int32_t* __restrict__ next, const uint32_t* __restrict__ F1,

@@ -45,11 +45,12 @@ __global__ void __launch_bounds__(kRepairThreads)
     const int i = __shfl_sync(0xffffffffu, base, 0) + __popc(m32 & ((1u << lane) - 1));
     if (!valid) return;
     const int32_t e0 = twin[e];  // the tip's only outgoing frontier half-edge
-    int32_t x = e0, d = 0;
+    int32_t x = e0;
+    int64_t d = 0;
     bool ok = true;
-    do {  // degree(v): rotation closure about v (an interior vertex)
+    do {  // degree(v): rotation closure about v (an interior vertex); deg(v) <= 3T
       const int32_t tx = twin[x];
-      if (tx >= T3 || ++d > kWalkBound) { ok = false; break; }
+      if (tx >= T3 || ++d > T3) { ok = false; break; }
       x = next_in(tx);
     } while (x != e0);
     tips[i] = e;
@@ -59,7 +60,7 @@ __global__ void __launch_bounds__(kRepairThreads)
       return;
     }
     int32_t m = e0;
-    for (int k = 0; k < (d - 1) / 2; ++k) m = next_in(twin[m]);  // CWvertexEdge steps (R1, R5)
+    for (int64_t k = 0; k < (d - 1) / 2; ++k) m = next_in(twin[m]);  // CWvertexEdge steps (R1, R5)
     const int32_t tm = twin[m];
     atomicOr(&F1[m >> 5], 1u << (m & 31));
     atomicOr(&F1[tm >> 5], 1u << (tm & 31));
@@ -74,24 +75,29 @@ __global__ void k_repair_rewire(int64_t T, const int32_t* __restrict__ twin, con
                                 const int32_t* __restrict__ aff, int32_t* next, DevCounters* ctr) {
   if (ctr->status) return;
   const int64_t T3 = 3 * T;
+  const int64_t H = T3 + ctr->n_border;  // walk bound (a rotation about w has <= deg(w) <= H steps)
   const int32_t n = 2 * ctr->n_tips;
   for (int32_t j = blockIdx.x * blockDim.x + threadIdx.x; j < n; j += gridDim.x * blockDim.x) {
     const int32_t o = aff[j];
     int32_t y = o;
-    int guard = 0;
+    int64_t guard = 0;
     do {
       if (y < T3) {
         const int32_t p = prev_in(y);  // incoming to w in y's triangle; next_in(p) = y
         if (f1_of(F1, T3, p)) {
           int32_t x = y;
-          int steps = 0;
-          while (!f1_of(F1, T3, x) && ++steps < kWalkBound) x = next_in(twin[x]);
+          int64_t steps = 0;
+          while (!f1_of(F1, T3, x) && ++steps <= H) x = next_in(twin[x]);
+          if (steps > H) {  // the rotation to the next F1 half-edge did not close
+            raise_status(ctr, ST_WALK);
+            return;
+          }
           next[p] = x;
         }
       }
       const int32_t ty = twin[y];
       y = ty >= T3 ? next[ty] : next_in(ty);  // full rotation about w (border chain at the hull)
-      if (++guard > kWalkBound) { raise_status(ctr, ST_WALK); break; }
+      if (++guard > H) { raise_status(ctr, ST_WALK); break; }
     } while (y != o);
   }
 }
@@ -105,10 +111,10 @@ __device__ __forceinline__ void process_seed(int32_t s, int64_t T3, int64_t H, c
                                              const int32_t* __restrict__ next, const uint32_t* __restrict__ F1,
                                              uint32_t* C, int32_t* len, int32_t* wlen, DevCounters* ctr) {
   int32_t x = s;
-  int steps = 0;
-  while (!f1_of(F1, T3, x)) {  // Alg. 12: rotate (sweep_out) to a frontier half-edge
+  int64_t steps = 0;
+  while (!f1_of(F1, T3, x)) {  // Alg. 12: rotate (sweep_out) to a frontier half-edge (<= deg <= 3T steps)
     x = next_in(twin[x]);
-    if (++steps > kWalkBound || x == s) { raise_status(ctr, ST_WALK); return; }
+    if (++steps > T3 || x == s) { raise_status(ctr, ST_WALK); return; }
   }
   int32_t mn = x, y = x;
   int64_t n = 0;

@@ -107,6 +107,7 @@ int launch_generate(Ctx* c, cudaStream_t s);
 int launch_extract(Ctx* c, int32_t* offsets, int64_t offsets_cap, int32_t* loops, int64_t loops_cap,
                    int32_t* prev, cudaStream_t s);
 int launch_regions(Ctx* c, int32_t* poly_of_tri, cudaStream_t s);
+int launch_check_manifold(Ctx* c, cudaStream_t s);
 
 // ------------------------------------------------------------------ device helpers
 __device__ __forceinline__ int32_t next_in(int32_t e) {  // 3f + (k+1)%3
@@ -133,8 +134,18 @@ __device__ __forceinline__ uint32_t mix32(uint32_t a, uint32_t b) {
 
 constexpr uint32_t kEmpty = 0xFFFFFFFFu;   // empty hash slot
 constexpr uint32_t kPaired = 0x80000000u;  // flag in hash slots (slot values < 2^31 - 1)
-constexpr int kWalkBound = 1 << 16;      // rotation bound (vertex degree)
 constexpr int kBuildTileTris = 2048;     // triangles per k_tile tile (list segments are 3 * 2048 wide)
+
+// Block -> tile schedule of the per-tile kernels.  POLYLLA_REVERSE_TILES (a test variant,
+// tests/variants.py) runs the tiles in reverse order: results must not depend on it.
+__device__ __forceinline__ int64_t sched_tile(int64_t i, int64_t ntiles) {
+#ifdef POLYLLA_REVERSE_TILES
+  return ntiles - 1 - i;
+#else
+  (void)ntiles;
+  return i;
+#endif
+}
 
 // Set bits of a bit-vector, spread over warps: warp g of the grid scans kBitChunk-word
 // chunks g, g + G, ... and expands the set bits into its shared queue q (kBitQueue

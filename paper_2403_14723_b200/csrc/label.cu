@@ -37,7 +37,8 @@ __global__ void __launch_bounds__(kLabelThreads)
   if (ctr->status) return;
   const int64_t T3 = 3 * T;
   const int lane = threadIdx.x & 31;
-  for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+  for (int64_t it = blockIdx.x; it < ntiles; it += gridDim.x) {
+    const int64_t tile = sched_tile(it, ntiles);
     const int32_t n = cnt_ld[2 * tile + 1];
     const int32_t seg = (int32_t)(3 * kBuildTileTris * tile);
     for (int32_t base = 0; base < n; base += kLabelThreads) {  // warp-uniform trip count
@@ -55,12 +56,12 @@ __global__ void __launch_bounds__(kLabelThreads)
         int32_t nx = next_in(e);
         if (fr) {
           int32_t x = nx;
-          for (int steps = 0;; ++steps) {
+          for (int64_t steps = 0;; ++steps) {  // bound: a rotation has <= deg(v) <= 3T steps
             const int32_t tx = twin[x];
             if (tx >= T3) break;                                         // border edge: frontier
             if (!is_longest(lcode, x) && !is_longest(lcode, tx)) break;  // frontier edge
             x = next_in(tx);                                             // cross the edge (sweep_out)
-            if (steps > kWalkBound) { walk_err = true; break; }
+            if (steps > T3) { walk_err = true; break; }
           }
           nx = x;
           tip = (x == t);

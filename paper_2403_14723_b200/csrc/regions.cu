@@ -68,8 +68,9 @@ constexpr int kUfTile = kBuildTileTris, kUfThreads = POLYLLA_UF_THREADS;
 static_assert(3 * kUfTile % kUfThreads == 0, "half-edges per thread");
 __global__ void __launch_bounds__(kUfThreads) k_uf_local(int64_t T, const int32_t* __restrict__ twin,
                                                   const uint32_t* __restrict__ F1, int32_t* __restrict__ parent,
-                                                  int32_t* __restrict__ slot) {
+                                                  int32_t* __restrict__ slot, const DevCounters* ctr) {
   __shared__ int32_t p[kUfTile];
+  if (ctr->status) return;
   const int64_t t0 = (int64_t)blockIdx.x * kUfTile;
   const int nt = T - t0 < kUfTile ? (int)(T - t0) : kUfTile;
   for (int i = threadIdx.x; i < nt; i += blockDim.x) p[i] = i;
@@ -141,8 +142,12 @@ __global__ void k_uf_seed(const int32_t* __restrict__ seeds, int32_t* parent, in
 
 __global__ void k_uf_out(int64_t T, int32_t* parent, const int32_t* __restrict__ slot, int32_t* __restrict__ out,
                          const DevCounters* ctr) {
-  if (ctr->status) return;
+  const bool bad = ctr->status != 0;  // (e.g. a capacity error: no seeds were written) -> all -1
   for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < T; t += (int64_t)gridDim.x * blockDim.x) {
+    if (bad) {
+      out[t] = -1;
+      continue;
+    }
     const int32_t v = slot[uf_find(parent, (int32_t)t)];
     out[t] = v == INT32_MAX ? -1 : v;  // -1: a piece without a loop (not reachable on valid output)
   }
@@ -154,7 +159,8 @@ int launch_regions(Ctx* c, int32_t* poly_of_tri, cudaStream_t s) {
   int32_t* slot = parent + c->T;
   const unsigned g = 148 * 8;
   prof_mark(s, "k_regions");
-  k_uf_local<<<(unsigned)((c->T + kUfTile - 1) / kUfTile), kUfThreads, 0, s>>>(c->T, c->twin, c->F1, parent, slot);
+  k_uf_local<<<(unsigned)((c->T + kUfTile - 1) / kUfTile), kUfThreads, 0, s>>>(c->T, c->twin, c->F1, parent, slot,
+                                                                                 c->ctr);
   const int64_t tiles = (c->T + kUfTile - 1) / kUfTile;
   k_uf_hook<<<(unsigned)tiles, 256, 0, s>>>(tiles, c->cnt_ld, c->left_e, c->twin, c->F1, parent, c->ctr);
   k_uf_seed<<<g, 256, 0, s>>>(c->seeds, parent, slot, c->ctr);

@@ -29,6 +29,7 @@ EXPORTS = (
     "polylla_get_counts", "polylla_get_polygons", "polylla_get_views", "polylla_set_debug",
     "polylla_run_host", "polylla_destroy", "polylla_status_string", "polylla_launch_count",
     "polylla_profile_enable", "polylla_profile_read", "polylla_get_triangle_polygons",
+    "polylla_check_manifold",
 )
 
 
@@ -54,6 +55,17 @@ class Views(ctypes.Structure):
 
 
 _LIB = None
+_LIBS = {}
+
+
+def set_library(path: str | None):
+    """Use another build of the library (a flag variant, tests/variants.py) for the calls
+    that follow; None restores the default.  Returns the previous path."""
+    global _LIB, LIB_PATH
+    prev = LIB_PATH
+    LIB_PATH = path or os.path.join(_HERE, "libpolylla.so")
+    _LIB = _LIBS.get(LIB_PATH)
+    return prev
 
 
 def lib():
@@ -67,7 +79,7 @@ def lib():
         L.polylla_workspace_bytes.argtypes = [i64, i64]
         L.polylla_build_halfedges.restype = ctypes.c_int
         L.polylla_build_halfedges.argtypes = [vp, i64, vp, i64, vp, ctypes.c_size_t, vp, ctypes.POINTER(vp)]
-        for n in ("polylla_label", "polylla_generate"):
+        for n in ("polylla_label", "polylla_generate", "polylla_check_manifold"):
             getattr(L, n).restype = ctypes.c_int
             getattr(L, n).argtypes = [vp, vp]
         L.polylla_get_counts.restype = ctypes.c_int
@@ -94,7 +106,7 @@ def lib():
         L.polylla_profile_read.restype = ctypes.c_int
         L.polylla_profile_read.argtypes = [ctypes.POINTER(ctypes.c_char_p), ctypes.POINTER(ctypes.c_double),
                                            ctypes.POINTER(ctypes.c_int64), ctypes.c_int]
-        _LIB = L
+        _LIB = _LIBS[LIB_PATH] = L
     return _LIB
 
 
@@ -146,6 +158,12 @@ def build_halfedges(xy: torch.Tensor, tri: torch.Tensor, workspace: torch.Tensor
                                        workspace.numel(), _stream(stream), ctypes.byref(h))
     _check(rc, "polylla_build_halfedges")
     return Context(h, xy, tri, workspace)
+
+
+def check_manifold(ctx: Context, stream=None) -> None:
+    """Opt-in exact non-manifold-edge check (polylla_check_manifold); the verdict arrives
+    with the next get_counts."""
+    _check(lib().polylla_check_manifold(ctx.handle, _stream(stream)), "polylla_check_manifold")
 
 
 def label(ctx: Context, stream=None) -> None:
@@ -228,13 +246,15 @@ def status_string(code: int) -> str:
 # ----------------------------------------------------------------------- conveniences
 
 def run(xy: torch.Tensor, tri: torch.Tensor, stream=None, arrays=True, prev=False, debug=False,
-        regions=False) -> dict:
+        regions=False, check=False) -> dict:
     """build -> label -> generate -> get_counts -> get_polygons on device tensors.
     Returns a dict of torch tensors (offsets, loops, seeds, [origin, twin, next, prev],
     [lcode, frontier0, frontier1, seed_bits, next_pre]) plus the counts."""
     V, T = xy.shape[0], tri.shape[0]
     ws = alloc_workspace(V, T, xy.device)
     ctx = build_halfedges(xy, tri, ws, stream)
+    if check:
+        check_manifold(ctx, stream)
     next_pre = None
     if debug:
         next_pre = torch.empty(6 * T, dtype=torch.int32, device=xy.device)

@@ -1,0 +1,83 @@
+"""BASELINE config 4 (the capacity probe: jittered 16000 x 16000 grid, V = 256M,
+T = 511,936,002, H = 1,535,872,002 < 2^31) bit-exact against the CPU oracle.
+
+The oracle needs ~100 GB of host memory (its [H] arrays trimmed to the known H =
+3T + 4(s-1) through oracle.run(hcap=...)) and ~15-25 minutes on one core, so this test
+runs only when POLYLLA_HUGE=1 (tools/gpurun/r2_config4.sh; its log is committed under
+profiles/).  The device-side invariant check of the same mesh runs in the default GPU
+suite (tests/test_gpu_parity.py::test_config4_capacity_invariants)."""
+import os
+import time
+
+import numpy as np
+import pytest
+import torch
+
+import oracle
+import synth
+
+pytestmark = [pytest.mark.gpu, pytest.mark.slow,
+              pytest.mark.skipif(os.environ.get("POLYLLA_HUGE") != "1", reason="set POLYLLA_HUGE=1 (needs ~100 GB RAM)")]
+
+
+def _host_info():
+    mem = [l for l in open("/proc/meminfo") if l.startswith(("MemTotal", "MemAvailable"))]
+    cpu = next((l.split(":", 1)[1].strip() for l in open("/proc/cpuinfo") if l.startswith("model name")), "?")
+    return f"host: {cpu}, {os.cpu_count()} logical CPUs; " + "; ".join(l.strip() for l in mem)
+
+
+def _eq_chunked(dev_arr, host_arr, name, chunk=1 << 27):
+    n = host_arr.shape[0]
+    assert dev_arr.numel() >= n, name
+    for a in range(0, n, chunk):
+        b = min(n, a + chunk)
+        h = torch.from_numpy(np.ascontiguousarray(host_arr[a:b])).cuda()
+        if not torch.equal(dev_arr[a:b], h):
+            bad = int(torch.nonzero(dev_arr[a:b] != h)[0, 0]) + a
+            raise AssertionError(f"{name}[{bad}]: gpu {int(dev_arr[bad])} oracle {int(host_arr[bad])}")
+        del h
+
+
+def test_config4_bit_exact_vs_oracle():
+    from paper_2403_14723_b200 import polylla as pp
+    print(_host_info(), flush=True)
+    s = 16000
+    t0 = time.time()
+    xy, tri = synth.grid(s, 0.2, 4)
+    T = tri.shape[0]
+    assert T == 511_936_002
+    H = 3 * T + 4 * (s - 1)
+    print(f"generated in {time.time() - t0:.0f} s", flush=True)
+    # GPU first (its inputs from the host arrays: the same mesh the oracle reads)
+    xd, td = torch.from_numpy(xy).cuda(), torch.from_numpy(tri).cuda()
+    ws = pp.alloc_workspace(xy.shape[0], T)
+    t0 = time.time()
+    ctx = pp.build_halfedges(xd, td, ws)
+    pp.label(ctx)
+    pp.generate(ctx)
+    c = pp.get_counts(ctx)
+    assert c["n_halfedges"] == H
+    P, L = c["n_polygons"], c["n_loop_entries"]
+    offsets = torch.empty(P + 1, dtype=torch.int32, device="cuda")
+    loops = torch.empty(L, dtype=torch.int32, device="cuda")
+    pp.get_polygons(ctx, offsets, loops)
+    assert pp.get_counts(ctx)["status"] == 0
+    torch.cuda.synchronize()
+    print(f"gpu: {time.time() - t0:.1f} s (incl. first launches) P={P} L={L} tips={c['n_tips']}", flush=True)
+    del xd, td
+    # the oracle
+    t0 = time.time()
+    ref = oracle.run(xy, tri, hcap=H)
+    print(f"oracle: {time.time() - t0:.0f} s, phases {ref['times']}", flush=True)
+    assert (ref["H"], ref["P"], ref["L"], ref["n_tips"]) == (H, P, L, c["n_tips"])
+    v = pp.get_views(ctx)
+    view = lambda k, n: pp.view_tensor(ctx, v[k], n, torch.int32)  # noqa: E731
+    for k in ("origin", "twin", "next"):
+        _eq_chunked(view(k, H), ref[k], k)
+    _eq_chunked(view("seeds", P), ref["seeds"], "seeds")
+    _eq_chunked(offsets, ref["offsets"], "offsets")
+    _eq_chunked(loops, ref["loops"], "loops")
+    lc = pp.view_tensor(ctx, v["lcode"], T, torch.uint8)
+    _eq_chunked(lc, ref["lcode"], "lcode")
+    print(f"config 4 bit-exact: origin/twin/next [{H}], lcode [{T}], seeds [{P}], offsets, loops [{L}]", flush=True)
+    pp.destroy(ctx)

@@ -260,20 +260,57 @@ def test_concurrent_meshes_on_two_streams():
             assert torch.equal(loops[:L], ref[i]["loops"]), i
 
 
-def test_run_host_e2e_matches_device():
+def test_run_host_e2e_matches_oracle():
+    """polylla_run_host (host buffers in, host buffers out) against the oracle."""
     pp = _pp()
-    xy, tri = synth.random_delaunay(30000, 12)
-    a = gpu_run(xy, tri)
-    b = pp.run_host(xy, tri)
-    for k in ("origin", "twin", "next", "offsets", "loops"):
-        np.testing.assert_array_equal(a[k].cpu().numpy(), b[k].numpy(), err_msg=k)
+    for xy, tri in (synth.random_delaunay(30000, 12), synth.grid(120, 0.2, 4)):
+        ref = oracle.run(xy, tri)
+        b = pp.run_host(xy, tri)
+        assert b["H"] == ref["H"] and b["P"] == ref["P"]
+        for k in ("origin", "twin", "next", "offsets", "loops"):
+            np.testing.assert_array_equal(b[k].numpy(), ref[k], err_msg=k)
 
 
-def _gpu_status(xy, tri):
+def _gpu_status(xy, tri, check=False):
     pp = _pp()
     with pytest.raises(pp.PolyllaError) as ei:
-        gpu_run(np.asarray(xy, np.float64), np.asarray(tri, np.int32))
+        gpu_run(np.asarray(xy, np.float64), np.asarray(tri, np.int32), check=check)
     return pp.STATUS[ei.value.code]
+
+
+def _cross_tile_nonmanifold(two_pairs):
+    """A jittered grid (T = 3,042 > one 2,048-triangle build tile) plus, at the end (tile 1),
+    a triangle on an interior edge {a, b} of tile 0 -- the edge's third copy -- or
+    (two_pairs) two triangles pairing on {a, b} inside tile 1 (copies three and four)."""
+    xy, tri = synth.grid(40, 0.2, 5)
+    a, b = int(tri[700, 0]), int(tri[700, 1])
+    c = np.array([[1000.0, 1000.0], [-1000.0, -1000.0]])
+    V = xy.shape[0]
+    extra = [[a, b, V], [b, a, V + 1]] if two_pairs else [[a, b, V]]
+    return np.vstack([xy, c]), np.vstack([tri, np.array(extra, np.int32)]).astype(np.int32)
+
+
+@pytest.mark.parametrize("two_pairs", [False, True])
+def test_cross_tile_nonmanifold_edge(two_pairs):
+    """R20: copies of an edge paired inside one tile plus copies in another tile.  The
+    oracle reports NON_MANIFOLD_EDGE; so does the GPU with polylla_check_manifold."""
+    xy, tri = _cross_tile_nonmanifold(two_pairs)
+    with pytest.raises(oracle.OracleError) as ei:
+        oracle.run(xy, tri)
+    assert oracle.STATUS[ei.value.code] == "NON_MANIFOLD_EDGE"
+    assert _gpu_status(xy, tri, check=True) == "NON_MANIFOLD_EDGE"
+
+
+def test_check_manifold_passes_valid_meshes():
+    """The exact check raises nothing on valid meshes (shuffled input: every twin crosses
+    tiles) and leaves the results bit-exact."""
+    rng = np.random.default_rng(2)
+    xy, tri = synth.random_delaunay(30000, 13)
+    for t in (tri, np.ascontiguousarray(tri[rng.permutation(tri.shape[0])])):
+        ref = oracle.run(xy, t)
+        res = gpu_run(xy, t, check=True)
+        np.testing.assert_array_equal(res["loops"].cpu().numpy(), ref["loops"])
+        np.testing.assert_array_equal(res["next"].cpu().numpy(), ref["next"])
 
 
 def test_error_kinds_match_oracle():
@@ -290,6 +327,7 @@ def test_error_kinds_match_oracle():
         with pytest.raises(oracle.OracleError) as ei:
             oracle.run(np.asarray(xy, np.float64), np.asarray(tri, np.int32))
         assert _gpu_status(xy, tri) == oracle.STATUS[ei.value.code]
+        assert _gpu_status(xy, tri, check=True) == oracle.STATUS[ei.value.code]
 
 
 def test_call_order_and_workspace_errors():
@@ -459,9 +497,10 @@ def test_cuda_graph_replay_matches_eager():
         assert torch.equal(offsets[:P + 1], ref["offsets"]) and torch.equal(loops[:L], ref["loops"])
 
 
-def test_host_pipeline_matches_device():
+def test_host_pipeline_matches_oracle():
+    """HostPipeline (pinned host in/out, copies overlapped across meshes) against the oracle."""
     pp = _pp()
-    meshes = [synth.random_delaunay(20_000, 50 + i) for i in range(3)]
+    meshes = [synth.random_delaunay(20_000, 50 + i) for i in range(3)] + [synth.grid(90, 0.2, 9)]
     V = max(m[0].shape[0] for m in meshes)
     T = max(m[1].shape[0] for m in meshes)
     pipe = pp.HostPipeline(V, T)
@@ -469,9 +508,10 @@ def test_host_pipeline_matches_device():
     outs = [pp.alloc_host_outputs(T) for _ in meshes]
     counts = pipe.run(inputs, outs)
     for (x, t), o, c in zip(meshes, outs, counts):
-        ref = gpu_run(x, t)
+        ref = oracle.run(x, t)
         P, L, H = c["n_polygons"], c["n_loop_entries"], c["n_halfedges"]
-        assert torch.equal(o["offsets"][:P + 1], ref["offsets"].cpu())
-        assert torch.equal(o["loops"][:L], ref["loops"].cpu())
+        assert (P, L, H) == (ref["P"], ref["L"], ref["H"])
+        np.testing.assert_array_equal(o["offsets"][:P + 1].numpy(), ref["offsets"])
+        np.testing.assert_array_equal(o["loops"][:L].numpy(), ref["loops"])
         for k in ("origin", "twin", "next"):
-            assert torch.equal(o[k][:H], ref[k].cpu()), k
+            np.testing.assert_array_equal(o[k][:H].numpy(), ref[k], err_msg=k)

@@ -62,6 +62,13 @@ for lib in libs:
         e1.synchronize()
         times.append(e0.elapsed_time(e1))
     med = {k: statistics.median(v) for k, v in per.items()}
+    ctx = pp.build_halfedges(xy_d, tri_d, ws, s)
+    pp.label(ctx, s)
+    pp.generate(ctx, s)
+    cn = pp.get_counts(ctx, s)
+    pp.destroy(ctx)
+    print("  counts: " + " ".join(f"{k}={cn[k]}" for k in ("n_leftover", "n_deferred", "n_seed_deferred", "n_tips",
+                                                            "n_exact") if k in cn), flush=True)
     print(f"{os.path.basename(lib or pp.LIB_PATH)} cfg{cfg}: step(graph) median {statistics.median(times):.3f} ms  "
           f"min {min(times):.3f}  | " + " ".join(f"{k}={v:.3f}" for k, v in med.items()), flush=True)
     del g
