@@ -172,6 +172,20 @@ POLYLLA_API polylla_status polylla_get_polygons(polylla_ctx* ctx, int32_t* offse
  * entry is -1.  Uses dead workspace scratch; asynchronous (4 launches). */
 POLYLLA_API polylla_status polylla_get_triangle_polygons(polylla_ctx* ctx, int32_t* poly_of_tri, polylla_stream stream);
 
+/* Per-triangle terminal-edge-region ids (the pre-repair Lepp
+ * partition): the terminal-edge regions of PAPER.md Defs. 1-2 (L121-128) -- the triangles
+ * whose longest-edge propagating paths end at the same terminal edge -- which the
+ * data-parallel Lepp refinement of PAPER.md L76 works on, and which the repair (L517-570)
+ * later splits into the output polygons.  On the device a region is the piece of
+ * triangles connected across interior non-frontier edges of the label-phase frontier F0:
+ *   region_of_tri[t] = the smallest triangle index of t's region.
+ * region_of_tri: device int32 [T], caller-owned.  Call after polylla_label (stage >= 2);
+ * valid only if a later polylla_get_counts returns POLYLLA_OK (else every entry is -1).
+ * Uses dead workspace scratch (shared with get_triangle_polygons, check_manifold and a
+ * host-pointer prev: not concurrently); asynchronous (3 launches). */
+POLYLLA_API polylla_status polylla_get_triangle_regions(polylla_ctx* ctx, int32_t* region_of_tri,
+                                                        polylla_stream stream);
+
 /* Device views into the workspace (valid until polylla_destroy / workspace reuse).
  * Any pointer argument may be NULL.  Sizes: origin/twin/next [H]; lcode [T] (k* of
  * each triangle); frontier0 / frontier1 / seed_bits: bit-vectors of uint32 words

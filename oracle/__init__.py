@@ -176,3 +176,24 @@ def triangle_polygons(ref: dict):
             if x == s:
                 break
     return best[comp].astype(np.int32)
+
+
+def triangle_regions(ref: dict):
+    """Per-triangle terminal-edge-region label (pre-repair), from a
+    ``run`` result, by the definition: the terminal-edge regions of PAPER.md Defs. 1-2
+    (L121-128) are the connected components of the triangles joined across interior
+    non-frontier edges of the label-phase frontier F0 (pinned against a brute-force
+    enumeration of Defs. 1-2 in tests/test_oracle_pins.py); label = the smallest triangle
+    id of the component (library routine: scipy's connected_components)."""
+    import scipy.sparse as sp
+    from scipy.sparse.csgraph import connected_components
+
+    T = ref["T"]
+    e = np.arange(3 * T)
+    tw = ref["twin"][:3 * T].astype(np.int64)
+    m = (ref["frontier0"][:3 * T] == 0) & (tw < 3 * T) & (e < tw)
+    g = sp.coo_matrix((np.ones(int(m.sum())), (e[m] // 3, tw[m] // 3)), shape=(T, T))
+    _, comp = connected_components(g, directed=False)
+    first = np.full(comp.max() + 1, T, np.int64)
+    np.minimum.at(first, comp, np.arange(T))
+    return first[comp].astype(np.int32)

@@ -322,7 +322,17 @@ POLYLLA_API polylla_status polylla_get_triangle_polygons(polylla_ctx* p, int32_t
   if (!p || !poly_of_tri) return POLYLLA_E_INVALID_ARGUMENT;
   Ctx* c = &p->c;
   if (!c->extracted) return POLYLLA_E_CALL_ORDER;
-  const int n = launch_regions(c, poly_of_tri, S(stream));
+  const int n = launch_regions(c, poly_of_tri, 0, S(stream));
+  if (n < 0) return POLYLLA_E_CUDA;
+  c->launches += n;
+  return POLYLLA_OK;
+}
+
+POLYLLA_API polylla_status polylla_get_triangle_regions(polylla_ctx* p, int32_t* region_of_tri, polylla_stream stream) {
+  if (!p || !region_of_tri) return POLYLLA_E_INVALID_ARGUMENT;
+  Ctx* c = &p->c;
+  if (c->stage < 2) return POLYLLA_E_CALL_ORDER;  // F0 is complete after polylla_label
+  const int n = launch_regions(c, region_of_tri, 1, S(stream));
   if (n < 0) return POLYLLA_E_CUDA;
   c->launches += n;
   return POLYLLA_OK;

@@ -43,7 +43,9 @@ struct DevCounters {
   uint32_t hash_cap; // capacity (pow2 <= 2^31) of the leftover hash for this run
   int32_t n_def;     // half-edges deferred by k_tile to the label fixup
   int32_t n_sdef;    // seeds walked by k_seed_walk (deferred + repair halves)
-  int32_t pad[5];
+  uint32_t pad0;
+  unsigned long long hash_scale;  // leftover-hash home slot = (lo * hash_scale) >> 32 (cap / V in 32.32 fixed point)
+  int32_t pad[2];
 };
 
 struct Ctx {
@@ -106,7 +108,7 @@ int launch_label(Ctx* c, cudaStream_t s);
 int launch_generate(Ctx* c, cudaStream_t s);
 int launch_extract(Ctx* c, int32_t* offsets, int64_t offsets_cap, int32_t* loops, int64_t loops_cap,
                    int32_t* prev, cudaStream_t s);
-int launch_regions(Ctx* c, int32_t* poly_of_tri, cudaStream_t s);
+int launch_regions(Ctx* c, int32_t* out, int mode, cudaStream_t s);  // mode 0: polygon ids, 1: F0 regions
 int launch_check_manifold(Ctx* c, cudaStream_t s);
 
 // ------------------------------------------------------------------ device helpers

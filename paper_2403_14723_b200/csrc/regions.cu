@@ -1,9 +1,14 @@
-// regions.cu -- per-triangle polygon ids: the output polygons
+// regions.cu -- per-triangle polygon ids and terminal-edge-region ids (SURVEY.md §8(f)
+// NEXT-4).  (1) Post-repair: the output polygons
 // of PAPER.md L113 / L579 as unions of triangles, i.e. the terminal-edge regions of
 // PAPER.md L76-L128 after the barrier repair.  A polygon's triangles are the piece of
 // triangles connected across its non-frontier (F1 = 0) edges; its loop bounds the piece.
 //   poly_of_tri[t] = min { p : the loop of polygon p bounds the piece of t }
 // (a piece has several loops only around a hole of the mesh).
+// (2) Pre-repair: the terminal-edge regions of PAPER.md Defs. 1-2 (L121-128), the Lepp
+// partition that the data-parallel Lepp of PAPER.md L76 refines: the pieces of triangles
+// connected across non-frontier edges of F0 (the frontier before the repair), labelled by
+// their smallest triangle id.
 // GPU: lock-free union-find over the non-frontier interior edges (hook the larger root
 // under the smaller with CAS, path halving in find; per tile in shared memory first), then every polygon's canonical seed
 // (an interior half-edge of its loop, whose triangle lies in the piece) takes the min over
@@ -153,20 +158,35 @@ __global__ void k_uf_out(int64_t T, int32_t* parent, const int32_t* __restrict__
   }
 }
 
-int launch_regions(Ctx* c, int32_t* poly_of_tri, cudaStream_t s) {
-  // scratch: the leftover-key region (24 B per interior triangle slot, dead after generate)
+// pre-repair terminal-edge regions: every triangle reads its root, which is the smallest
+// triangle id of its set (roots only ever hook under smaller roots)
+__global__ void k_uf_roots(int64_t T, int32_t* parent, int32_t* __restrict__ out, const DevCounters* ctr) {
+  const bool bad = ctr->status != 0;
+  for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < T; t += (int64_t)gridDim.x * blockDim.x)
+    out[t] = bad ? -1 : uf_find(parent, (int32_t)t);
+}
+
+// out[t]: post-repair polygon index (F1 pieces, mode 0) or pre-repair terminal-edge region
+// label = smallest triangle id of the region (F0 pieces, mode 1)
+int launch_regions(Ctx* c, int32_t* out, int mode, cudaStream_t s) {
+  // scratch: the leftover-key region (24 B per interior triangle slot, dead after the build)
   int32_t* parent = reinterpret_cast<int32_t*>(c->left_key);
   int32_t* slot = parent + c->T;
+  const uint32_t* F = mode == 1 ? c->F0 : c->F1;
   const unsigned g = 148 * 8;
-  prof_mark(s, "k_regions");
-  k_uf_local<<<(unsigned)((c->T + kUfTile - 1) / kUfTile), kUfThreads, 0, s>>>(c->T, c->twin, c->F1, parent, slot,
+  prof_mark(s, mode == 1 ? "k_regions_pre" : "k_regions");
+  k_uf_local<<<(unsigned)((c->T + kUfTile - 1) / kUfTile), kUfThreads, 0, s>>>(c->T, c->twin, F, parent, slot,
                                                                                  c->ctr);
   const int64_t tiles = (c->T + kUfTile - 1) / kUfTile;
-  k_uf_hook<<<(unsigned)tiles, 256, 0, s>>>(tiles, c->cnt_ld, c->left_e, c->twin, c->F1, parent, c->ctr);
-  k_uf_seed<<<g, 256, 0, s>>>(c->seeds, parent, slot, c->ctr);
-  k_uf_out<<<g, 256, 0, s>>>(c->T, parent, slot, poly_of_tri, c->ctr);
+  k_uf_hook<<<(unsigned)tiles, 256, 0, s>>>(tiles, c->cnt_ld, c->left_e, c->twin, F, parent, c->ctr);
+  if (mode == 1) {
+    k_uf_roots<<<g, 256, 0, s>>>(c->T, parent, out, c->ctr);
+  } else {
+    k_uf_seed<<<g, 256, 0, s>>>(c->seeds, parent, slot, c->ctr);
+    k_uf_out<<<g, 256, 0, s>>>(c->T, parent, slot, out, c->ctr);
+  }
   prof_end(s);
-  return cudaGetLastError() == cudaSuccess ? 4 : -1;
+  return cudaGetLastError() == cudaSuccess ? (mode == 1 ? 3 : 4) : -1;
 }
 
 }  // namespace polylla

@@ -29,7 +29,7 @@ EXPORTS = (
     "polylla_get_counts", "polylla_get_polygons", "polylla_get_views", "polylla_set_debug",
     "polylla_run_host", "polylla_destroy", "polylla_status_string", "polylla_launch_count",
     "polylla_profile_enable", "polylla_profile_read", "polylla_get_triangle_polygons",
-    "polylla_check_manifold",
+    "polylla_check_manifold", "polylla_get_triangle_regions",
 )
 
 
@@ -88,6 +88,8 @@ def lib():
         L.polylla_get_polygons.argtypes = [vp, i32p, i64, i32p, i64, i32p, i32p, i32p, i32p, vp]
         L.polylla_get_triangle_polygons.restype = ctypes.c_int
         L.polylla_get_triangle_polygons.argtypes = [vp, i32p, vp]
+        L.polylla_get_triangle_regions.restype = ctypes.c_int
+        L.polylla_get_triangle_regions.argtypes = [vp, i32p, vp]
         L.polylla_get_views.restype = ctypes.c_int
         L.polylla_get_views.argtypes = [vp, ctypes.POINTER(Views)]
         L.polylla_set_debug.restype = ctypes.c_int
@@ -196,6 +198,13 @@ def get_triangle_polygons(ctx: Context, poly_of_tri: torch.Tensor, stream=None) 
            "polylla_get_triangle_polygons")
 
 
+def get_triangle_regions(ctx: Context, region_of_tri: torch.Tensor, stream=None) -> None:
+    """region_of_tri (device int32 [T]) = smallest triangle id of each triangle's
+    terminal-edge region (the pre-repair Lepp partition); after label."""
+    _check(lib().polylla_get_triangle_regions(ctx.handle, _ptr(region_of_tri), _stream(stream)),
+           "polylla_get_triangle_regions")
+
+
 def set_debug(ctx: Context, next_pre: torch.Tensor | None) -> None:
     _check(lib().polylla_set_debug(ctx.handle, _ptr(next_pre)), "polylla_set_debug")
 
@@ -278,6 +287,8 @@ def run(xy: torch.Tensor, tri: torch.Tensor, stream=None, arrays=True, prev=Fals
     if regions:
         out["poly_of_tri"] = torch.empty(T, dtype=torch.int32, device=dev)
         get_triangle_polygons(ctx, out["poly_of_tri"], stream)
+        out["region_of_tri"] = torch.empty(T, dtype=torch.int32, device=dev)
+        get_triangle_regions(ctx, out["region_of_tri"], stream)
     c2 = get_counts(ctx, stream)  # synchronises; surfaces a capacity error
     out["loops"] = out["loops"][:L]
     v = get_views(ctx)

@@ -218,6 +218,16 @@ def test_triangle_polygons(name):
     np.testing.assert_array_equal(res["poly_of_tri"].cpu().numpy(), oracle.triangle_polygons(ref))
 
 
+@pytest.mark.parametrize("name", ["square", "fan", "tie", "grid", "jittered", "random", "holes", "wheels", "shuffled"])
+def test_triangle_regions(name):
+    """polylla_get_triangle_regions (NEXT-4, pre-repair Lepp partition) against the
+    oracle's definition, element by element."""
+    xy, tri = _regions_case(name)
+    ref = oracle.run(xy, tri)
+    res = gpu_run(xy, tri, regions=True)
+    np.testing.assert_array_equal(res["region_of_tri"].cpu().numpy(), oracle.triangle_regions(ref))
+
+
 def test_determinism_and_streams():
     xy, tri = synth.random_delaunay(20000, 8)
     a = gpu_run(xy, tri)

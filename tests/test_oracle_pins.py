@@ -177,6 +177,31 @@ def test_prerepair_partition_equals_lepp_regions(name, xy, tri):
     assert info["repeated_vertex_loops"] >= 0
 
 
+@pytest.mark.parametrize("name,xy,tri", _corpus()[::3], ids=lambda v: v if isinstance(v, str) else "")
+def test_triangle_regions_label_the_lepp_partition(name, xy, tri):
+    """oracle.triangle_regions (NEXT-4, pre-repair): its label classes are exactly the
+    brute-force terminal-edge regions of Defs. 1-2 and each label is the smallest
+    triangle id of its region."""
+    regions, _ = lepp_regions(xy, tri)
+    lab = oracle.triangle_regions(oracle.run(xy, tri))
+    assert len(set(lab.tolist())) == len(regions)
+    for g in regions:
+        ids = sorted(g)
+        assert set(lab[ids].tolist()) == {ids[0]}
+
+
+def test_triangle_regions_closed_forms():
+    """Alg. 13 grids: every cell (triangles 2c, 2c+1, sharing their hypotenuse) is one
+    terminal-edge region -> label t - t % 2; the square is one region; the barrier fan is
+    one region before the repair (its two polygons come from the repair)."""
+    for s in (2, 3, 9):
+        lab = oracle.triangle_regions(oracle.run(*synth.grid(s)))
+        t = np.arange(2 * (s - 1) ** 2)
+        assert np.array_equal(lab, t - t % 2)
+    assert oracle.triangle_regions(oracle.run(*synth.fixture_square())).tolist() == [0, 0]
+    assert oracle.triangle_regions(oracle.run(*synth.fixture_fan())).tolist() == [0] * 5
+
+
 def test_repair_splits_are_region_subsets():
     """Repair (Alg. 6) only splits regions: each final polygon's flood piece (F1)
     lies inside one Lepp region, and every region is the union of its pieces."""

@@ -14,12 +14,15 @@ import synth  # noqa: E402
 cfg = int(sys.argv[1]) if len(sys.argv) > 1 else 3
 reps = int(sys.argv[2]) if len(sys.argv) > 2 else 40
 libs = sys.argv[3:] or [None]
-if cfg == 5:
+if cfg == 4:
+    xy_d, tri_d = synth.grid_device(16000, 0.2, 4)
+elif cfg == 5:
     xy, tri = synth.grid(2000, 0.2, 1000)
 else:
     xy, tri = synth.random_delaunay({2: 1_000_000, 3: 10_000_000}[cfg], cfg)
-xy_d, tri_d = torch.from_numpy(xy).cuda(), torch.from_numpy(tri).cuda()
-T = tri.shape[0]
+if cfg != 4:
+    xy_d, tri_d = torch.from_numpy(xy).cuda(), torch.from_numpy(tri).cuda()
+V, T = xy_d.shape[0], tri_d.shape[0]
 import importlib  # noqa: E402
 
 for lib in libs:
@@ -27,7 +30,7 @@ for lib in libs:
         os.environ["POLYLLA_LIB"] = lib
     import paper_2403_14723_b200.polylla as pp
     pp = importlib.reload(pp)
-    ws = pp.alloc_workspace(xy.shape[0], T)
+    ws = pp.alloc_workspace(V, T)
     offs = torch.empty(T + 1, dtype=torch.int32, device="cuda")
     loops = torch.empty(3 * T, dtype=torch.int32, device="cuda")
     s = torch.cuda.Stream()
@@ -71,4 +74,5 @@ for lib in libs:
                                                             "n_exact") if k in cn), flush=True)
     print(f"{os.path.basename(lib or pp.LIB_PATH)} cfg{cfg}: step(graph) median {statistics.median(times):.3f} ms  "
           f"min {min(times):.3f}  | " + " ".join(f"{k}={v:.3f}" for k, v in med.items()), flush=True)
-    del g
+    del g, ws, offs, loops
+    torch.cuda.empty_cache()
