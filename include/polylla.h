@@ -139,6 +139,17 @@ POLYLLA_API polylla_status polylla_label(polylla_ctx* ctx, polylla_stream stream
  * loop lengths into CSR offsets.  Asynchronous. */
 POLYLLA_API polylla_status polylla_generate(polylla_ctx* ctx, polylla_stream stream);
 
+/* Ablation: label + generate by the paper's own GPU kernel
+ * sequence instead of polylla_label + polylla_generate -- LLK (Alg. 7, per triangle),
+ * LFK (Alg. 8) and LSK (Alg. 9, per half-edge), LEK (Alg. 10: every VERTEX counts its
+ * frontier edges; barrier tips get their middle edge before the rewire), CaK (Alg. 11:
+ * next and prev of every frontier half-edge by rotation), SFK (Alg. 12) and Overwrite
+ * seeds (per seed), then Scan and compact, one thread per element.
+ * Same results as the default path, bit for bit.  Call after polylla_build_halfedges
+ * (stage 1); afterwards get_counts / get_polygons as usual (get_triangle_polygons and
+ * get_triangle_regions too).  Asynchronous (~14 launches and memsets). */
+POLYLLA_API polylla_status polylla_label_generate_paper(polylla_ctx* ctx, polylla_stream stream);
+
 /* Synchronises `stream` and returns the counts and the device status.  The return
  * value is counts->status (POLYLLA_OK when the conversion succeeded). */
 POLYLLA_API polylla_status polylla_get_counts(polylla_ctx* ctx, polylla_stream stream, polylla_counts* counts);

@@ -646,10 +646,12 @@ __global__ void __launch_bounds__(kTileThreads, 2)
            uint8_t* __restrict__ lcode, uint32_t* __restrict__ F0, int64_t bv_stride, uint32_t* __restrict__ C, int32_t* __restrict__ len, int32_t* __restrict__ wlen,
            unsigned long long* __restrict__ left_key, int32_t* __restrict__ left_e, int32_t* __restrict__ def_e,
            uint32_t* __restrict__ SDB, int32_t* __restrict__ cnt_ld, DevCounters* ctr,
-           int64_t prefetch_dist) {
+           int64_t prefetch_dist, int64_t tile_base) {
   extern __shared__ __align__(16) unsigned char smem_tile[];
   const int64_t ntiles = (T + kTileTris - 1) / kTileTris;
-  const int64_t tile = sched_tile(blockIdx.x, ntiles);
+  // tiles [tile_base, tile_base + gridDim.x): all of them, or one chunk of an upload
+  // pipeline (polylla_run_host)
+  const int64_t tile = tile_base + sched_tile(blockIdx.x, gridDim.x);
   // the tile that starts about when this one ends (blocks are dispatched in index order,
   // kResident at a time): its data is prefetched into L2, which every SM shares
   const int64_t nxt = tile + prefetch_dist < ntiles ? tile + prefetch_dist : -1;
@@ -904,12 +906,7 @@ static int device_setup(int* n_sm) {
   return 0;
 }
 
-int launch_build(Ctx* c, cudaStream_t s) {
-  int n = 0;
-  const int64_t tiles = (c->T + kTileTris - 1) / kTileTris;
-  cudaMemsetAsync(c->ctr, 0, sizeof(DevCounters), s);
-  int n_sm = 0;
-  if (device_setup(&n_sm) != 0) return -1;
+static int64_t prefetch_distance(int n_sm) {
   // L2 prefetch distance in tiles (default: one per SM, measured best of {0, 148, 296, 444, 592} on config 3);
   // POLYLLA_PREFETCH_DIST overrides it (<= 0 disables the prefetch) for experiments
   static const int64_t pf_env = [] {
@@ -917,15 +914,45 @@ int launch_build(Ctx* c, cudaStream_t s) {
     // INT64_MIN: unset (one tile per SM); <= 0: no prefetch
     return env ? (int64_t)std::atoll(env) : INT64_MIN;
   }();
-  const int64_t pf_dist = pf_env == INT64_MIN ? (int64_t)n_sm : pf_env <= 0 ? int64_t(1) << 40 : pf_env;
+  return pf_env == INT64_MIN ? (int64_t)n_sm : pf_env <= 0 ? int64_t(1) << 40 : pf_env;
+}
+
+// the start of a build: counters zeroed, per-device setup
+int launch_build_begin(Ctx* c, cudaStream_t s) {
+  if (cudaMemsetAsync(c->ctr, 0, sizeof(DevCounters), s) != cudaSuccess) return -1;
+  int n_sm = 0;
+  return device_setup(&n_sm);
+}
+
+// k_tile over tiles [t0, t1)
+int launch_build_tiles(Ctx* c, cudaStream_t s, int64_t t0, int64_t t1) {
+  if (t1 <= t0) return 0;
+  int n_sm = 0;
+  if (device_setup(&n_sm) != 0) return -1;
+  const int64_t pf_dist = prefetch_distance(n_sm);
   const int64_t bv_stride = c->F1 - c->F0;  // F0, F1, S, TB are equally spaced (capi.cu layout)
   if (c->S - c->F1 != bv_stride || c->TB - c->S != bv_stride) return -1;
   prof_mark(s, "k_tile");
-  k_tile<<<(unsigned)tiles, kTileThreads, kTileSmem, s>>>(reinterpret_cast<const double2*>(c->xy), c->tri, c->V, c->T,
+  k_tile<<<(unsigned)(t1 - t0), kTileThreads, kTileSmem, s>>>(reinterpret_cast<const double2*>(c->xy), c->tri, c->V, c->T,
                                                           c->origin, c->twin, c->next, c->lcode, c->F0, bv_stride, c->C,
                                                           c->len, c->wlen, c->left_key, c->left_e, c->def_e, c->SDB,
-                                                          c->cnt_ld, c->ctr, pf_dist);
-  ++n;
+                                                          c->cnt_ld, c->ctr, pf_dist, t0);
+  return cudaGetLastError() == cudaSuccess ? 1 : -1;
+}
+
+int launch_build(Ctx* c, cudaStream_t s) {
+  const int64_t tiles = (c->T + kTileTris - 1) / kTileTris;
+  if (launch_build_begin(c, s) != 0) return -1;
+  const int n = launch_build_tiles(c, s, 0, tiles);
+  if (n < 0) return -1;
+  const int m = launch_build_rest(c, s);
+  return m < 0 ? -1 : n + m;
+}
+
+// everything after the tiles: leftover match, border half-edges and their chain
+int launch_build_rest(Ctx* c, cudaStream_t s) {
+  int n = 0;
+  const int64_t tiles = (c->T + kTileTris - 1) / kTileTris;
   const int grid = 148 * 32;  // enough threads for ~1 leftover each on 10M-vertex meshes (latency-bound)
   prof_mark(s, "k_left_match");
   k_hash_clear<<<grid, 256, 0, s>>>(c->ctr, c->ehash, c->hash_cap_max, c->V, c->T);

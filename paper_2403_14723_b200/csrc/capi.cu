@@ -191,11 +191,10 @@ POLYLLA_API size_t polylla_workspace_bytes(int64_t n_vertices, int64_t n_triangl
   return workspace_bytes(n_vertices, n_triangles);
 }
 
-POLYLLA_API polylla_status polylla_build_halfedges(const double* xy, int64_t V, const int32_t* tri, int64_t T,
-                                                   void* workspace, size_t workspace_bytes_, polylla_stream stream,
-                                                   polylla_ctx** ctx_out) {
-  if (!ctx_out) return POLYLLA_E_INVALID_ARGUMENT;
-  *ctx_out = nullptr;
+// a new ctx over caller memory (no launches): argument checks + workspace carving
+static polylla_status new_ctx(const double* xy, int64_t V, const int32_t* tri, int64_t T, void* workspace,
+                              size_t workspace_bytes_, polylla_ctx** out) {
+  *out = nullptr;
   if (!xy || !tri || !workspace || V < 3 || T < 1) return POLYLLA_E_INVALID_ARGUMENT;
   if ((reinterpret_cast<uintptr_t>(xy) & 15) || (reinterpret_cast<uintptr_t>(tri) & 3))
     return POLYLLA_E_INVALID_ARGUMENT;
@@ -211,6 +210,18 @@ POLYLLA_API polylla_status polylla_build_halfedges(const double* xy, int64_t V, 
     std::free(p);
     return POLYLLA_E_WORKSPACE;
   }
+  *out = p;
+  return POLYLLA_OK;
+}
+
+POLYLLA_API polylla_status polylla_build_halfedges(const double* xy, int64_t V, const int32_t* tri, int64_t T,
+                                                   void* workspace, size_t workspace_bytes_, polylla_stream stream,
+                                                   polylla_ctx** ctx_out) {
+  if (!ctx_out) return POLYLLA_E_INVALID_ARGUMENT;
+  polylla_ctx* p = nullptr;
+  const polylla_status st = new_ctx(xy, V, tri, T, workspace, workspace_bytes_, &p);
+  if (st != POLYLLA_OK) return st;
+  Ctx* c = &p->c;
   const int n = launch_build(c, S(stream));
   if (n < 0) {
     std::free(p);
@@ -245,6 +256,16 @@ POLYLLA_API polylla_status polylla_generate(polylla_ctx* p, polylla_stream strea
   if (!p) return POLYLLA_E_INVALID_ARGUMENT;
   if (p->c.stage != 2) return POLYLLA_E_CALL_ORDER;
   const int n = launch_generate(&p->c, S(stream));
+  if (n < 0) return POLYLLA_E_CUDA;
+  p->c.launches += n;
+  p->c.stage = 3;
+  return POLYLLA_OK;
+}
+
+POLYLLA_API polylla_status polylla_label_generate_paper(polylla_ctx* p, polylla_stream stream) {
+  if (!p) return POLYLLA_E_INVALID_ARGUMENT;
+  if (p->c.stage != 1) return POLYLLA_E_CALL_ORDER;
+  const int n = launch_paper(&p->c, S(stream));
   if (n < 0) return POLYLLA_E_CUDA;
   p->c.launches += n;
   p->c.stage = 3;
@@ -360,6 +381,38 @@ POLYLLA_API polylla_status polylla_set_debug(polylla_ctx* p, int32_t* next_pre) 
   return POLYLLA_OK;
 }
 
+// End to end from host buffers, pipelined inside one mesh:
+//   up stream   : H2D xy, then tri in kRunChunks chunks of whole build tiles
+//   `stream`    : k_tile over each chunk as soon as it has landed, then the rest of the
+//                 build, label, generate (one host sync for the counts), extraction
+//   down stream : D2H of each chunk's origin rows right behind its k_tile (full duplex:
+//                 overlaps the upload of the next chunks), of twin once the build is done
+//                 (overlaps label/generate), then the border rows, next and the CSR.
+constexpr int kRunChunks = 8;
+
+namespace {
+struct RunRes {  // streams and events of one run_host call, released on every exit path
+  cudaStream_t up = nullptr, down = nullptr;
+  cudaEvent_t ev[2 * kRunChunks + 4] = {};
+  int nev = 0;
+  bool ok = true;
+  cudaEvent_t make() {
+    cudaEvent_t e = nullptr;
+    if (cudaEventCreateWithFlags(&e, cudaEventDisableTiming) != cudaSuccess) ok = false;
+    ev[nev++] = e;
+    return e;
+  }
+  ~RunRes() {
+    if (up) cudaStreamSynchronize(up);
+    if (down) cudaStreamSynchronize(down);
+    for (int i = 0; i < nev; ++i)
+      if (ev[i]) cudaEventDestroy(ev[i]);
+    if (up) cudaStreamDestroy(up);
+    if (down) cudaStreamDestroy(down);
+  }
+};
+}  // namespace
+
 POLYLLA_API polylla_status polylla_run_host(const double* xy_host, int64_t V, const int32_t* tri_host, int64_t T,
                                             void* workspace, size_t workspace_bytes_, int32_t* offsets_host,
                                             int64_t offsets_cap, int32_t* loops_host, int64_t loops_cap,
@@ -372,42 +425,101 @@ POLYLLA_API polylla_status polylla_run_host(const double* xy_host, int64_t V, co
   probe.V = V;
   probe.T = T;
   if (!carve(&probe, workspace, workspace_bytes_)) return POLYLLA_E_WORKSPACE;
-  cudaStream_t s = S(stream);
-  if (cudaMemcpyAsync(probe.xy_stage, xy_host, (size_t)V * 16, cudaMemcpyHostToDevice, s) != cudaSuccess ||
-      cudaMemcpyAsync(probe.tri_stage, tri_host, (size_t)T * 12, cudaMemcpyHostToDevice, s) != cudaSuccess)
-    return POLYLLA_E_CUDA;
   polylla_ctx* p = nullptr;
-  polylla_status st = polylla_build_halfedges(probe.xy_stage, V, probe.tri_stage, T, workspace, workspace_bytes_,
-                                              stream, &p);
+  polylla_status st = new_ctx(probe.xy_stage, V, probe.tri_stage, T, workspace, workspace_bytes_, &p);
   if (st != POLYLLA_OK) return st;
-  if ((st = polylla_label(p, stream)) != POLYLLA_OK || (st = polylla_generate(p, stream)) != POLYLLA_OK) {
-    polylla_destroy(p);
-    return st;
-  }
-  st = polylla_get_counts(p, stream, counts);
-  if (st != POLYLLA_OK) {
-    polylla_destroy(p);
-    return st;
-  }
   Ctx* c = &p->c;
-  const int64_t P = counts->n_polygons, L = counts->n_loop_entries, H = counts->n_halfedges;
-  if (offsets_cap < P + 1 || loops_cap < L || ((origin_host || twin_host || next_host) && halfedge_cap < H)) {
-    polylla_destroy(p);
-    return POLYLLA_E_CAPACITY;
-  }
-  // extraction into the workspace staging (offsets and loops), then exact-size D2H copies
+  cudaStream_t s = S(stream);
   polylla_status out = POLYLLA_OK;
-  if (launch_extract(c, nullptr, T + 1, c->loops, 3 * T, nullptr, s) < 0) out = POLYLLA_E_CUDA;
-  if (cudaMemcpyAsync(offsets_host, c->offsets, (size_t)(P + 1) * 4, cudaMemcpyDeviceToHost, s) != cudaSuccess ||
-      cudaMemcpyAsync(loops_host, c->loops, (size_t)L * 4, cudaMemcpyDeviceToHost, s) != cudaSuccess)
-    out = POLYLLA_E_CUDA;
-  if (origin_host && cudaMemcpyAsync(origin_host, c->origin, (size_t)H * 4, cudaMemcpyDeviceToHost, s) != cudaSuccess)
-    out = POLYLLA_E_CUDA;
-  if (twin_host && cudaMemcpyAsync(twin_host, c->twin, (size_t)H * 4, cudaMemcpyDeviceToHost, s) != cudaSuccess)
-    out = POLYLLA_E_CUDA;
-  if (next_host && cudaMemcpyAsync(next_host, c->next, (size_t)H * 4, cudaMemcpyDeviceToHost, s) != cudaSuccess)
-    out = POLYLLA_E_CUDA;
-  if (cudaStreamSynchronize(s) != cudaSuccess) out = POLYLLA_E_CUDA;
+  {
+    RunRes r;
+    if (cudaStreamCreateWithFlags(&r.up, cudaStreamNonBlocking) != cudaSuccess ||
+        cudaStreamCreateWithFlags(&r.down, cudaStreamNonBlocking) != cudaSuccess) {
+      polylla_destroy(p);
+      return POLYLLA_E_CUDA;
+    }
+    const int64_t tiles = (T + kBuildTileTris - 1) / kBuildTileTris;
+    const int nch = (int)(tiles < kRunChunks ? tiles : kRunChunks);
+    cudaEvent_t ev_start = r.make(), ev_rest = r.make(), ev_ext = r.make();
+    cudaEvent_t ev_up[kRunChunks], ev_tile[kRunChunks];
+    for (int i = 0; i < nch; ++i) {
+      ev_up[i] = r.make();
+      ev_tile[i] = r.make();
+    }
+    if (!r.ok) {
+      polylla_destroy(p);
+      return POLYLLA_E_CUDA;
+    }
+    bool cuda_ok = true;
+    auto chk = [&](cudaError_t e) { cuda_ok = cuda_ok && e == cudaSuccess; };
+    chk(cudaEventRecord(ev_start, s));  // the side streams start after the caller's prior work
+    chk(cudaStreamWaitEvent(r.up, ev_start, 0));
+    chk(cudaStreamWaitEvent(r.down, ev_start, 0));
+    chk(cudaMemcpyAsync(probe.xy_stage, xy_host, (size_t)V * 16, cudaMemcpyHostToDevice, r.up));
+    if (launch_build_begin(c, s) != 0) cuda_ok = false;
+    int64_t launches = 0;
+    for (int i = 0; i < nch && cuda_ok; ++i) {
+      const int64_t t0 = tiles * i / nch, t1 = tiles * (i + 1) / nch;
+      const int64_t f0 = t0 * kBuildTileTris, f1 = t1 * kBuildTileTris < T ? t1 * kBuildTileTris : T;
+      chk(cudaMemcpyAsync(probe.tri_stage + 3 * f0, tri_host + 3 * f0, (size_t)(f1 - f0) * 12, cudaMemcpyHostToDevice,
+                          r.up));
+      chk(cudaEventRecord(ev_up[i], r.up));
+      chk(cudaStreamWaitEvent(s, ev_up[i], 0));
+      const int n = launch_build_tiles(c, s, t0, t1);
+      if (n < 0) cuda_ok = false;
+      launches += n;
+      chk(cudaEventRecord(ev_tile[i], s));
+      if (origin_host) {  // interior origin rows of the chunk are final after its k_tile
+        chk(cudaStreamWaitEvent(r.down, ev_tile[i], 0));
+        chk(cudaMemcpyAsync(origin_host + 3 * f0, c->origin + 3 * f0, (size_t)(f1 - f0) * 12, cudaMemcpyDeviceToHost,
+                            r.down));
+      }
+    }
+    if (cuda_ok) {
+      const int n = launch_build_rest(c, s);
+      if (n < 0) cuda_ok = false;
+      launches += n;
+      chk(cudaEventRecord(ev_rest, s));
+      if (twin_host) {  // interior twins are final after the leftover match and the border ranking
+        chk(cudaStreamWaitEvent(r.down, ev_rest, 0));
+        chk(cudaMemcpyAsync(twin_host, c->twin, (size_t)(3 * T) * 4, cudaMemcpyDeviceToHost, r.down));
+      }
+    }
+    if (!cuda_ok) {
+      polylla_destroy(p);
+      return POLYLLA_E_CUDA;
+    }
+    c->launches += launches;
+    c->stage = 1;
+    if ((st = polylla_label(p, stream)) != POLYLLA_OK || (st = polylla_generate(p, stream)) != POLYLLA_OK) {
+      polylla_destroy(p);
+      return st;
+    }
+    st = polylla_get_counts(p, stream, counts);  // the one host sync (the side streams keep copying)
+    if (st != POLYLLA_OK) {
+      polylla_destroy(p);
+      return st;
+    }
+    const int64_t P = counts->n_polygons, L = counts->n_loop_entries, H = counts->n_halfedges;
+    if (offsets_cap < P + 1 || loops_cap < L || ((origin_host || twin_host || next_host) && halfedge_cap < H)) {
+      polylla_destroy(p);
+      return POLYLLA_E_CAPACITY;
+    }
+    // extraction into the workspace staging, then exact-size copies
+    if (launch_extract(c, nullptr, T + 1, c->loops, 3 * T, nullptr, s) < 0) out = POLYLLA_E_CUDA;
+    chk(cudaEventRecord(ev_ext, s));
+    chk(cudaStreamWaitEvent(r.down, ev_ext, 0));  // (after generate too: next is final)
+    const size_t hb = (size_t)(H - 3 * T) * 4;     // border rows
+    if (origin_host && hb) chk(cudaMemcpyAsync(origin_host + 3 * T, c->origin + 3 * T, hb, cudaMemcpyDeviceToHost, r.down));
+    if (twin_host && hb) chk(cudaMemcpyAsync(twin_host + 3 * T, c->twin + 3 * T, hb, cudaMemcpyDeviceToHost, r.down));
+    if (next_host) chk(cudaMemcpyAsync(next_host, c->next, (size_t)H * 4, cudaMemcpyDeviceToHost, r.down));
+    chk(cudaMemcpyAsync(offsets_host, c->offsets, (size_t)(P + 1) * 4, cudaMemcpyDeviceToHost, r.down));
+    chk(cudaMemcpyAsync(loops_host, c->loops, (size_t)L * 4, cudaMemcpyDeviceToHost, r.down));
+    chk(cudaStreamSynchronize(r.down));
+    chk(cudaStreamSynchronize(r.up));
+    if (!cuda_ok) out = POLYLLA_E_CUDA;
+    // (RunRes releases the streams and events)
+  }
   polylla_destroy(p);
   return out;
 }

@@ -241,6 +241,8 @@ __global__ void __launch_bounds__(kTopThreads)
   }
 }
 
+int launch_canon_scan(Ctx* c, cudaStream_t s);
+
 int launch_generate(Ctx* c, cudaStream_t s) {
   int n = 0;
   if (c->next_pre) cudaMemcpyAsync(c->next_pre, c->next, (size_t)c->Hmax * 4, cudaMemcpyDeviceToDevice, s);
@@ -252,13 +254,19 @@ int launch_generate(Ctx* c, cudaStream_t s) {
   k_seed_walk<<<148 * (2048 / kSeedThreads), kSeedThreads, 0, s>>>(c->T, c->n_words, c->SDB, c->twin, c->next, c->F1, c->C, c->len,
                                                c->wlen, c->ctr);
   n += 3;
+  const int m = launch_canon_scan(c, s);
+  if (m < 0) return -1;
+  n += m;
+  return cudaGetLastError() == cudaSuccess ? n : -1;
+}
+
+int launch_canon_scan(Ctx* c, cudaStream_t s) {
   prof_mark(s, "k_canon_scan");
   const int64_t tiles = (c->T + kBuildTileTris - 1) / kBuildTileTris;
   k_canon_tiles<<<(unsigned)((tiles + 7) / 8), 256, 0, s>>>(c->n_words, tiles, c->C, c->wlen, c->F1, c->tsum, c->ctr);
   k_tiles_scan<<<1, kTopThreads, 0, s>>>(tiles, c->tsum, c->tbase, c->offsets, c->ctr);
-  n += 2;
   prof_end(s);
-  return cudaGetLastError() == cudaSuccess ? n : -1;
+  return cudaGetLastError() == cudaSuccess ? 2 : -1;
 }
 
 }  // namespace polylla

@@ -103,13 +103,17 @@ size_t workspace_bytes(int64_t V, int64_t T);
 bool carve(Ctx* c, void* ws, size_t bytes);
 
 // launchers (each returns the number of kernel launches issued, < 0 on CUDA error)
-int launch_build(Ctx* c, cudaStream_t s);
+int launch_build(Ctx* c, cudaStream_t s);  // = begin + tiles [0, ntiles) + rest
+int launch_build_begin(Ctx* c, cudaStream_t s);
+int launch_build_tiles(Ctx* c, cudaStream_t s, int64_t t0, int64_t t1);
+int launch_build_rest(Ctx* c, cudaStream_t s);
 int launch_label(Ctx* c, cudaStream_t s);
 int launch_generate(Ctx* c, cudaStream_t s);
 int launch_extract(Ctx* c, int32_t* offsets, int64_t offsets_cap, int32_t* loops, int64_t loops_cap,
                    int32_t* prev, cudaStream_t s);
 int launch_regions(Ctx* c, int32_t* out, int mode, cudaStream_t s);  // mode 0: polygon ids, 1: F0 regions
 int launch_check_manifold(Ctx* c, cudaStream_t s);
+int launch_paper(Ctx* c, cudaStream_t s);  // the paper's LLK..OSK + Scan sequence (NEXT-2 ablation)
 
 // ------------------------------------------------------------------ device helpers
 __device__ __forceinline__ int32_t next_in(int32_t e) {  // 3f + (k+1)%3

@@ -29,7 +29,7 @@ EXPORTS = (
     "polylla_get_counts", "polylla_get_polygons", "polylla_get_views", "polylla_set_debug",
     "polylla_run_host", "polylla_destroy", "polylla_status_string", "polylla_launch_count",
     "polylla_profile_enable", "polylla_profile_read", "polylla_get_triangle_polygons",
-    "polylla_check_manifold", "polylla_get_triangle_regions",
+    "polylla_check_manifold", "polylla_get_triangle_regions", "polylla_label_generate_paper",
 )
 
 
@@ -79,7 +79,7 @@ def lib():
         L.polylla_workspace_bytes.argtypes = [i64, i64]
         L.polylla_build_halfedges.restype = ctypes.c_int
         L.polylla_build_halfedges.argtypes = [vp, i64, vp, i64, vp, ctypes.c_size_t, vp, ctypes.POINTER(vp)]
-        for n in ("polylla_label", "polylla_generate", "polylla_check_manifold"):
+        for n in ("polylla_label", "polylla_generate", "polylla_check_manifold", "polylla_label_generate_paper"):
             getattr(L, n).restype = ctypes.c_int
             getattr(L, n).argtypes = [vp, vp]
         L.polylla_get_counts.restype = ctypes.c_int
@@ -166,6 +166,11 @@ def check_manifold(ctx: Context, stream=None) -> None:
     """Opt-in exact non-manifold-edge check (polylla_check_manifold); the verdict arrives
     with the next get_counts."""
     _check(lib().polylla_check_manifold(ctx.handle, _stream(stream)), "polylla_check_manifold")
+
+
+def label_generate_paper(ctx: Context, stream=None) -> None:
+    """The paper's kernel sequence (LLK..OSK + Scan) instead of label + generate (ablation)."""
+    _check(lib().polylla_label_generate_paper(ctx.handle, _stream(stream)), "polylla_label_generate_paper")
 
 
 def label(ctx: Context, stream=None) -> None:
@@ -255,7 +260,7 @@ def status_string(code: int) -> str:
 # ----------------------------------------------------------------------- conveniences
 
 def run(xy: torch.Tensor, tri: torch.Tensor, stream=None, arrays=True, prev=False, debug=False,
-        regions=False, check=False) -> dict:
+        regions=False, check=False, paper=False) -> dict:
     """build -> label -> generate -> get_counts -> get_polygons on device tensors.
     Returns a dict of torch tensors (offsets, loops, seeds, [origin, twin, next, prev],
     [lcode, frontier0, frontier1, seed_bits, next_pre]) plus the counts."""
@@ -268,8 +273,11 @@ def run(xy: torch.Tensor, tri: torch.Tensor, stream=None, arrays=True, prev=Fals
     if debug:
         next_pre = torch.empty(6 * T, dtype=torch.int32, device=xy.device)
         set_debug(ctx, next_pre)
-    label(ctx, stream)
-    generate(ctx, stream)
+    if paper:
+        label_generate_paper(ctx, stream)
+    else:
+        label(ctx, stream)
+        generate(ctx, stream)
     counts = get_counts(ctx, stream)
     P, L, H = counts["n_polygons"], counts["n_loop_entries"], counts["n_halfedges"]
     dev = xy.device
@@ -350,14 +358,20 @@ class GraphStep:
     The C ABI is called unchanged during capture; its kernels read the mesh size from the
     workspace counters on the device, so a replay recomputes everything."""
 
-    def __init__(self, xy, tri, workspace, offsets, loops, stream=None):
+    def __init__(self, xy, tri, workspace, offsets, loops, stream=None, paper=False):
         self.stream = stream or torch.cuda.Stream(device=xy.device)
+
+        def lg(ctx, st):
+            if paper:
+                label_generate_paper(ctx, st)
+            else:
+                label(ctx, st)
+                generate(ctx, st)
         self.args = (xy, tri, workspace, offsets, loops)
         # warm once outside capture (lazy CUDA attribute setup inside the library)
         with torch.cuda.stream(self.stream):
             ctx = build_halfedges(xy, tri, workspace, self.stream)
-            label(ctx, self.stream)
-            generate(ctx, self.stream)
+            lg(ctx, self.stream)
             get_polygons(ctx, offsets, loops, stream=self.stream)
             self.launches = launch_count(ctx)
             destroy(ctx)
@@ -366,8 +380,7 @@ class GraphStep:
         with torch.cuda.graph(self.graph, stream=self.stream):
             s = torch.cuda.current_stream()
             ctx = build_halfedges(xy, tri, workspace, s)
-            label(ctx, s)
-            generate(ctx, s)
+            lg(ctx, s)
             get_polygons(ctx, offsets, loops, stream=s)
             destroy(ctx)
 

@@ -35,10 +35,15 @@ for lib in libs:
     loops = torch.empty(3 * T, dtype=torch.int32, device="cuda")
     s = torch.cuda.Stream()
 
+    paper = os.environ.get("POLYLLA_PAPER") == "1"  # the paper's kernel sequence (NEXT-2 ablation)
+
     def step():
         ctx = pp.build_halfedges(xy_d, tri_d, ws, s)
-        pp.label(ctx, s)
-        pp.generate(ctx, s)
+        if paper:
+            pp.label_generate_paper(ctx, s)
+        else:
+            pp.label(ctx, s)
+            pp.generate(ctx, s)
         pp.get_polygons(ctx, offs, loops, stream=s)
         pp.destroy(ctx)
 
@@ -52,7 +57,7 @@ for lib in libs:
         for k, (ms, _) in pp.profile_read().items():
             per.setdefault(k, []).append(ms)
     pp.profile_enable(False)
-    g = pp.GraphStep(xy_d, tri_d, ws, offs, loops, s)
+    g = pp.GraphStep(xy_d, tri_d, ws, offs, loops, s, paper=paper)
     for _ in range(5):
         g.replay()
     torch.cuda.synchronize()
@@ -66,8 +71,11 @@ for lib in libs:
         times.append(e0.elapsed_time(e1))
     med = {k: statistics.median(v) for k, v in per.items()}
     ctx = pp.build_halfedges(xy_d, tri_d, ws, s)
-    pp.label(ctx, s)
-    pp.generate(ctx, s)
+    if paper:
+        pp.label_generate_paper(ctx, s)
+    else:
+        pp.label(ctx, s)
+        pp.generate(ctx, s)
     cn = pp.get_counts(ctx, s)
     pp.destroy(ctx)
     print("  counts: " + " ".join(f"{k}={cn[k]}" for k in ("n_leftover", "n_deferred", "n_seed_deferred", "n_tips",
