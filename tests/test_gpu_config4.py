@@ -26,8 +26,7 @@ def _mem_available_gb():
     return 0.0
 
 
-pytestmark = [pytest.mark.gpu, pytest.mark.slow,
-              pytest.mark.skipif(_mem_available_gb() < 150, reason="needs ~100 GB of host RAM (150 GB available)")]
+pytestmark = [pytest.mark.gpu, pytest.mark.slow]
 
 
 def _host_info():
@@ -48,6 +47,7 @@ def _eq_chunked(dev_arr, host_arr, name, chunk=1 << 27):
         del h
 
 
+@pytest.mark.skipif(_mem_available_gb() < 150, reason="needs ~100 GB of host RAM (150 GB available)")
 def test_config4_bit_exact_vs_oracle():
     from paper_2403_14723_b200 import polylla as pp
     print(_host_info(), flush=True)
@@ -90,4 +90,40 @@ def test_config4_bit_exact_vs_oracle():
     lc = pp.view_tensor(ctx, v["lcode"], T, torch.uint8)
     _eq_chunked(lc, ref["lcode"], "lcode")
     print(f"config 4 bit-exact: origin/twin/next [{H}], lcode [{T}], seeds [{P}], offsets, loops [{L}]", flush=True)
+    pp.destroy(ctx)
+
+
+def test_int32_ceiling_invariants():
+    """The int32 ceiling of the half-edge ids (PAPER.md L55's
+    capacity question): a jittered grid with s = 18,919 has T = 715,781,448 and
+    H = 3T + 4(s-1) = 2,147,420,016 <= 2^31 - 1 half-edges -- the largest grid the int32
+    ids address (s = 18,920 overflows).  Workspace ~144 GB + 14 GB of input on the 178 GB
+    device; checked by the properties that hold at any size, on the device."""
+    from paper_2403_14723_b200 import polylla as pp
+    from test_gpu_parity import device_invariants
+    import gc
+    gc.collect()
+    torch.cuda.empty_cache()  # (other tests' cached blocks: this one needs ~158 GB of the 178)
+    s = 18919
+    T = 2 * (s - 1) ** 2
+    H = 3 * T + 4 * (s - 1)
+    assert H <= 2**31 - 1 < 3 * 2 * s * s + 4 * s  # (s + 1 would overflow)
+    xy, tri = synth.grid_device(s, 0.2, 5)
+    ws = pp.alloc_workspace(xy.shape[0], T)
+    ctx = pp.build_halfedges(xy, tri, ws)
+    pp.label(ctx)
+    pp.generate(ctx)
+    c = pp.get_counts(ctx)
+    assert c["n_halfedges"] == H and c["n_border"] == 4 * (s - 1)
+    P, L = c["n_polygons"], c["n_loop_entries"]
+    offsets = torch.empty(P + 1, dtype=torch.int32, device="cuda")
+    loops = torch.empty(L, dtype=torch.int32, device="cuda")
+    pp.get_polygons(ctx, offsets, loops)
+    assert pp.get_counts(ctx)["status"] == 0
+    v = pp.get_views(ctx)
+    view = lambda k, n: pp.view_tensor(ctx, v[k], n, torch.int32)  # noqa: E731
+    got = device_invariants(xy, tri, view("origin", H), view("twin", H), view("next", H), offsets, loops,
+                            view("seeds", P))
+    assert got == P
+    print(f"int32 ceiling s={s}: T={T} H={H} P={P} L={L} tips={c['n_tips']}", flush=True)
     pp.destroy(ctx)
