@@ -29,7 +29,8 @@ namespace polylla {
 constexpr int kTileTris = kBuildTileTris;
 constexpr int kTileHE = 3 * kTileTris;   // 6144 half-edges = 192 bit-vector words (e order)
 constexpr int kTileQ = 4 * kTileTris;    // quad slots q = 4t + k (slot 3: copy of vertex 0 / unused)
-constexpr int kTileSlots = 8192;         // pow2 hash slots (load ~0.38: only the lo->hi halves insert)
+constexpr int kTileSlots = 16384;        // pow2 hash slots of 16 bits (load ~0.19: only the lo->hi halves insert)
+constexpr int kSlotBits = 14;            // log2(kTileSlots)
 #ifndef POLYLLA_TILE_THREADS
 #define POLYLLA_TILE_THREADS 768
 #endif
@@ -52,16 +53,17 @@ __device__ __forceinline__ int q_step(int q) {
 // shared memory (bytes):
 //   tri_q int32[kTileQ]   32768  quad layout (v0, v1, v2, v0): half-edge q runs tri_q[q] -> tri_q[q+1]
 //   tw_s  int16[kTileQ]   16384  twin as a quad index, -1 = outside the tile
-//   slot  u32[kTileSlots] 32768  (dead after P2: reused for succ u16[kTileQ])
+//   slot  u16[kTileSlots] 32768  quad index of a lo->hi half-edge, 0xFFFF empty (dead after
+//                                P2: reused for succ u16[kTileQ])
 //   lc_s  u8[kTileTris]    2048
 //   nx_l  int16[kTileHE] 12288 | Sw, Cw, Wl, Lm, Dm, SDm u32[192] 4608   (P4-P6)
-constexpr size_t kOffTw = kTileQ * 4, kOffSlot = kOffTw + kTileQ * 2, kOffLc = kOffSlot + kTileSlots * 4,
+constexpr size_t kOffTw = kTileQ * 4, kOffSlot = kOffTw + kTileQ * 2, kOffLc = kOffSlot + kTileSlots * 2,
                  kOffNx = kOffLc + kTileTris,
                  kNxBytes = kTileHE * 2 + 6 * (kTileHE / 8),                   // P4-P6 arrays (16,896 B)
                  kTileSmem = kOffNx + kNxBytes;                                // 100,864 B -> 2 CTAs/SM
 static_assert(2 * (kTileSmem + 1024) <= 228 * 1024, "two tiles per SM");
 constexpr unsigned long long kLeftDown = 1ull << 63;  // leftover key: set if origin > target
-constexpr uint32_t kSlotQ = (1u << 13) - 1;       // slot = fingerprint(19 bits) << 13 | quad index
+constexpr uint32_t kEmpty16 = 0xFFFFu;             // empty 16-bit slot (quad indices are < 8192)
 // rotation successors (P3/P4): quad index in the low 13 bits, terminal flags above
 constexpr uint16_t kSuccIdx = 0x1FFF, kSuccFront = 0x4000, kSuccUnknown = 0x8000;
 #ifndef POLYLLA_TILE_JUMPS
@@ -114,6 +116,15 @@ __device__ __forceinline__ uint32_t ld_relaxed(const uint32_t* p) {
   return v;
 }
 
+__device__ __forceinline__ void st_relaxed16(uint16_t* p, uint32_t v) {
+  asm volatile("st.relaxed.cta.shared.u16 [%0], %1;" ::"r"((uint32_t)__cvta_generic_to_shared(p)), "h"((uint16_t)v));
+}
+__device__ __forceinline__ uint32_t ld_relaxed16(const uint16_t* p) {
+  uint16_t v;
+  asm volatile("ld.relaxed.cta.shared.u16 %0, [%1];" : "=h"(v) : "r"((uint32_t)__cvta_generic_to_shared(p)));
+  return v;
+}
+
 __device__ __forceinline__ double sq_len(double2 p, double2 q) {
   // |q - p|^2 = dx*dx + dy*dy, dx = x[target] - x[origin]; IEEE RN, no FMA (R11)
   const double dx = __dsub_rn(q.x, p.x), dy = __dsub_rn(q.y, p.y);
@@ -128,55 +139,49 @@ __device__ __forceinline__ uint64_t policy_evict_last() {
 }
 __device__ __forceinline__ double2 ld_xy(const double2* ptr, uint64_t pol) {
   double2 r;
-  asm volatile("ld.global.nc.L2::cache_hint.v2.f64 {%0, %1}, [%2], %3;" : "=d"(r.x), "=d"(r.y) : "l"(ptr), "l"(pol));
+  asm("ld.global.nc.L2::cache_hint.v2.f64 {%0, %1}, [%2], %3;" : "=d"(r.x), "=d"(r.y) : "l"(ptr), "l"(pol));
   return r;
 }
 
-// Tile hash on the undirected key (lo, hi), linear probing over uint32 slots holding
-// fingerprint(19 bits) << 13 | q.  The half-edges with origin < target insert their key,
-// those with origin > target look it up (read-only).
-// two multiplies: the high bits of the final product are well mixed; they give the slot
-// (position = top 13 bits via tile_pos) and the fingerprint (bits 13..31)
+// Tile hash on the undirected key (lo, hi): linear probing over 16-bit slots holding the
+// quad index of the lo->hi half-edge (origin < target); the hi->lo halves look it up
+// read-only.  A slot is verified against the key through tri_q (the slot carries no
+// fingerprint: 16-bit slots double the slot count in the same 32 KB, halving the
+// collision losers of the claim pass).  The high bits of the product are well mixed.
 __device__ __forceinline__ uint32_t tile_hash(uint32_t lo, uint32_t hi) {
   return ((lo * 0x9E3779B1u) ^ hi) * 0x85EBCA6Bu;
 }
-__device__ __forceinline__ uint32_t tile_pos(uint32_t h) { return h >> (32 - 13); }
+__device__ __forceinline__ uint32_t tile_pos(uint32_t lo, uint32_t hi) { return tile_hash(lo, hi) >> (32 - kSlotBits); }
 
-// does slot word w hold the directed key lo -> hi? (fingerprint, then the vertices)
-__device__ __forceinline__ bool slot_is(uint32_t w, uint32_t fp, const int32_t* tri_q, uint32_t lo, uint32_t hi) {
-  if ((w & ~kSlotQ) != fp) return false;
-  const int32_t sq = (int32_t)(w & kSlotQ);
-  return (uint32_t)tri_q[sq] == lo && (uint32_t)tri_q[sq + 1] == hi;
-}
-
-// collision loser: CAS + linear probing from the slot after its home
-__device__ __noinline__ uint32_t tile_insert_probe(uint32_t* slot, const int32_t* tri_q, int32_t q, uint32_t lo,
+// collision loser of the claim pass: CAS (on the 32-bit word holding the 16-bit slot) +
+// linear probing from its home slot
+__device__ __noinline__ uint32_t tile_insert_probe(uint16_t* slot, const int32_t* tri_q, int32_t q, uint32_t lo,
                                                    uint32_t hi) {
-  const uint32_t h = tile_hash(lo, hi);
-  const uint32_t fp = h & ~kSlotQ;
-  const uint32_t mine = fp | (uint32_t)q;
-  uint32_t p = tile_pos(h);
+  uint32_t p = tile_pos(lo, hi);
   for (int probe = 0; probe < kTileSlots; ++probe, p = (p + 1) & (kTileSlots - 1)) {
-    uint32_t w = ld_relaxed(&slot[p]);
-    if (w == kEmpty) {
-      w = atomicCAS(&slot[p], kEmpty, mine);
-      if (w == kEmpty) return 0;
+    uint32_t* wp = reinterpret_cast<uint32_t*>(slot + (p & ~1u));
+    const int sh = (int)(p & 1) * 16;
+    uint32_t word = ld_relaxed(wp);
+    uint32_t v = (word >> sh) & 0xFFFFu;
+    while (v == kEmpty16) {
+      const uint32_t old = atomicCAS(wp, word, (word & ~(0xFFFFu << sh)) | ((uint32_t)q << sh));
+      if (old == word) return 0;
+      word = old;  // (the other half changed, or this one was taken)
+      v = (word >> sh) & 0xFFFFu;
     }
-    if (slot_is(w, fp, tri_q, lo, hi)) return ST_NONMANIFOLD_EDGE;  // the same directed edge twice
+    if ((uint32_t)tri_q[v] == lo && (uint32_t)tri_q[v + 1] == hi) return ST_NONMANIFOLD_EDGE;  // same directed edge twice
   }
   return ST_INTERNAL;
 }
 
-// the quad holding key lo -> hi, probing from the slot after `p` (the home slot missed), or -1
-__device__ __noinline__ int32_t tile_lookup_probe(const uint32_t* slot, const int32_t* tri_q, uint32_t lo, uint32_t hi) {
-  const uint32_t h = tile_hash(lo, hi);
-  const uint32_t fp = h & ~kSlotQ;
-  uint32_t p = tile_pos(h);
+// the quad holding key lo -> hi, probing from the slot after its home (the home missed), or -1
+__device__ __noinline__ int32_t tile_lookup_probe(const uint16_t* slot, const int32_t* tri_q, uint32_t lo, uint32_t hi) {
+  uint32_t p = tile_pos(lo, hi);
   for (int probe = 1; probe < kTileSlots; ++probe) {
     p = (p + 1) & (kTileSlots - 1);
     const uint32_t w = slot[p];
-    if (w == kEmpty) return -1;
-    if (slot_is(w, fp, tri_q, lo, hi)) return (int32_t)(w & kSlotQ);
+    if (w == kEmpty16) return -1;
+    if ((uint32_t)tri_q[w] == lo && (uint32_t)tri_q[w + 1] == hi) return (int32_t)w;
   }
   return -1;
 }
@@ -221,7 +226,7 @@ __device__ __forceinline__ void tile_body(
   int32_t* tri_q = reinterpret_cast<int32_t*>(smem_tile);
   int4* tri_q4 = reinterpret_cast<int4*>(smem_tile);
   int16_t* tw_s = reinterpret_cast<int16_t*>(smem_tile + kOffTw);
-  uint32_t* slot = reinterpret_cast<uint32_t*>(smem_tile + kOffSlot);
+  uint16_t* slot = reinterpret_cast<uint16_t*>(smem_tile + kOffSlot);
   uint8_t* lc_s = smem_tile + kOffLc;
   int16_t* nx_l = reinterpret_cast<int16_t*>(smem_tile + kOffNx);               // local next, -1: not walkable
   // six word arrays in a row (P4b stores word wl of array r at Sw + r * kTileWords + wl)
@@ -232,7 +237,7 @@ __device__ __forceinline__ void tile_body(
   uint32_t* Dm = Lm + kTileWords;                                                // deferred bits
   uint32_t* SDm = Dm + kTileWords;                                               // deferred seed bits
   // overlays of the slot area (after P2)
-  uint16_t* succ = reinterpret_cast<uint16_t*>(slot);
+  uint16_t* succ = slot;
 
   const int64_t f0 = tile * kTileTris;
   const int64_t f0n = tile_next * kTileTris;  // this CTA's next tile (prefetched), if tile_next >= 0
@@ -245,29 +250,41 @@ __device__ __forceinline__ void tile_body(
   long long t_phase_ = clock64();
 #endif
 
-  // ---- P0: clear the hash slots and the twins; P1 reads the raw triangles straight from
-  // global memory (the tile was bulk-prefetched into L2 by the CTA before; staging it in
-  // shared memory first measured 1% slower)
+  // ---- P0: clear the hash slots and the twins (the claims of P1 need the barrier); P1
+  // reads the raw triangles straight from global memory (the tile was bulk-prefetched
+  // into L2 by the CTA before; staging it in shared memory first measured 1% slower)
   const int32_t* raw = tri + e0;
-  for (int i = tid; i < kTileSlots / 4; i += kTileThreads)
-    reinterpret_cast<uint4*>(slot)[i] = make_uint4(kEmpty, kEmpty, kEmpty, kEmpty);
+  for (int i = tid; i < kTileSlots / 8; i += kTileThreads)
+    reinterpret_cast<uint4*>(slot)[i] = make_uint4(0xFFFFFFFFu, 0xFFFFFFFFu, 0xFFFFFFFFu, 0xFFFFFFFFu);
   for (int i = tid; i < kTileQ / 2; i += kTileThreads) reinterpret_cast<uint32_t*>(tw_s)[i] = 0xFFFFFFFFu;
   if (tid == 0 && tile_next >= 0) {  // the next tile's triangles -> L2 (TMA bulk prefetch)
     const int64_t nn = T - f0n < kTileTris ? T - f0n : kTileTris;
     const int32_t* pn = tri + 3 * f0n;
     const uint32_t bytes = (uint32_t)((3 * nn * 4) & ~int64_t(15));
     if (bytes && (reinterpret_cast<uintptr_t>(pn) & 15) == 0)
-      asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(pn), "r"(bytes) : "memory");
+      asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(pn), "r"(bytes));
   }
+  // the raw triangles of this thread, loaded before the barrier
+  int32_t ids[kTriIters][3];
+#pragma unroll
+  for (int i = 0; i < kTriIters; ++i) {
+    const int t = tid + i * kTileThreads;
+    if (tri_ok<FULL>(i, t, nt)) {
+      ids[i][0] = raw[3 * t]; ids[i][1] = raw[3 * t + 1]; ids[i][2] = raw[3 * t + 2];
+    } else {
+      ids[i][0] = ids[i][1] = ids[i][2] = 0;
+    }
+  }
+  __syncthreads();
   PHASE_MARK(0);
 
-  // ---- P1: per triangle: checks, orientation, Lcode
+  // ---- P1: per triangle: checks, orientation, Lcode; the lo->hi halves claim their home
+  // slot of the tile hash with a plain store (last writer wins; P2 verifies)
   const uint64_t pol = policy_evict_last();
   uint32_t bad = 0;
   int flips = 0;
   // the FP64 decisions (R11: IEEE RN, no FMA)
-  auto orient_tri = [&](int t) {
-    int32_t a = raw[3 * t], b = raw[3 * t + 1], c = raw[3 * t + 2];
+  auto orient_tri = [&](int t, int32_t a, int32_t b, int32_t c) {
     if ((uint64_t)a >= (uint64_t)V || (uint64_t)b >= (uint64_t)V || (uint64_t)c >= (uint64_t)V) {
       bad |= ST_DANGLING;
       a = 0; b = 0; c = 0;
@@ -290,12 +307,15 @@ __device__ __forceinline__ void tile_body(
     lc_s[t] = (uint8_t)k;
     lcode[f0 + t] = (uint8_t)k;
     tri_q4[t] = make_int4(a, b, c, a);
+    if (a < b) st_relaxed16(slot + tile_pos(a, b), 4 * t);
+    if (b < c) st_relaxed16(slot + tile_pos(b, c), 4 * t + 1);
+    if (c < a) st_relaxed16(slot + tile_pos(c, a), 4 * t + 2);
   };
 #pragma unroll
   for (int i = 0; i < kTriIters; ++i) {
     const int t = tid + i * kTileThreads;
     if (!tri_ok<FULL>(i, t, nt)) continue;
-    orient_tri(t);
+    orient_tri(t, ids[i][0], ids[i][1], ids[i][2]);
   }
   flips = __reduce_add_sync(0xffffffffu, flips);
   bad = __reduce_or_sync(0xffffffffu, bad);
@@ -308,8 +328,8 @@ __device__ __forceinline__ void tile_body(
 
   // L2 prefetch of the coordinates of the next tile's vertices (its triangles were
   // bulk-prefetched in P0), so that tile's P1 gathers hit L2 instead of HBM: one triangle
-  // per thread per P2 pass, its ids loaded at the start of the pass and the prefetches
-  // issued at its end (the loads' latency hides behind the pass)
+  // per thread per pass (P2, P2c, P3), its ids loaded at the start of the pass and the
+  // prefetches issued at its end (the loads' latency hides behind the pass)
   const int64_t nn_pf = tile_next >= 0 ? (T - f0n < kTileTris ? T - f0n : kTileTris) : 0;
   int32_t pf_v[3];
   bool pf_ok = false;
@@ -330,109 +350,74 @@ __device__ __forceinline__ void tile_body(
     }
   };
 
-  // ---- P2a: the lo->hi halves claim their home slot with a plain store (last writer wins)
+  // ---- P2: every half-edge re-reads its home slot (the claims are final: a slot, once
+  // claimed, never changes).  lo->hi: the losers of their home slot insert with CAS +
+  // linear probing (after the loop, one merged loop per lane).  hi->lo: a twin found in
+  // the home slot is recorded now; a different key there -> probed in P2c (after every
+  // loser is in); an empty home slot -> no twin in the tile (a loser never lands in an
+  // empty home of a key whose lo->hi half exists: that half claimed it).
   pf_load(0);
-#pragma unroll
-  for (int i = 0; i < kTriIters; ++i) {
-    const int t = tid + i * kTileThreads;
-    if (!tri_ok<FULL>(i, t, nt)) continue;
-    const int4 v = tri_q4[t];
-    const int32_t vs[4] = {v.x, v.y, v.z, v.w};
-#pragma unroll
-    for (int k = 0; k < 3; ++k) {
-      const uint32_t o = (uint32_t)vs[k], tg = (uint32_t)vs[k + 1];
-      const uint32_t h = tile_hash(min(o, tg), max(o, tg));
-      if (o < tg) st_relaxed(&slot[tile_pos(h)], (h & ~kSlotQ) | (uint32_t)(4 * t + k));
-    }
-  }
-  pf_issue();
-  __syncthreads();
-  // ... the losers of a home slot insert with CAS + linear probing (one merged loop per lane)
-  pf_load(1);
-  uint32_t nm = 0;
+  uint32_t nm = 0, pend_look = 0;
   {
-    uint32_t pend = 0;
+    uint32_t pend_ins = 0;
 #pragma unroll
     for (int i = 0; i < kTriIters; ++i) {
       const int t = tid + i * kTileThreads;
       if (!tri_ok<FULL>(i, t, nt)) continue;
       const int4 v = tri_q4[t];
       const int32_t vs[4] = {v.x, v.y, v.z, v.w};
-      uint32_t got[3], mine[3];
+      // the three home slots, then the candidates' vertices, then the decisions (loads
+      // issued together, predicated, no branch between them)
+      uint32_t w[3];
 #pragma unroll
-      for (int k = 0; k < 3; ++k) {  // the three re-reads issued together
+      for (int k = 0; k < 3; ++k) {
         const uint32_t o = (uint32_t)vs[k], tg = (uint32_t)vs[k + 1];
-        const uint32_t h = tile_hash(min(o, tg), max(o, tg));
-        mine[k] = (h & ~kSlotQ) | (uint32_t)(4 * t + k);
-        got[k] = o < tg ? ld_relaxed(&slot[tile_pos(h)]) : mine[k];
+        w[k] = ld_relaxed16(slot + tile_pos(min(o, tg), max(o, tg)));
+      }
+      int32_t ca[3], cb[3];
+#pragma unroll
+      for (int k = 0; k < 3; ++k) {
+        const bool look = vs[k] > vs[k + 1] && w[k] != kEmpty16;
+        ca[k] = look ? tri_q[w[k]] : -1;
+        cb[k] = look ? tri_q[w[k] + 1] : -1;
       }
 #pragma unroll
-      for (int k = 0; k < 3; ++k)
-        if (got[k] != mine[k]) pend |= 1u << (4 * i + k);
+      for (int k = 0; k < 3; ++k) {
+        const int32_t q = 4 * t + k;
+        if (vs[k] < vs[k + 1]) {
+          if (w[k] != (uint32_t)q) pend_ins |= 1u << (4 * i + k);
+        } else if (vs[k] > vs[k + 1] && w[k] != kEmpty16) {
+          if (ca[k] == vs[k + 1] && cb[k] == vs[k]) {
+            tw_s[q] = (int16_t)w[k];
+            tw_s[w[k]] = (int16_t)q;
+          } else {
+            pend_look |= 1u << (4 * i + k);
+          }
+        }
+      }
     }
-    while (pend) {
-      const int b = __ffs(pend) - 1;
-      pend &= pend - 1;
+    while (pend_ins) {
+      const int b = __ffs(pend_ins) - 1;
+      pend_ins &= pend_ins - 1;
       const int q = 4 * (tid + (b >> 2) * kTileThreads) + (b & 3);
       nm |= tile_insert_probe(slot, tri_q, q, (uint32_t)tri_q[q], (uint32_t)tri_q[q + 1]);
     }
   }
   pf_issue();
   __syncthreads();
-  // ---- P2b: the hi->lo halves find their twin: home slot probed by every lane, misses loop
-  if (kTriIters > 2) pf_load(2);
-  {
-    uint32_t pend = 0;
-#pragma unroll
-    for (int i = 0; i < kTriIters; ++i) {
-      const int t = tid + i * kTileThreads;
-      if (!tri_ok<FULL>(i, t, nt)) continue;
-      const int4 v = tri_q4[t];
-      const int32_t vs[4] = {v.x, v.y, v.z, v.w};
-      // the three half-edges' probes issued together (predicated loads, no branch
-      // between them): home slots, then the candidates' vertices, then the decisions
-      uint32_t w[3], fp[3];
-      bool look[3];
-#pragma unroll
-      for (int k = 0; k < 3; ++k) {
-        const uint32_t o = (uint32_t)vs[k], tg = (uint32_t)vs[k + 1];
-        look[k] = o > tg;
-        const uint32_t h = tile_hash(tg, o);
-        fp[k] = h & ~kSlotQ;
-        w[k] = look[k] ? slot[tile_pos(h)] : kEmpty;
-      }
-      int32_t ca[3], cb[3];
-#pragma unroll
-      for (int k = 0; k < 3; ++k) {
-        const bool f = w[k] != kEmpty && (w[k] & ~kSlotQ) == fp[k];
-        const int32_t sq = (int32_t)(w[k] & kSlotQ);
-        ca[k] = f ? tri_q[sq] : -1;
-        cb[k] = f ? tri_q[sq + 1] : -1;
-      }
-#pragma unroll
-      for (int k = 0; k < 3; ++k) {
-        const bool hit = look[k] && ca[k] == vs[k + 1] && cb[k] == vs[k];
-        if (hit) {
-          const int32_t sq = (int32_t)(w[k] & kSlotQ);
-          tw_s[4 * t + k] = (int16_t)sq;
-          tw_s[sq] = (int16_t)(4 * t + k);
-        } else if (look[k] && w[k] != kEmpty) {
-          pend |= 1u << (4 * i + k);
-        }
-      }
-    }
-    while (pend) {
-      const int b = __ffs(pend) - 1;
-      pend &= pend - 1;
-      const int q = 4 * (tid + (b >> 2) * kTileThreads) + (b & 3);
-      const int32_t sq = tile_lookup_probe(slot, tri_q, (uint32_t)tri_q[q + 1], (uint32_t)tri_q[q]);
-      if (sq >= 0) {
-        tw_s[q] = (int16_t)sq;
-        tw_s[sq] = (int16_t)q;
-      }
+  // ---- P2c: the hi->lo halves whose home slot held another key probe on
+  pf_load(1);
+  while (pend_look) {
+    const int b = __ffs(pend_look) - 1;
+    pend_look &= pend_look - 1;
+    const int q = 4 * (tid + (b >> 2) * kTileThreads) + (b & 3);
+    const int32_t sq = tile_lookup_probe(slot, tri_q, (uint32_t)tri_q[q + 1], (uint32_t)tri_q[q]);
+    if (sq >= 0) {
+      tw_s[q] = (int16_t)sq;
+      tw_s[sq] = (int16_t)q;
     }
   }
-  if (kTriIters > 2) pf_issue();
+  pf_issue();
   if (nm) raise_status(ctr, nm);
   __syncthreads();
   PHASE_MARK(2);
@@ -441,6 +426,7 @@ __device__ __forceinline__ void tile_body(
   //   succ[x] = x | FRONT   if x is a frontier half-edge (walk ends there)
   //   succ[x] = x | UNKNOWN if twin(x) is outside the tile (walk must be deferred)
   //   succ[x] = next_q(twin x)  otherwise (cross the non-frontier edge: sweep_out)
+  if (kTriIters > 2) pf_load(2);
   nm = 0;
 #pragma unroll 4
   for (int i = 0, q = q0; i < kHeIters; ++i, q = q_step(q)) {
@@ -460,6 +446,7 @@ __device__ __forceinline__ void tile_body(
     const bool front = lq != k && lt != (tq & 3);  // neither half the longest edge of its triangle
     succ[q] = (uint16_t)(tq < 0 ? (q | kSuccUnknown) : front ? (q | kSuccFront) : next_q(tq));
   }
+  if (kTriIters > 2) pf_issue();
   if (nm) raise_status(ctr, nm);
   __syncthreads();
   PHASE_MARK(3);
