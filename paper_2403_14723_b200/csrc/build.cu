@@ -37,11 +37,11 @@ constexpr int kSlotBits = 14;            // log2(kTileSlots)
 constexpr int kTileThreads = POLYLLA_TILE_THREADS;
 constexpr int kTileWords = kTileHE / 32; // 192
 constexpr int kTriIters = (kTileTris + kTileThreads - 1) / kTileThreads;  // 768: 3 (the third: threads < 512)
-constexpr int kHeIters = kTileHE / kTileThreads;                           // 768: 8 exactly
-static_assert(kTileHE % kTileThreads == 0 && kTileThreads % 3 != 2, "half-edge loops: q_step below");
 static_assert(kTileThreads % 32 == 0 && (kTileTris - (kTriIters - 1) * kTileThreads) % 32 == 0,
               "warp-uniform last triangle iteration");
 static_assert(4 * kTriIters <= 32, "per-lane pending bit masks");
+constexpr int kHeIters = kTileHE / kTileThreads;                           // 768: 8 exactly
+static_assert(kTileHE % kTileThreads == 0 && kTileThreads % 3 != 2, "half-edge loops: q_step below");
 // quad of half-edge j + kTileThreads from the quad q of j (no division): 768 = 3 * 256
 // -> q + 1024; 1024 = 3 * 341 + 1 -> q + 1365, skipping the padding slot k = 3
 constexpr int kQStep = 4 * (kTileThreads / 3) + kTileThreads % 3;
@@ -56,11 +56,11 @@ __device__ __forceinline__ int q_step(int q) {
 //   slot  u16[kTileSlots] 32768  quad index of a lo->hi half-edge, 0xFFFF empty (dead after
 //                                P2: reused for succ u16[kTileQ])
 //   lc_s  u8[kTileTris]    2048
-//   nx_l  int16[kTileHE] 12288 | Sw, Cw, Wl, Lm, Dm, SDm u32[192] 4608   (P4-P6)
+//   nx_l  int16[kTileQ]  16384 | Sw, Cw, Wl, Lm, Dm, SDm u32[192] 4608   (P4-P6; quad-indexed local next)
 constexpr size_t kOffTw = kTileQ * 4, kOffSlot = kOffTw + kTileQ * 2, kOffLc = kOffSlot + kTileSlots * 2,
                  kOffNx = kOffLc + kTileTris,
-                 kNxBytes = kTileHE * 2 + 6 * (kTileHE / 8),                   // P4-P6 arrays (16,896 B)
-                 kTileSmem = kOffNx + kNxBytes;                                // 100,864 B -> 2 CTAs/SM
+                 kNxBytes = kTileQ * 2 + 6 * (kTileHE / 8),                    // P4-P6 arrays (20,992 B)
+                 kTileSmem = kOffNx + kNxBytes;                                // 104,960 B -> 2 CTAs/SM
 static_assert(2 * (kTileSmem + 1024) <= 228 * 1024, "two tiles per SM");
 constexpr unsigned long long kLeftDown = 1ull << 63;  // leftover key: set if origin > target
 constexpr uint32_t kEmpty16 = 0xFFFFu;             // empty 16-bit slot (quad indices are < 8192)
@@ -72,10 +72,6 @@ constexpr uint16_t kSuccIdx = 0x1FFF, kSuccFront = 0x4000, kSuccUnknown = 0x8000
 // pointer-jumping rounds (even: the result ends in succ); each use of a successor then
 // follows up to kTileHops more jumped pointers, so chains up to 16 steps resolve in-tile
 constexpr int kTileJumps = POLYLLA_TILE_JUMPS;
-#ifndef POLYLLA_P4B_UNROLL
-#define POLYLLA_P4B_UNROLL 2
-#endif
-constexpr int kP4bUnroll = POLYLLA_P4B_UNROLL;  // P4b loop unroll (1 / 2 / 4 measured: 2 best)
 constexpr int kTileHops = (16 >> kTileJumps) - 1;
 #ifndef POLYLLA_P6_MAXLEN
 #define POLYLLA_P6_MAXLEN 1024  // (a test variant sets it tiny to force the global seed walk)
@@ -228,9 +224,9 @@ __device__ __forceinline__ void tile_body(
   int16_t* tw_s = reinterpret_cast<int16_t*>(smem_tile + kOffTw);
   uint16_t* slot = reinterpret_cast<uint16_t*>(smem_tile + kOffSlot);
   uint8_t* lc_s = smem_tile + kOffLc;
-  int16_t* nx_l = reinterpret_cast<int16_t*>(smem_tile + kOffNx);               // local next, -1: not walkable
-  // six word arrays in a row (P4b stores word wl of array r at Sw + r * kTileWords + wl)
-  uint32_t* Sw = reinterpret_cast<uint32_t*>(smem_tile + kOffNx + kTileHE * 2);  // seed bits (e order)
+  int16_t* nx_l = reinterpret_cast<int16_t*>(smem_tile + kOffNx);               // local next (quad), -1: not walkable
+  // six word arrays in a row (word wl of array r at Sw + r * kTileWords + wl)
+  uint32_t* Sw = reinterpret_cast<uint32_t*>(smem_tile + kOffNx + kTileQ * 2);   // seed bits (e order)
   uint32_t* Cw = Sw + kTileWords;                                                // canonical seed bits
   int32_t* Wl = reinterpret_cast<int32_t*>(Cw + kTileWords);                     // loop lengths per C word
   uint32_t* Lm = reinterpret_cast<uint32_t*>(Wl + kTileWords);                   // leftover bits
@@ -245,7 +241,6 @@ __device__ __forceinline__ void tile_body(
   const int nhe = 3 * nt;
   const int64_t e0 = 3 * f0;
   const int tid = threadIdx.x, lane = tid & 31;
-  const int q0 = q_of(tid);  // quad of half-edge j = tid (then q_step per kTileThreads)
 #ifdef POLYLLA_PHASE_TIMING
   long long t_phase_ = clock64();
 #endif
@@ -422,29 +417,68 @@ __device__ __forceinline__ void tile_body(
   __syncthreads();
   PHASE_MARK(2);
 
-  // ---- P3: origin/twin out (coalesced); rotation successors:
+  // ---- P3..P4b run per triangle (thread t = tid + 768 i takes the quad 4t..4t+3: one
+  // 8-byte shared access per array instead of three, and the three half-edges' gathers
+  // issued together).  A warp's 32 triangles are the 96 half-edges of 3 bit-vector words
+  // (tile words 72 i + 3 warp + m, m < 3): per-lane flag bits go to the words by one
+  // shuffle + one ballot per word and flag (word_bits below).
+  // Loop over every triangle slot of the tile (warp-uniform; triangles past nt of a
+  // partial tile contribute zero bits, so every shared word is written).
+  static_assert(kTileThreads % 32 == 0 && (kTileTris - (kTriIters - 1) * kTileThreads) % 32 == 0, "uniform");
+  const int wl_warp = 3 * (tid >> 5);  // + (3 * 768 / 32) i: tile-local word of the warp's first half-edge
+  const int lane_m = lane % 3, lane_ty = lane / 3;  // word stores: lane = 3 * type + m
+  // bit k (k < 3) of field f of lane src -> bit `lane` of word m: half-edge h = 32 m + lane
+  // of the warp's 96 is half-edge k = h % 3 of the warp's triangle h / 3
+  auto word_bits = [&](uint32_t packed, int m, int field) -> uint32_t {
+    const int h = 32 * m + lane, src = (h * 0x5556) >> 16, k = h - 3 * src;
+    const uint32_t v = __shfl_sync(0xffffffffu, packed, src);
+    return __ballot_sync(0xffffffffu, (v >> (4 * field + k)) & 1u);
+  };
+  auto pick_m = [&](uint32_t w0, uint32_t w1, uint32_t w2) { return lane_m == 0 ? w0 : lane_m == 1 ? w1 : w2; };
+
+  // ---- P3 (per half-edge, e order): origin/twin out (coalesced); rotation successors:
   //   succ[x] = x | FRONT   if x is a frontier half-edge (walk ends there)
   //   succ[x] = x | UNKNOWN if twin(x) is outside the tile (walk must be deferred)
   //   succ[x] = next_q(twin x)  otherwise (cross the non-frontier edge: sweep_out)
+  // seed bits S (Alg. 9: a terminal edge's smaller half; never a frontier half-edge, so
+  // never deferred) and leftover bits (twin outside the tile) by warp ballots -> Sw / S / Lm
+  // (slot 3 of every quad: 0xFFFF, terminal, never a target)
   if (kTriIters > 2) pf_load(2);
   nm = 0;
+  for (int i = tid; i < kTileTris; i += kTileThreads) succ[4 * i + 3] = 0xFFFFu;
+  {
+    uint32_t* const s_dst = lane == 0 ? Sw : Lm;
+    int q = q_of(tid);
 #pragma unroll 4
-  for (int i = 0, q = q0; i < kHeIters; ++i, q = q_step(q)) {
-    const int j = tid + i * kTileThreads;
-    if (!FULL && j >= nhe) break;
-    const int k = q & 3, t = q >> 2;
-    // loads issued together: own twin / vertex / Lcode, then the twin's back-pointer and Lcode
-    const int32_t tq = tw_s[q];
-    const int32_t org = tri_q[q];
-    const uint8_t lq = lc_s[t];
-    const int32_t tqs = tq < 0 ? q : tq;
-    const int32_t back = tw_s[tqs];
-    const uint8_t lt = lc_s[tqs >> 2];
-    if (tq >= 0 && back != q) nm = ST_NONMANIFOLD_EDGE;  // twin claimed twice (edge in > 2 triangles)
-    __stcs(origin + e0 + j, org);
-    __stcs(twin + e0 + j, tq >= 0 ? (int32_t)(e0 + j_of(tq)) : -1);
-    const bool front = lq != k && lt != (tq & 3);  // neither half the longest edge of its triangle
-    succ[q] = (uint16_t)(tq < 0 ? (q | kSuccUnknown) : front ? (q | kSuccFront) : next_q(tq));
+    for (int i = 0; i < kHeIters; ++i, q = q_step(q)) {
+      const int j = tid + i * kTileThreads;
+      bool sd = false, left = false;
+      if (FULL || j < nhe) {
+        const int k = q & 3, t = q >> 2;
+        // loads issued together: own twin / vertex / Lcode, then the twin's back-pointer and Lcode
+        const int32_t tq = tw_s[q];
+        const int32_t org = tri_q[q];
+        const int32_t lq = lc_s[t];
+        const int32_t tqs = tq < 0 ? q : tq;
+        const int32_t back = tw_s[tqs];
+        const int32_t lt = lc_s[tqs >> 2];
+        if (tq >= 0 && back != q) nm = ST_NONMANIFOLD_EDGE;  // twin claimed twice (edge in > 2 triangles)
+        __stcs(origin + e0 + j, org);
+        __stcs(twin + e0 + j, tq >= 0 ? (int32_t)(e0 + j_of(tq)) : -1);
+        const bool front = lq != k && lt != (tq & 3);  // neither half the longest edge of its triangle
+        succ[q] = (uint16_t)(tq < 0 ? (q | kSuccUnknown) : front ? (q | kSuccFront) : next_q(tq));
+        sd = tq >= 0 && lq == k && lt == (tq & 3) && q < tq;  // terminal edge, smaller id
+        left = tq < 0;
+      }
+      const uint32_t sw = __ballot_sync(0xffffffffu, sd), lw = __ballot_sync(0xffffffffu, left);
+      const int wl = (j - lane) >> 5;  // tile-local word of this warp
+      // lane 0: Sw, lane 1: Lm (shared); lane 2: the global S
+      if (lane < 2) {
+        s_dst[wl] = lane == 0 ? sw : lw;
+      } else if (lane == 2 && (FULL || j - lane < nhe)) {
+        F0[2 * bv_stride + (e0 >> 5) + wl] = sw;
+      }
+    }
   }
   if (kTriIters > 2) pf_issue();
   if (nm) raise_status(ctr, nm);
@@ -453,78 +487,78 @@ __device__ __forceinline__ void tile_body(
 
   // ---- P4a: pointer jumping, double-buffered between succ and the (still unused) P4-P6
   // area: each round doubles the resolved chain length; an even number of rounds leaves
-  // the result in succ.
+  // the result in succ.  (Slot 3 of a quad holds 0xFFFF: terminal, never a target.)
   static_assert(kTileJumps % 2 == 0 && kTileJumps <= 4, "result must end in succ");
   uint16_t* succ_b = reinterpret_cast<uint16_t*>(smem_tile + kOffNx);  // 16 KB <= the P4-P6 area
 #pragma unroll 1
   for (int round = 0; round < kTileJumps; ++round) {
     const uint16_t* src = (round & 1) ? succ_b : succ;
     uint16_t* dst = (round & 1) ? succ : succ_b;
-    int q = q0;
 #pragma unroll
-    for (int i = 0; i < kHeIters; ++i, q = q_step(q)) {
-      if (!FULL && tid + i * kTileThreads >= nhe) break;
-      const uint16_t sc = src[q];
-      dst[q] = (sc & (kSuccFront | kSuccUnknown)) ? sc : src[sc];
+    for (int i = 0; i < kTriIters; ++i) {
+      const int t = tid + i * kTileThreads;
+      if (!tri_ok<FULL>(i, t, nt)) continue;
+      const uint2 s2 = *reinterpret_cast<const uint2*>(src + 4 * t);
+      const uint32_t sc[3] = {s2.x & 0xFFFFu, s2.x >> 16, s2.y & 0xFFFFu};
+      uint32_t d[3];
+#pragma unroll
+      for (int k = 0; k < 3; ++k) d[k] = (sc[k] & (kSuccFront | kSuccUnknown)) ? sc[k] : src[sc[k]];
+      *reinterpret_cast<uint2*>(dst + 4 * t) = make_uint2(d[0] | (d[1] << 16), d[2] | 0xFFFF0000u);
     }
     __syncthreads();
   }
   PHASE_MARK(4);
 
-  // ---- P4b: per half-edge (e order): F / S words (Alg. 8-9), next (Alg. 11), tips
-  // (per-lane word targets hoisted: lanes 0-5 the shared arrays Sw..SDm, lanes 8-11 the
-  // global F0, F1, S, TB)
-  const int s_off = lane < 6 ? lane * kTileWords : -1;
-  uint32_t* const g_word = F0 + (int64_t)(lane >= 8 && lane < 12 ? lane - 8 : 0) * bv_stride + (e0 >> 5);
-  const bool g_lane = lane >= 8 && lane < 12;
-  // per-lane value masks (a select chain on the lane compiles to a divergent jump table)
-  const uint32_t m_s = 0u - (uint32_t)(lane == 0 || lane == 10), m_l = 0u - (uint32_t)(lane == 3),
-                 m_d = 0u - (uint32_t)(lane == 4), m_f = 0u - (uint32_t)(lane == 8 || lane == 9),
-                 m_t = 0u - (uint32_t)(lane == 11);
-#pragma unroll kP4bUnroll
-  for (int i = 0, q = q0; i < kHeIters; ++i, q = q_step(q)) {
-    const int j = tid + i * kTileThreads;
-    bool fr = false, sd = false, tip = false, deferred = false, left = false;
-    int32_t nl_j = -1;
-    if (FULL || j < nhe) {
-      const int32_t tq = tw_s[q];
-      if (tq < 0) {
-        deferred = left = true;
-      } else {
-        fr = succ[q] == (uint16_t)(q | kSuccFront);  // terminal of its own chain: a frontier half-edge
-        sd = lc_s[q >> 2] == (q & 3) && lc_s[tq >> 2] == (tq & 3) && q < tq;  // terminal edge, smaller id
+  // ---- P4b: per triangle: next (Alg. 11) of its three half-edges, F words (Alg. 8), tips
+  // (next == twin, R4), deferred half-edges; the local next in quad indices (nx_q; the
+  // global origin/twin/next are written from the quad arrays in half-edge order in P5)
+  int16_t* nx_q = nx_l;  // quad-indexed local next: -1 not walkable, -2 barrier tip
+#pragma unroll
+  for (int i = 0; i < kTriIters; ++i) {
+    if (!(i < kTriIters - 1 || tid < kTileTris - (kTriIters - 1) * kTileThreads)) continue;
+    const int t = tid + i * kTileThreads;
+    uint32_t packed = 0;  // field 0: frontier, 1: tip, 2: deferred
+    if (FULL || t < nt) {
+      const uint2 s2 = *reinterpret_cast<const uint2*>(succ + 4 * t);
+      const uint2 tw2 = *reinterpret_cast<const uint2*>(tw_s + 4 * t);
+      const uint32_t sc[3] = {s2.x & 0xFFFFu, s2.x >> 16, s2.y & 0xFFFFu};
+      const int32_t tq[3] = {(int16_t)(tw2.x & 0xFFFFu), (int16_t)(tw2.x >> 16), (int16_t)(tw2.y & 0xFFFFu)};
+      int32_t nl[3];
+#pragma unroll
+      for (int k = 0; k < 3; ++k) {
+        const int32_t q = 4 * t + k;
+        const bool left = sc[k] == (uint32_t)(q | kSuccUnknown);
+        bool fr = sc[k] == (uint32_t)(q | kSuccFront);  // terminal of its own chain: a frontier half-edge
+        bool tip = false, deferred = left;
         int32_t nx = next_q(q);
         if (fr) {
-          uint16_t r = succ[nx];  // first frontier half-edge about target(j), if reached
+          uint32_t r = sc[k == 2 ? 0 : k + 1];  // succ[next_q(q)]: first frontier half-edge about target, if reached
           for (int h = 0; h < kTileHops && !(r & (kSuccFront | kSuccUnknown)); ++h) r = succ[r];
           if (r & kSuccFront) {
-            nx = r & kSuccIdx;
-            tip = nx == tq;  // barrier tip: next == twin (R4)
+            nx = (int32_t)(r & kSuccIdx);
+            tip = nx == tq[k];  // barrier tip: next == twin (R4)
           } else {
             deferred = true;
+            fr = false;  // the fixup sets every bit of a deferred half-edge
           }
         }
-        if (!deferred) {
-          nx = j_of(nx);
-          __stcs(next + e0 + j, (int32_t)(e0 + nx));
-          nl_j = tip ? -2 : nx;  // -2: a barrier tip (the loop will be split by the repair)
-        } else {
-          fr = sd = false;  // the fixup sets every bit of a deferred half-edge
-        }
+        nl[k] = deferred ? -1 : tip ? -2 : nx;  // -2: a barrier tip (the loop will be split by the repair)
+        packed |= ((uint32_t)fr << k) | ((uint32_t)tip << (4 + k)) | ((uint32_t)deferred << (8 + k));
       }
-      nx_l[j] = (int16_t)nl_j;
+      *reinterpret_cast<uint2*>(nx_q + 4 * t) =
+          make_uint2((uint32_t)(uint16_t)nl[0] | ((uint32_t)(uint16_t)nl[1] << 16), (uint32_t)(uint16_t)nl[2] | 0xFFFF0000u);
     }
-    const uint32_t fw = __ballot_sync(0xffffffffu, fr), sw = __ballot_sync(0xffffffffu, sd);
-    const uint32_t tm = __ballot_sync(0xffffffffu, tip), dm = __ballot_sync(0xffffffffu, deferred),
-                   lm = __ballot_sync(0xffffffffu, left);
-    const int wl = (j - lane) >> 5;  // tile-local word of this warp
-    // one store per lane: lanes 0-5 the shared words Sw, Cw, Wl, Lm, Dm, SDm; lanes 8-11
-    // the global words F0, F1, S, TB (equally spaced in the workspace, bv_stride words)
-    const uint32_t val = (sw & m_s) | (lm & m_l) | (dm & m_d) | (fw & m_f) | (tm & m_t);
-    if (s_off >= 0) {
-      Sw[s_off + wl] = val;
-    } else if (g_lane && (FULL || j - lane < nhe)) {
-      g_word[wl] = val;
+    const int wl0 = (3 * kTileThreads / 32) * i + wl_warp;
+    const uint32_t f0w = word_bits(packed, 0, 0), f1w = word_bits(packed, 1, 0), f2w = word_bits(packed, 2, 0);
+    const uint32_t t0w = word_bits(packed, 0, 1), t1w = word_bits(packed, 1, 1), t2w = word_bits(packed, 2, 1);
+    const uint32_t d0w = word_bits(packed, 0, 2), d1w = word_bits(packed, 1, 2), d2w = word_bits(packed, 2, 2);
+    // lanes 0-11: shared Cw (0), Wl (0), Dm, SDm (0); lanes 12-20: global F0, F1, TB
+    if (lane < 12) {
+      const int r = lane_ty == 0 ? 1 : lane_ty == 1 ? 2 : lane_ty == 2 ? 4 : 5;  // Cw, Wl, Dm, SDm
+      Sw[r * kTileWords + wl0 + lane_m] = lane_ty == 2 ? pick_m(d0w, d1w, d2w) : 0u;
+    } else if (lane < 21 && (FULL || 32 * (wl0 + lane_m) < nhe)) {
+      const int g = lane_ty == 4 ? 0 : lane_ty == 5 ? 1 : 3;  // F0, F1, TB
+      F0[g * bv_stride + (e0 >> 5) + wl0 + lane_m] = lane_ty == 6 ? pick_m(t0w, t1w, t2w) : pick_m(f0w, f1w, f2w);
     }
   }
   __syncthreads();
@@ -568,6 +602,20 @@ __device__ __forceinline__ void tile_body(
     }
   }
 
+  // ---- P5b: next out in half-edge order (coalesced stores; a per-triangle store of three
+  // consecutive ids writes a third of 12 sectors per instruction): nx_q's resolved
+  // successor, twin for a barrier tip, untouched for a deferred half-edge
+  {
+    int q = q_of(tid);
+#pragma unroll 4
+    for (int i = 0; i < kHeIters; ++i, q = q_step(q)) {
+      const int j = tid + i * kTileThreads;
+      if (!FULL && j >= nhe) break;
+      const int32_t nl = nx_q[q];
+      if (nl != -1) __stcs(next + e0 + j, (int32_t)(e0 + j_of(nl == -2 ? tw_s[q] : nl)));
+    }
+  }
+
   // ---- P6: seeds whose polygon closes inside the tile (Alg. 12 + Overwrite seeds,
   // PAPER.md L778-849): land on a frontier half-edge by rotation (the resolved successor
   // chain), walk the loop on nx_l, keep the minimum id and the length.  Loops that touch
@@ -586,19 +634,20 @@ __device__ __forceinline__ void tile_body(
       for (int h = 0; h < kTileHops && !(r & (kSuccFront | kSuccUnknown)); ++h) r = succ[r];
       bool ok = (r & kSuccFront) != 0, tipped = false;
       const bool landed = ok;
-      int32_t mn = 0, n = 0, x = sj;
+      int32_t mn = 0, n = 0, x = 0;  // quad indices (the same order as half-edge ids)
       if (ok) {
-        x = j_of(r & kSuccIdx);
+        x = r & kSuccIdx;
         int32_t y = x;
         mn = x;
         do {
           mn = min(mn, y);
           ++n;
-          y = nx_l[y];
+          y = nx_q[y];
           if (y < 0 || n > kP6MaxLen) { ok = false; tipped = y == -2; break; }  // deferred / barrier-tip / long loop
         } while (y != x);
       }
       if (ok) {
+        mn = j_of(mn);
         len[e0 + mn] = n;
         const uint32_t bit = 1u << (mn & 31);
         if (!(atomicOr(&Cw[mn >> 5], bit) & bit)) atomicAdd(&Wl[mn >> 5], n);  // first setter only
@@ -608,7 +657,7 @@ __device__ __forceinline__ void tile_body(
         // The global walk starts from the frontier half-edge the seed landed on when the
         // landing stayed in the tile (the same loop: F1 adds frontier edges only to
         // repaired loops, whose pieces the middle-edge halves seed anyway), else from the seed.
-        const int32_t g = landed ? x : sj;
+        const int32_t g = landed ? j_of(x) : sj;
         atomicOr(&SDm[g >> 5], 1u << (g & 31));
       }
     }

@@ -10,12 +10,14 @@ sys.path.insert(0, ROOT)
 import numpy as np  # noqa
 import torch  # noqa
 
-so = "/tmp/libpolylla_phase.so"
-csrc = os.path.join(ROOT, "paper_2403_14723_b200", "csrc")
+so = "/tmp/libpolylla_phase%s.so" % os.getpid()
+# POLYLLA_SRC: another source tree (A/B against an older commit: git archive ... | tar -x -C DIR)
+SRC = os.environ.get("POLYLLA_SRC", ROOT)
+csrc = os.path.join(SRC, "paper_2403_14723_b200", "csrc")
 cu = [os.path.join(csrc, f) for f in sorted(os.listdir(csrc)) if f.endswith(".cu")]
 subprocess.run(["nvcc", "-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17", "-fmad=false",
                 "-DPOLYLLA_PHASE_TIMING", "-Xcompiler", "-fPIC,-fvisibility=hidden", "-shared", "-I",
-                os.path.join(ROOT, "include"), "-o", so, *cu], check=True)
+                os.path.join(SRC, "include"), "-o", so, *cu], check=True)
 from paper_2403_14723_b200 import polylla as pp  # noqa
 pp.LIB_PATH = so
 L = pp.lib()
