@@ -11,8 +11,13 @@
  * the caller's workspace and launches kernels.
  *
  * Conventions (readings R1-R18):
- *   - indices are int32, 0-based; coordinates are float64 interleaved
- *     (x0,y0,x1,y1,...) = a contiguous torch.float64 tensor [V,2];
+ *   - indices are 0-based; vertex ids (tri, origin, loops) are int32 (V <= 2^31 - 1);
+ *     half-edge ids (twin, next, prev, seeds) and CSR offsets are UNSIGNED 32-bit, so
+ *     a mesh may have up to H = 2^32 - 2 half-edges (the capacity question of PAPER.md
+ *     L55: twice the int32 ceiling).  For H <= 2^31 - 1 the
+ *     arrays read identically as int32 (the int32 reading of every earlier version);
+ *   - coordinates are float64 interleaved (x0,y0,x1,y1,...) = a contiguous
+ *     torch.float64 tensor [V,2];
  *   - interior half-edge e = 3f+k has origin tri'[f][k] and target tri'[f][(k+1)%3],
  *     where tri' is the input triangle re-oriented CCW (a CW triangle has its 2nd and
  *     3rd vertex swapped, R10); next_in(e) = 3f+(k+1)%3;
@@ -66,8 +71,8 @@ typedef enum {
   POLYLLA_E_DEGENERATE_TRI = -3,      /* zero signed area or repeated vertex */
   POLYLLA_E_NON_MANIFOLD_EDGE = -4,   /* an edge in > 2 triangles, or twice in one direction */
   POLYLLA_E_NON_MANIFOLD_VERTEX = -5, /* a vertex with > 1 outgoing border half-edge (border chain ambiguous) */
-  POLYLLA_E_INDEX_OVERFLOW = -6,      /* 3T + B > INT32_MAX */
-  POLYLLA_E_WORKSPACE = -7,           /* workspace too small or not 256-byte aligned */
+  POLYLLA_E_INDEX_OVERFLOW = -6,      /* 3T + max_border > 2^32 - 2, or V > INT32_MAX */
+  POLYLLA_E_WORKSPACE = -7,           /* workspace too small or not 256-byte aligned; or (device) B > max_border */
   POLYLLA_E_WALK_BOUND = -8,          /* SPEC.md L160/L174/L260: a rotation or loop walk did not close */
   POLYLLA_E_UNSEEDED_LOOP = -9,       /* sum of loop lengths != #interior frontier half-edges (exact-tie Lepp cycle, R12) */
   POLYLLA_E_CALL_ORDER = -10,
@@ -96,6 +101,19 @@ typedef struct {
  * (worst case B = 3T; includes staging for polylla_run_host).  Host-only. */
 POLYLLA_API size_t polylla_workspace_bytes(int64_t n_vertices, int64_t n_triangles);
 
+/* Workspace flags. */
+#define POLYLLA_WS_STAGING 1u /* hold the host-buffer staging regions of polylla_run_host */
+
+/* Bytes of device workspace for a mesh with at most max_border border half-edges
+ * (0 <= max_border <= 3T; e.g. 4(s-1) for an s x s grid) and, with POLYLLA_WS_STAGING in
+ * flags, run_host's staging.  polylla_workspace_bytes(V, T) ==
+ * polylla_workspace_bytes_ex(V, T, 3T, POLYLLA_WS_STAGING).  The origin/twin/next
+ * regions shrink from 6T to 3T + max_border entries and the staging (12T + 12T + 16V
+ * bytes) is dropped: the capacity path for meshes near the HBM limit (SURVEY.md §8(f)
+ * NEXT-3).  Returns 0 on invalid arguments.  Host-only. */
+POLYLLA_API size_t polylla_workspace_bytes_ex(int64_t n_vertices, int64_t n_triangles, int64_t max_border,
+                                              uint32_t flags);
+
 /* Half-edge construction (SPEC.md L45-53 build_from_triangles),
  * moved on-device, fused with the longest-edge labelling of Alg. 2 / Alg. 7
  * (PAPER.md L351-376, L608-635):
@@ -110,6 +128,16 @@ POLYLLA_API polylla_status polylla_build_halfedges(const double* xy, int64_t n_v
                                                    int64_t n_triangles, void* workspace, size_t workspace_bytes,
                                                    polylla_stream stream, polylla_ctx** ctx_out);
 
+/* polylla_build_halfedges over a workspace laid out by polylla_workspace_bytes_ex with
+ * the same max_border and flags (the layout must match).  A mesh with more than
+ * max_border border half-edges sets POLYLLA_E_WORKSPACE in the device status (returned
+ * by polylla_get_counts); nothing is written past the bound.
+ * polylla_build_halfedges(...) == polylla_build_halfedges_ex(..., 3T, POLYLLA_WS_STAGING, ...). */
+POLYLLA_API polylla_status polylla_build_halfedges_ex(const double* xy, int64_t n_vertices, const int32_t* tri,
+                                                      int64_t n_triangles, int64_t max_border, uint32_t flags,
+                                                      void* workspace, size_t workspace_bytes, polylla_stream stream,
+                                                      polylla_ctx** ctx_out);
+
 /* Exact non-manifold-edge check (SPEC.md L49 NonManifoldEdge), opt-in.  The build
  * detects an edge in more than two triangles (or twice in one direction) when all of
  * its copies fall in one 2,048-triangle build tile or all of them cross tiles; a copy
@@ -119,7 +147,8 @@ POLYLLA_API polylla_status polylla_build_halfedges(const double* xy, int64_t n_v
  * copy, ORs POLYLLA_E_NON_MANIFOLD_EDGE into the device status (returned by the next
  * polylla_get_counts).  Call after polylla_build_halfedges and before
  * polylla_get_triangle_polygons / a host-pointer prev (which reuse the same scratch);
- * asynchronous (2 launches). */
+ * asynchronous (2 launches).  Needs 3T + max_border <= INT32_MAX (else
+ * POLYLLA_E_INDEX_OVERFLOW): its slots carry a flag bit next to the half-edge id. */
 POLYLLA_API polylla_status polylla_check_manifold(polylla_ctx* ctx, polylla_stream stream);
 
 /* Label phase (Alg. 8-9): frontier bits F[e] = border(e) or
@@ -147,7 +176,8 @@ POLYLLA_API polylla_status polylla_generate(polylla_ctx* ctx, polylla_stream str
  * seeds (per seed), then Scan and compact, one thread per element.
  * Same results as the default path, bit for bit.  Call after polylla_build_halfedges
  * (stage 1); afterwards get_counts / get_polygons as usual (get_triangle_polygons and
- * get_triangle_regions too).  Asynchronous (~14 launches and memsets). */
+ * get_triangle_regions too).  Asynchronous (~14 launches and memsets).  Needs
+ * 3T + max_border <= INT32_MAX (else POLYLLA_E_INDEX_OVERFLOW). */
 POLYLLA_API polylla_status polylla_label_generate_paper(polylla_ctx* ctx, polylla_stream stream);
 
 /* Synchronises `stream` and returns the counts and the device status.  The return
@@ -166,9 +196,9 @@ POLYLLA_API polylla_status polylla_get_counts(polylla_ctx* ctx, polylla_stream s
  * device memory, else into workspace scratch that is then copied out).  offsets and
  * loops are both given or both NULL.  Asynchronous; a too-small capacity sets
  * POLYLLA_E_CAPACITY in the device status. */
-POLYLLA_API polylla_status polylla_get_polygons(polylla_ctx* ctx, int32_t* offsets, int64_t offsets_cap,
-                                                int32_t* loops, int64_t loops_cap, int32_t* origin, int32_t* twin,
-                                                int32_t* next, int32_t* prev, polylla_stream stream);
+POLYLLA_API polylla_status polylla_get_polygons(polylla_ctx* ctx, uint32_t* offsets, int64_t offsets_cap,
+                                                int32_t* loops, int64_t loops_cap, int32_t* origin, uint32_t* twin,
+                                                uint32_t* next, uint32_t* prev, polylla_stream stream);
 
 /* Per-triangle polygon ids (the output polygons as unions of triangles: the terminal-edge
  * regions of PAPER.md L76-L128 after the barrier repair):
@@ -205,32 +235,33 @@ POLYLLA_API polylla_status polylla_get_triangle_regions(polylla_ctx* ctx, int32_
  * polylla_get_polygons). */
 typedef struct {
   const int32_t* origin;
-  const int32_t* twin;
-  const int32_t* next;
+  const uint32_t* twin;
+  const uint32_t* next;
   const uint8_t* lcode;
   const uint32_t* frontier0;
   const uint32_t* frontier1;
   const uint32_t* seed_bits;
-  const int32_t* seeds;
-  const int32_t* tips;  /* [n_tips] incoming frontier half-edge of each barrier tip (unordered) */
+  const uint32_t* seeds;
+  const uint32_t* tips;  /* [n_tips] incoming frontier half-edge of each barrier tip (unordered) */
 } polylla_views;
 POLYLLA_API polylla_status polylla_get_views(polylla_ctx* ctx, polylla_views* views);
 
 /* Debug: when next_pre (device [H]) is non-NULL, polylla_generate first copies the
  * pre-repair next array into it (stage-wise parity tests). */
-POLYLLA_API polylla_status polylla_set_debug(polylla_ctx* ctx, int32_t* next_pre);
+POLYLLA_API polylla_status polylla_set_debug(polylla_ctx* ctx, uint32_t* next_pre);
 
 /* End to end from HOST buffers (pageable or pinned): H2D of xy/tri into the
  * workspace, build -> label -> generate, one sync, extraction, D2H of the CSR
  * (offsets [P+1], loops [L]) and, if non-NULL, origin/twin/next [H] -- all on
  * `stream`, synchronised before returning.  Host capacities as in get_polygons
  * (origin/twin/next need n_halfedges <= 6T entries).  *counts receives the counts.
- * The ctx is destroyed before returning. */
+ * The workspace is laid out by polylla_workspace_bytes (staging included).  The ctx is
+ * destroyed before returning. */
 POLYLLA_API polylla_status polylla_run_host(const double* xy_host, int64_t n_vertices, const int32_t* tri_host,
                                             int64_t n_triangles, void* workspace, size_t workspace_bytes,
-                                            int32_t* offsets_host, int64_t offsets_cap, int32_t* loops_host,
-                                            int64_t loops_cap, int32_t* origin_host, int32_t* twin_host,
-                                            int32_t* next_host, int64_t halfedge_cap, polylla_counts* counts,
+                                            uint32_t* offsets_host, int64_t offsets_cap, int32_t* loops_host,
+                                            int64_t loops_cap, int32_t* origin_host, uint32_t* twin_host,
+                                            uint32_t* next_host, int64_t halfedge_cap, polylla_counts* counts,
                                             polylla_stream stream);
 
 POLYLLA_API void polylla_destroy(polylla_ctx* ctx);

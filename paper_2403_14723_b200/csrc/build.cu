@@ -62,7 +62,8 @@ constexpr size_t kOffTw = kTileQ * 4, kOffSlot = kOffTw + kTileQ * 2, kOffLc = k
                  kNxBytes = kTileQ * 2 + 6 * (kTileHE / 8),                    // P4-P6 arrays (20,992 B)
                  kTileSmem = kOffNx + kNxBytes;                                // 104,960 B -> 2 CTAs/SM
 static_assert(2 * (kTileSmem + 1024) <= 228 * 1024, "two tiles per SM");
-constexpr unsigned long long kLeftDown = 1ull << 63;  // leftover key: set if origin > target
+constexpr unsigned long long kLeftDown = 1ull << 63;    // leftover key: set if origin > target
+constexpr unsigned long long kLeftPaired = 1ull << 31;  // leftover key: set once the key's slot holder is paired
 constexpr uint32_t kEmpty16 = 0xFFFFu;             // empty 16-bit slot (quad indices are < 8192)
 // rotation successors (P3/P4): quad index in the low 13 bits, terminal flags above
 constexpr uint16_t kSuccIdx = 0x1FFF, kSuccFront = 0x4000, kSuccUnknown = 0x8000;
@@ -214,10 +215,10 @@ __device__ __forceinline__ bool tri_ok(int i, int t, int nt) {
 template <bool FULL>
 __device__ __forceinline__ void tile_body(
     unsigned char* smem_tile, const double2* __restrict__ xy, const int32_t* __restrict__ tri, int64_t V, int64_t T,
-    int32_t* __restrict__ origin, int32_t* __restrict__ twin, int32_t* __restrict__ next, uint8_t* __restrict__ lcode,
+    int32_t* __restrict__ origin, hid* __restrict__ twin, hid* __restrict__ next, uint8_t* __restrict__ lcode,
     uint32_t* __restrict__ F0, int64_t bv_stride, uint32_t* __restrict__ C,
     int32_t* __restrict__ len, int32_t* __restrict__ wlen, unsigned long long* __restrict__ left_key,
-    int32_t* __restrict__ left_e, int32_t* __restrict__ def_e, uint32_t* __restrict__ SDB,
+    hid* __restrict__ left_e, hid* __restrict__ def_e, uint32_t* __restrict__ SDB,
     int32_t* __restrict__ cnt_ld, DevCounters* ctr, int64_t tile, int64_t tile_next) {
   int32_t* tri_q = reinterpret_cast<int32_t*>(smem_tile);
   int4* tri_q4 = reinterpret_cast<int4*>(smem_tile);
@@ -464,7 +465,7 @@ __device__ __forceinline__ void tile_body(
         const int32_t lt = lc_s[tqs >> 2];
         if (tq >= 0 && back != q) nm = ST_NONMANIFOLD_EDGE;  // twin claimed twice (edge in > 2 triangles)
         __stcs(origin + e0 + j, org);
-        __stcs(twin + e0 + j, tq >= 0 ? (int32_t)(e0 + j_of(tq)) : -1);
+        __stcs(twin + e0 + j, tq >= 0 ? (hid)(e0 + j_of(tq)) : kNoHe);
         const bool front = lq != k && lt != (tq & 3);  // neither half the longest edge of its triangle
         succ[q] = (uint16_t)(tq < 0 ? (q | kSuccUnknown) : front ? (q | kSuccFront) : next_q(tq));
         sd = tq >= 0 && lq == k && lt == (tq & 3) && q < tq;  // terminal edge, smaller id
@@ -586,7 +587,7 @@ __device__ __forceinline__ void tile_body(
       if (bl + il) atomicAdd(&ctr->n_left, bl + il);  // totals (result unused: a reduction)
       if (bd + id) atomicAdd(&ctr->n_def, bd + id);
     }
-    int pl = (int)e0 + bl + il - cl, pd = (int)e0 + bd + id - cd;
+    int64_t pl = e0 + bl + il - cl, pd = e0 + bd + id - cd;
     while (lw) {
       const int j = tid * 32 + __ffs(lw) - 1;
       lw &= lw - 1;
@@ -594,10 +595,10 @@ __device__ __forceinline__ void tile_body(
       const int32_t o = tri_q[q], tg = tri_q[q + 1];
       const uint64_t lo = (uint32_t)min(o, tg), hi = (uint32_t)max(o, tg);
       left_key[pl] = (lo << 32) | hi | (o > tg ? kLeftDown : 0ull);  // undirected key + direction bit
-      left_e[pl++] = (int32_t)(e0 + j);
+      left_e[pl++] = (hid)(e0 + j);
     }
     while (dw) {
-      def_e[pd++] = (int32_t)(e0 + tid * 32 + __ffs(dw) - 1);
+      def_e[pd++] = (hid)(e0 + tid * 32 + __ffs(dw) - 1);
       dw &= dw - 1;
     }
   }
@@ -612,7 +613,7 @@ __device__ __forceinline__ void tile_body(
       const int j = tid + i * kTileThreads;
       if (!FULL && j >= nhe) break;
       const int32_t nl = nx_q[q];
-      if (nl != -1) __stcs(next + e0 + j, (int32_t)(e0 + j_of(nl == -2 ? tw_s[q] : nl)));
+      if (nl != -1) __stcs(next + e0 + j, (hid)(e0 + j_of(nl == -2 ? tw_s[q] : nl)));
     }
   }
 
@@ -678,9 +679,9 @@ __device__ __forceinline__ void tile_body(
 // body (constant trip counts, no bounds checks), the ragged last tile the generic one.
 __global__ void __launch_bounds__(kTileThreads, 2)
     k_tile(const double2* __restrict__ xy, const int32_t* __restrict__ tri, int64_t V, int64_t T,
-           int32_t* __restrict__ origin, int32_t* __restrict__ twin, int32_t* __restrict__ next,
+           int32_t* __restrict__ origin, hid* __restrict__ twin, hid* __restrict__ next,
            uint8_t* __restrict__ lcode, uint32_t* __restrict__ F0, int64_t bv_stride, uint32_t* __restrict__ C, int32_t* __restrict__ len, int32_t* __restrict__ wlen,
-           unsigned long long* __restrict__ left_key, int32_t* __restrict__ left_e, int32_t* __restrict__ def_e,
+           unsigned long long* __restrict__ left_key, hid* __restrict__ left_e, hid* __restrict__ def_e,
            uint32_t* __restrict__ SDB, int32_t* __restrict__ cnt_ld, DevCounters* ctr,
            int64_t prefetch_dist, int64_t tile_base) {
   extern __shared__ __align__(16) unsigned char smem_tile[];
@@ -710,7 +711,7 @@ extern "C" __attribute__((visibility("default"))) int polylla_debug_phase_cycles
 }
 #endif
 
-__device__ __forceinline__ uint64_t hash_cap_for(int32_t n) {
+__device__ __forceinline__ uint64_t hash_cap_for(uint32_t n) {
   uint64_t c = 1024;
   while (c < 2ull * (uint64_t)n) c <<= 1;
   return c;
@@ -751,19 +752,19 @@ __device__ __forceinline__ uint32_t left_home(uint32_t lo, uint32_t hi, unsigned
   return ((uint32_t)(((unsigned long long)lo * scale) >> 32) + ((hi * 0x9E3779B1u) >> 30)) & mask;
 }
 __global__ void k_left_insert(DevCounters* ctr, int64_t ntiles, const int32_t* __restrict__ cnt_ld,
-                              const unsigned long long* __restrict__ left_key, const int32_t* __restrict__ left_e,
-                              int32_t* twin, uint32_t* ehash) {
+                              unsigned long long* left_key, const hid* __restrict__ left_e,
+                              hid* twin, uint32_t* ehash) {
   if (ctr->status) return;
   const uint32_t mask = (uint32_t)ctr->hash_cap - 1;
   const unsigned long long scale = ctr->hash_scale;
   for (int64_t it = blockIdx.x; it < ntiles; it += gridDim.x) {
     const int64_t tile = sched_tile(it, ntiles);
     const int32_t n = cnt_ld[2 * tile];
-    const int32_t base = (int32_t)(3 * kTileTris * tile);
+    const int64_t base = 3 * kTileTris * tile;
     for (int32_t k = threadIdx.x; k < n; k += blockDim.x) {
-      const int32_t i = base + k;
+      const int64_t i = base + k;  // < 3T <= 2^32 - 2: a slot value never equals kEmpty
       const unsigned long long kd = left_key[i], key = kd & ~kLeftDown;
-      const int32_t ei = left_e[i];
+      const hid ei = left_e[i];
       uint32_t h = left_home((uint32_t)(key >> 32), (uint32_t)key, scale, mask);
       for (uint32_t probe = 0; probe <= mask; ++probe) {
         uint32_t s = ehash[h];
@@ -772,15 +773,16 @@ __global__ void k_left_insert(DevCounters* ctr, int64_t ntiles, const int32_t* _
           if (old == kEmpty) break;
           s = old;
         }
-        const int32_t si = (int32_t)(s & ~kPaired);
-        const unsigned long long sd = left_key[si];
-        if ((sd & ~kLeftDown) == key) {
-          const int32_t es = left_e[si];
-          // a pair must run in opposite directions; a third copy finds the slot paired
-          if ((s & kPaired) || sd == kd || atomicCAS(&ehash[h], s, s | kPaired) != s) {
+        const unsigned long long sd = left_key[s];
+        if ((sd & ~(kLeftDown | kLeftPaired)) == key) {
+          // a pair must run in opposite directions; the pairing is claimed on the slot
+          // holder's key (bit 31: vertex ids < 2^31), so a third copy finds it taken
+          if (((sd ^ kd) & kLeftDown) == 0 || (sd & kLeftPaired) ||
+              atomicCAS(left_key + s, sd, sd | kLeftPaired) != sd) {
             raise_status(ctr, ST_NONMANIFOLD_EDGE);
             break;
           }
+          const hid es = left_e[s];
           twin[ei] = es;
           twin[es] = ei;
           break;
@@ -805,20 +807,20 @@ constexpr int kSegThreads = 256;
 
 __global__ void __launch_bounds__(kSegThreads)
     k_border_rank(DevCounters* ctr, int64_t ntiles, const int32_t* __restrict__ cnt_ld,
-                  const int32_t* __restrict__ left_e, const int32_t* __restrict__ twin, int32_t* __restrict__ blist,
-                  int32_t* __restrict__ bcnt) {
+                  const hid* __restrict__ left_e, const hid* __restrict__ twin, hid* __restrict__ blist,
+                  uint32_t* __restrict__ bcnt) {
   __shared__ int32_t wtot[kSegThreads / 32];
   if (ctr->status) return;
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   for (int64_t it = blockIdx.x; it < ntiles; it += gridDim.x) {
     const int64_t tile = sched_tile(it, ntiles);
     const int32_t n = cnt_ld[2 * tile];
-    const int32_t base = (int32_t)(3 * kTileTris * tile);
+    const int64_t base = 3 * kTileTris * tile;
     int carry = 0;
     for (int32_t k0 = 0; k0 < n; k0 += kSegThreads) {  // block-uniform trip count
       const int32_t k = k0 + threadIdx.x;
-      const int32_t e = k < n ? left_e[base + k] : -1;
-      const bool un = e >= 0 && twin[e] < 0;
+      const hid e = k < n ? left_e[base + k] : kNoHe;
+      const bool un = e != kNoHe && twin[e] == kNoHe;
       const uint32_t m = __ballot_sync(0xffffffffu, un);
       if (lane == 0) wtot[wid] = __popc(m);
       __syncthreads();
@@ -831,67 +833,69 @@ __global__ void __launch_bounds__(kSegThreads)
       carry += tot;
       __syncthreads();
     }
-    if (threadIdx.x == 0) bcnt[tile] = carry;
+    if (threadIdx.x == 0) bcnt[tile] = (uint32_t)carry;
   }
 }
 
 constexpr int kBorderScanThreads = 1024;
 __global__ void __launch_bounds__(kBorderScanThreads)
-    k_border_scan(DevCounters* ctr, int64_t ntiles, int64_t T3, int32_t* bcnt) {
+    k_border_scan(DevCounters* ctr, int64_t ntiles, int64_t T3, int64_t Bmax, uint32_t* bcnt) {
   constexpr int NW = kBorderScanThreads / 32;
-  __shared__ int32_t wsum[NW];
+  __shared__ long long wsum[NW];
   if (ctr->status) return;
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
   const int64_t per = ((ntiles + NW - 1) / NW + 31) & ~int64_t(31);
   const int64_t t0 = wid * per, t1 = t0 + per < ntiles ? t0 + per : ntiles;
-  int sum = 0;
+  long long sum = 0;
   for (int64_t t = t0 + lane; t < t1; t += 32) sum += bcnt[t];
-  sum = __reduce_add_sync(0xffffffffu, sum);
+#pragma unroll
+  for (int o = 16; o; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
   if (lane == 0) wsum[wid] = sum;
   __syncthreads();
   if (wid == 0) {
-    const int v = wsum[lane];
-    int inc = v;
+    const long long v = wsum[lane];
+    long long inc = v;
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
-      const int a = __shfl_up_sync(0xffffffffu, inc, o);
+      const long long a = __shfl_up_sync(0xffffffffu, inc, o);
       if (lane >= o) inc += a;
     }
     wsum[lane] = inc - v;
     if (lane == 31) {
-      if (T3 + inc > 0x7fffffffLL) raise_status(ctr, ST_OVERFLOW);
-      ctr->n_border = inc;
+      if (T3 + inc > kMaxHalfedges) raise_status(ctr, ST_OVERFLOW);
+      else if (inc > Bmax) raise_status(ctr, ST_BORDER_CAP);  // nothing is written past 3T + Bmax
+      ctr->n_border = (uint32_t)inc;
     }
   }
   __syncthreads();
-  int carry = wsum[wid];
+  long long carry = wsum[wid];
   for (int64_t tb0 = t0; tb0 < t1; tb0 += 32) {
     const int64_t t = tb0 + lane;
-    const int v = t < t1 ? bcnt[t] : 0;
-    int inc = v;
+    const long long v = t < t1 ? bcnt[t] : 0;
+    long long inc = v;
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
-      const int a = __shfl_up_sync(0xffffffffu, inc, o);
+      const long long a = __shfl_up_sync(0xffffffffu, inc, o);
       if (lane >= o) inc += a;
     }
-    if (t < t1) bcnt[t] = carry + inc - v;  // in place: the exclusive base of the tile
+    if (t < t1) bcnt[t] = (uint32_t)(carry + inc - v);  // in place: the exclusive base of the tile
     carry += __shfl_sync(0xffffffffu, inc, 31);
   }
 }
 
 __global__ void __launch_bounds__(kSegThreads)
-    k_border_emit(DevCounters* ctr, int64_t ntiles, int64_t T3, const int32_t* __restrict__ blist,
-                  const int32_t* __restrict__ bbase, int32_t* origin, int32_t* twin, int32_t* vmap) {
+    k_border_emit(DevCounters* ctr, int64_t ntiles, int64_t T3, const hid* __restrict__ blist,
+                  const uint32_t* __restrict__ bbase, int32_t* origin, hid* twin, hid* vmap) {
   if (ctr->status) return;
-  const int32_t nb = ctr->n_border;
+  const uint32_t nb = ctr->n_border;
   for (int64_t it = blockIdx.x; it < ntiles; it += gridDim.x) {
     const int64_t tile = sched_tile(it, ntiles);
-    const int32_t b0 = bbase[tile];
-    const int32_t n = (tile + 1 < ntiles ? bbase[tile + 1] : nb) - b0;
-    const int32_t base = (int32_t)(3 * kTileTris * tile);
+    const uint32_t b0 = bbase[tile];
+    const int32_t n = (int32_t)((tile + 1 < ntiles ? bbase[tile + 1] : nb) - b0);
+    const int64_t base = 3 * kTileTris * tile;
     for (int32_t k = threadIdx.x; k < n; k += kSegThreads) {
-      const int32_t e = blist[base + k];
-      const int32_t b = (int32_t)(T3 + b0 + k);
+      const hid e = blist[base + k];
+      const hid b = (hid)(T3 + b0 + k);
       const int32_t v = origin[next_in(e)];  // origin(b) = target(e)
       twin[e] = b;
       twin[b] = e;
@@ -905,16 +909,16 @@ __global__ void __launch_bounds__(kSegThreads)
 // with two outgoing border half-edges keeps only one of them in vmap: the other fails
 // the vmap[origin(b)] == b check (NON_MANIFOLD_VERTEX).
 __global__ void k_border_next(DevCounters* ctr, int64_t T3, const int32_t* __restrict__ origin,
-                              const int32_t* __restrict__ twin, const int32_t* __restrict__ vmap, int32_t* next) {
+                              const hid* __restrict__ twin, const hid* __restrict__ vmap, hid* next) {
   if (ctr->status) return;
-  const int32_t nb = ctr->n_border;
-  for (int32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < nb; i += gridDim.x * blockDim.x) {
-    const int32_t b = (int32_t)(T3 + i);
+  const uint32_t nb = ctr->n_border;
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < nb; i += gridDim.x * blockDim.x) {
+    const hid b = (hid)(T3 + i);
     const int32_t v = origin[twin[b]];
-    const int32_t nx = vmap[v];
+    const hid nx = vmap[v];
     const bool ok = vmap[origin[b]] == b && nx >= T3 && nx - T3 < nb && origin[nx] == v;
     if (!ok) raise_status(ctr, ST_NONMANIFOLD_VERTEX);
-    next[b] = ok ? nx : -1;
+    next[b] = ok ? nx : kNoHe;
   }
 }
 
@@ -991,18 +995,19 @@ int launch_build_rest(Ctx* c, cudaStream_t s) {
   const int64_t tiles = (c->T + kTileTris - 1) / kTileTris;
   const int grid = 148 * 32;  // enough threads for ~1 leftover each on 10M-vertex meshes (latency-bound)
   prof_mark(s, "k_left_match");
-  k_hash_clear<<<grid, 256, 0, s>>>(c->ctr, c->ehash, c->hash_cap_max, c->V, c->T);
+  uint32_t* ehash = static_cast<uint32_t*>(c->ehash);
+  k_hash_clear<<<grid, 256, 0, s>>>(c->ctr, ehash, c->hash_cap_max, c->V, c->T);
 #ifndef POLYLLA_LEFT_THREADS
 #define POLYLLA_LEFT_THREADS 256  // 128 / 256 / 384 / 512 measured: 128-256 best
 #endif
   const unsigned seg_grid = (unsigned)(tiles < 148 * 16 ? tiles : 148 * 16);
   const unsigned left_grid = (unsigned)(tiles < 148 * (4096 / POLYLLA_LEFT_THREADS) ? tiles : 148 * (4096 / POLYLLA_LEFT_THREADS));
-  k_left_insert<<<left_grid, POLYLLA_LEFT_THREADS, 0, s>>>(c->ctr, tiles, c->cnt_ld, c->left_key, c->left_e, c->twin, c->ehash);
-  int32_t* blist = reinterpret_cast<int32_t*>(c->left_key);  // dead after k_left_insert
+  k_left_insert<<<left_grid, POLYLLA_LEFT_THREADS, 0, s>>>(c->ctr, tiles, c->cnt_ld, c->left_key, c->left_e, c->twin, ehash);
+  hid* blist = reinterpret_cast<hid*>(c->left_key);  // dead after k_left_insert
   k_border_rank<<<seg_grid, kSegThreads, 0, s>>>(c->ctr, tiles, c->cnt_ld, c->left_e, c->twin, blist, c->bcnt);
   n += 3;
   prof_mark(s, "k_border_scan");
-  k_border_scan<<<1, kBorderScanThreads, 0, s>>>(c->ctr, tiles, 3 * c->T, c->bcnt);
+  k_border_scan<<<1, kBorderScanThreads, 0, s>>>(c->ctr, tiles, 3 * c->T, c->Bmax, c->bcnt);
   k_border_emit<<<seg_grid, kSegThreads, 0, s>>>(c->ctr, tiles, 3 * c->T, blist, c->bcnt, c->origin, c->twin,
                                                  c->vmap);
   n += 2;

@@ -25,9 +25,10 @@ struct Layout {
   size_t total;
 };
 
-// region order; sizes in bytes
-static Layout layout(int64_t V, int64_t T) {
-  const int64_t Hmax = 6 * T;
+// region order; sizes in bytes.  Hmax = 3T + Bmax (the caller's bound on the border
+// half-edges; 3T covers every mesh); the run_host staging regions only when `staging`.
+static Layout layout(int64_t V, int64_t T, int64_t Bmax, bool staging) {
+  const int64_t Hmax = 3 * T + Bmax;
   const int64_t nw = (3 * T + 31) / 32;
   const int64_t nb = (nw + 2047) / 2048 + 1;
   const int64_t cap = hash_cap_max_for(T);
@@ -49,15 +50,15 @@ static Layout layout(int64_t V, int64_t T) {
       0,                      // 14 (unused)
       (size_t)V * 4,          // 15 tips
       (size_t)(2 * V) * 4,    // 16 aff
-      (size_t)(2 * V) * 4,    // 17 mids
+      0,                      // 17 (unused)
       (size_t)nb * 8,         // 18 scan_a
       (size_t)nb * 8,         // 19 scan_b
       (size_t)nb * 8,         // 20 scan_c
       (size_t)T * 4,          // 21 seeds
       (size_t)(T + 1) * 4,    // 22 offsets
-      (size_t)(3 * T) * 4,    // 23 loops staging
-      (size_t)(2 * V) * 8,    // 24 xy staging
-      (size_t)(3 * T) * 4,    // 25 tri staging
+      staging ? (size_t)(3 * T) * 4 : 0,  // 23 loops staging (run_host)
+      staging ? (size_t)(2 * V) * 8 : 0,  // 24 xy staging
+      staging ? (size_t)(3 * T) * 4 : 0,  // 25 tri staging
       sizeof(DevCounters),    // 26 counters
       (size_t)(3 * T) * 4,    // 27 deferred half-edges
       (size_t)nw * 4,         // 28 SDB: seeds for the global seed walk
@@ -78,46 +79,46 @@ static Layout layout(int64_t V, int64_t T) {
   return L;
 }
 
-size_t workspace_bytes(int64_t V, int64_t T) { return layout(V, T).total; }
+size_t workspace_bytes(int64_t V, int64_t T, int64_t Bmax, bool staging) { return layout(V, T, Bmax, staging).total; }
 
 bool carve(Ctx* c, void* ws, size_t bytes) {
-  const Layout L = layout(c->V, c->T);
+  const Layout L = layout(c->V, c->T, c->Bmax, c->staging);
   if (bytes < L.total || (reinterpret_cast<uintptr_t>(ws) & 255)) return false;
   char* b = static_cast<char*>(ws);
-  c->Hmax = 6 * c->T;
+  c->Hmax = 3 * c->T + c->Bmax;
   c->origin = reinterpret_cast<int32_t*>(b + L.off[0]);
-  c->twin = reinterpret_cast<int32_t*>(b + L.off[1]);
-  c->next = reinterpret_cast<int32_t*>(b + L.off[2]);
+  c->twin = reinterpret_cast<hid*>(b + L.off[1]);
+  c->next = reinterpret_cast<hid*>(b + L.off[2]);
   c->lcode = reinterpret_cast<uint8_t*>(b + L.off[3]);
   c->F0 = reinterpret_cast<uint32_t*>(b + L.off[4]);
   c->F1 = reinterpret_cast<uint32_t*>(b + L.off[5]);
   c->S = reinterpret_cast<uint32_t*>(b + L.off[6]);
   c->TB = reinterpret_cast<uint32_t*>(b + L.off[7]);
-  c->bcnt = reinterpret_cast<int32_t*>(b + L.off[8]);
+  c->bcnt = reinterpret_cast<uint32_t*>(b + L.off[8]);
   c->len = reinterpret_cast<int32_t*>(b + L.off[9]);
   c->left_key = reinterpret_cast<unsigned long long*>(b + L.off[10]);
-  c->left_e = reinterpret_cast<int32_t*>(b + L.off[11]);
-  c->ehash = reinterpret_cast<uint32_t*>(b + L.off[12]);
-  c->vmap = reinterpret_cast<int32_t*>(b + L.off[13]);
+  c->left_e = reinterpret_cast<hid*>(b + L.off[11]);
+  c->ehash = b + L.off[12];
+  c->vmap = reinterpret_cast<hid*>(b + L.off[13]);
   c->hash_cap_max = hash_cap_max_for(c->T);
-  c->tips = reinterpret_cast<int32_t*>(b + L.off[15]);
-  c->aff = reinterpret_cast<int32_t*>(b + L.off[16]);
-  c->mids = reinterpret_cast<int32_t*>(b + L.off[17]);
+  c->tips = reinterpret_cast<hid*>(b + L.off[15]);
+  c->aff = reinterpret_cast<hid*>(b + L.off[16]);
+  c->mids = nullptr;
   c->scan_a = reinterpret_cast<long long*>(b + L.off[18]);
   c->scan_b = reinterpret_cast<long long*>(b + L.off[19]);
   c->scan_c = reinterpret_cast<long long*>(b + L.off[20]);
-  c->seeds = reinterpret_cast<int32_t*>(b + L.off[21]);
-  c->offsets = reinterpret_cast<int32_t*>(b + L.off[22]);
-  c->loops = reinterpret_cast<int32_t*>(b + L.off[23]);
-  c->xy_stage = reinterpret_cast<double*>(b + L.off[24]);
-  c->tri_stage = reinterpret_cast<int32_t*>(b + L.off[25]);
+  c->seeds = reinterpret_cast<hid*>(b + L.off[21]);
+  c->offsets = reinterpret_cast<uint32_t*>(b + L.off[22]);
+  c->loops = c->staging ? reinterpret_cast<int32_t*>(b + L.off[23]) : nullptr;
+  c->xy_stage = c->staging ? reinterpret_cast<double*>(b + L.off[24]) : nullptr;
+  c->tri_stage = c->staging ? reinterpret_cast<int32_t*>(b + L.off[25]) : nullptr;
   c->ctr = reinterpret_cast<DevCounters*>(b + L.off[26]);
-  c->def_e = reinterpret_cast<int32_t*>(b + L.off[27]);
+  c->def_e = reinterpret_cast<hid*>(b + L.off[27]);
   c->SDB = reinterpret_cast<uint32_t*>(b + L.off[28]);
   c->C = reinterpret_cast<uint32_t*>(b + L.off[30]);
   c->cnt_ld = reinterpret_cast<int32_t*>(b + L.off[31]);
   c->tsum = reinterpret_cast<int32_t*>(b + L.off[32]);
-  c->tbase = reinterpret_cast<int32_t*>(b + L.off[33]);
+  c->tbase = reinterpret_cast<uint32_t*>(b + L.off[33]);
   c->wlen = reinterpret_cast<int32_t*>(b + L.off[29]);
   c->n_words = (3 * c->T + 31) / 32;
   return true;
@@ -133,7 +134,7 @@ static polylla_status map_status(uint32_t st) {
   if (st & ST_WALK) return POLYLLA_E_WALK_BOUND;
   if (st & ST_UNSEEDED) return POLYLLA_E_UNSEEDED_LOOP;
   if (st & ST_CAPACITY) return POLYLLA_E_CAPACITY;
-  return POLYLLA_E_WORKSPACE;
+  return POLYLLA_E_WORKSPACE;  // (ST_BORDER_CAP: B above the workspace's border bound; ST_INTERNAL)
 }
 
 // ------------------------------------------------------------------ profiling
@@ -188,17 +189,28 @@ extern "C" {
 
 POLYLLA_API size_t polylla_workspace_bytes(int64_t n_vertices, int64_t n_triangles) {
   if (n_vertices < 0 || n_triangles < 0) return 0;
-  return workspace_bytes(n_vertices, n_triangles);
+  return workspace_bytes(n_vertices, n_triangles, 3 * n_triangles, true);
+}
+
+POLYLLA_API size_t polylla_workspace_bytes_ex(int64_t n_vertices, int64_t n_triangles, int64_t max_border,
+                                              uint32_t flags) {
+  if (n_vertices < 0 || n_triangles < 0 || max_border < 0 || max_border > 3 * n_triangles) return 0;
+  return workspace_bytes(n_vertices, n_triangles, max_border, (flags & POLYLLA_WS_STAGING) != 0);
+}
+
+// index limits (NEXT-3): vertex ids int32; half-edge ids uint32 with H <= 2^32 - 2
+static bool index_ok(int64_t V, int64_t T, int64_t Bmax) {
+  return V <= 0x7fffffffLL && 3 * T + Bmax <= kMaxHalfedges;
 }
 
 // a new ctx over caller memory (no launches): argument checks + workspace carving
-static polylla_status new_ctx(const double* xy, int64_t V, const int32_t* tri, int64_t T, void* workspace,
-                              size_t workspace_bytes_, polylla_ctx** out) {
+static polylla_status new_ctx(const double* xy, int64_t V, const int32_t* tri, int64_t T, int64_t Bmax,
+                              bool staging, void* workspace, size_t workspace_bytes_, polylla_ctx** out) {
   *out = nullptr;
-  if (!xy || !tri || !workspace || V < 3 || T < 1) return POLYLLA_E_INVALID_ARGUMENT;
+  if (!xy || !tri || !workspace || V < 3 || T < 1 || Bmax < 0 || Bmax > 3 * T) return POLYLLA_E_INVALID_ARGUMENT;
   if ((reinterpret_cast<uintptr_t>(xy) & 15) || (reinterpret_cast<uintptr_t>(tri) & 3))
     return POLYLLA_E_INVALID_ARGUMENT;
-  if (3 * T > 0x7fffffffLL || V > 0x7fffffffLL) return POLYLLA_E_INDEX_OVERFLOW;
+  if (!index_ok(V, T, Bmax)) return POLYLLA_E_INDEX_OVERFLOW;
   polylla_ctx* p = static_cast<polylla_ctx*>(std::calloc(1, sizeof(polylla_ctx)));
   if (!p) return POLYLLA_E_INVALID_ARGUMENT;
   Ctx* c = &p->c;
@@ -206,6 +218,8 @@ static polylla_status new_ctx(const double* xy, int64_t V, const int32_t* tri, i
   c->tri = tri;
   c->V = V;
   c->T = T;
+  c->Bmax = Bmax;
+  c->staging = staging;
   if (!carve(c, workspace, workspace_bytes_)) {
     std::free(p);
     return POLYLLA_E_WORKSPACE;
@@ -214,12 +228,14 @@ static polylla_status new_ctx(const double* xy, int64_t V, const int32_t* tri, i
   return POLYLLA_OK;
 }
 
-POLYLLA_API polylla_status polylla_build_halfedges(const double* xy, int64_t V, const int32_t* tri, int64_t T,
-                                                   void* workspace, size_t workspace_bytes_, polylla_stream stream,
-                                                   polylla_ctx** ctx_out) {
+POLYLLA_API polylla_status polylla_build_halfedges_ex(const double* xy, int64_t V, const int32_t* tri, int64_t T,
+                                                      int64_t max_border, uint32_t flags, void* workspace,
+                                                      size_t workspace_bytes_, polylla_stream stream,
+                                                      polylla_ctx** ctx_out) {
   if (!ctx_out) return POLYLLA_E_INVALID_ARGUMENT;
   polylla_ctx* p = nullptr;
-  const polylla_status st = new_ctx(xy, V, tri, T, workspace, workspace_bytes_, &p);
+  const polylla_status st =
+      new_ctx(xy, V, tri, T, max_border, (flags & POLYLLA_WS_STAGING) != 0, workspace, workspace_bytes_, &p);
   if (st != POLYLLA_OK) return st;
   Ctx* c = &p->c;
   const int n = launch_build(c, S(stream));
@@ -233,9 +249,17 @@ POLYLLA_API polylla_status polylla_build_halfedges(const double* xy, int64_t V, 
   return POLYLLA_OK;
 }
 
+POLYLLA_API polylla_status polylla_build_halfedges(const double* xy, int64_t V, const int32_t* tri, int64_t T,
+                                                   void* workspace, size_t workspace_bytes_, polylla_stream stream,
+                                                   polylla_ctx** ctx_out) {
+  return polylla_build_halfedges_ex(xy, V, tri, T, 3 * T, POLYLLA_WS_STAGING, workspace, workspace_bytes_, stream,
+                                    ctx_out);
+}
+
 POLYLLA_API polylla_status polylla_check_manifold(polylla_ctx* p, polylla_stream stream) {
   if (!p) return POLYLLA_E_INVALID_ARGUMENT;
   if (p->c.stage < 1) return POLYLLA_E_CALL_ORDER;
+  if (3 * p->c.T + p->c.Bmax > 0x7fffffffLL) return POLYLLA_E_INDEX_OVERFLOW;  // (its slots hold int32 ids + a flag)
   const int n = launch_check_manifold(&p->c, S(stream));
   if (n < 0) return POLYLLA_E_CUDA;
   p->c.launches += n;
@@ -265,6 +289,7 @@ POLYLLA_API polylla_status polylla_generate(polylla_ctx* p, polylla_stream strea
 POLYLLA_API polylla_status polylla_label_generate_paper(polylla_ctx* p, polylla_stream stream) {
   if (!p) return POLYLLA_E_INVALID_ARGUMENT;
   if (p->c.stage != 1) return POLYLLA_E_CALL_ORDER;
+  if (3 * p->c.T + p->c.Bmax > 0x7fffffffLL) return POLYLLA_E_INDEX_OVERFLOW;  // (the ablation keeps int32 ids)
   const int n = launch_paper(&p->c, S(stream));
   if (n < 0) return POLYLLA_E_CUDA;
   p->c.launches += n;
@@ -284,7 +309,7 @@ POLYLLA_API polylla_status polylla_get_counts(polylla_ctx* p, polylla_stream str
   r.n_vertices = c->V;
   r.n_triangles = c->T;
   r.n_border = h.n_border;
-  r.n_halfedges = 3 * c->T + h.n_border;
+  r.n_halfedges = 3 * c->T + (int64_t)h.n_border;
   r.n_polygons = c->stage >= 3 ? h.P : 0;
   r.n_loop_entries = c->stage >= 3 ? h.L : 0;
   r.n_tips = h.n_tips;
@@ -299,9 +324,9 @@ POLYLLA_API polylla_status polylla_get_counts(polylla_ctx* p, polylla_stream str
   return (polylla_status)r.status;
 }
 
-POLYLLA_API polylla_status polylla_get_polygons(polylla_ctx* p, int32_t* offsets, int64_t offsets_cap, int32_t* loops,
-                                                int64_t loops_cap, int32_t* origin, int32_t* twin, int32_t* next,
-                                                int32_t* prev, polylla_stream stream) {
+POLYLLA_API polylla_status polylla_get_polygons(polylla_ctx* p, uint32_t* offsets, int64_t offsets_cap, int32_t* loops,
+                                                int64_t loops_cap, int32_t* origin, uint32_t* twin, uint32_t* next,
+                                                uint32_t* prev, polylla_stream stream) {
   if (!p) return POLYLLA_E_INVALID_ARGUMENT;
   Ctx* c = &p->c;
   if (c->stage < 3) return POLYLLA_E_CALL_ORDER;
@@ -311,13 +336,13 @@ POLYLLA_API polylla_status polylla_get_polygons(polylla_ctx* p, int32_t* offsets
   // is device memory, else into dead workspace scratch (the leftover-key region, 24T bytes
   // >= 4H) and copied out like origin/twin/next -- a kernel must never store to a host
   // pointer
-  int32_t* prev_dev = nullptr;
+  hid* prev_dev = nullptr;
   if (prev) {
     cudaPointerAttributes pa{};
     const bool on_dev = cudaPointerGetAttributes(&pa, prev) == cudaSuccess &&
                         (pa.type == cudaMemoryTypeDevice || pa.type == cudaMemoryTypeManaged);
     cudaGetLastError();  // (clear a failed query of an unregistered host pointer)
-    prev_dev = on_dev ? prev : reinterpret_cast<int32_t*>(c->left_key);
+    prev_dev = on_dev ? prev : reinterpret_cast<hid*>(c->left_key);
     if (!on_dev && c->stage < 4) return POLYLLA_E_CALL_ORDER;  // the copy-out needs H (get_counts)
   }
   const size_t hb = (size_t)c->host_counts.n_halfedges * 4;
@@ -375,7 +400,7 @@ POLYLLA_API polylla_status polylla_get_views(polylla_ctx* p, polylla_views* v) {
   return POLYLLA_OK;
 }
 
-POLYLLA_API polylla_status polylla_set_debug(polylla_ctx* p, int32_t* next_pre) {
+POLYLLA_API polylla_status polylla_set_debug(polylla_ctx* p, uint32_t* next_pre) {
   if (!p) return POLYLLA_E_INVALID_ARGUMENT;
   p->c.next_pre = next_pre;
   return POLYLLA_OK;
@@ -414,19 +439,22 @@ struct RunRes {  // streams and events of one run_host call, released on every e
 }  // namespace
 
 POLYLLA_API polylla_status polylla_run_host(const double* xy_host, int64_t V, const int32_t* tri_host, int64_t T,
-                                            void* workspace, size_t workspace_bytes_, int32_t* offsets_host,
+                                            void* workspace, size_t workspace_bytes_, uint32_t* offsets_host,
                                             int64_t offsets_cap, int32_t* loops_host, int64_t loops_cap,
-                                            int32_t* origin_host, int32_t* twin_host, int32_t* next_host,
+                                            int32_t* origin_host, uint32_t* twin_host, uint32_t* next_host,
                                             int64_t halfedge_cap, polylla_counts* counts, polylla_stream stream) {
   if (!xy_host || !tri_host || !workspace || !offsets_host || !loops_host || !counts || V < 3 || T < 1)
     return POLYLLA_E_INVALID_ARGUMENT;
-  if (3 * T > 0x7fffffffLL || V > 0x7fffffffLL) return POLYLLA_E_INDEX_OVERFLOW;
+  if (!index_ok(V, T, 3 * T)) return POLYLLA_E_INDEX_OVERFLOW;
   Ctx probe{};
   probe.V = V;
   probe.T = T;
+  probe.Bmax = 3 * T;
+  probe.staging = true;
   if (!carve(&probe, workspace, workspace_bytes_)) return POLYLLA_E_WORKSPACE;
   polylla_ctx* p = nullptr;
-  polylla_status st = new_ctx(probe.xy_stage, V, probe.tri_stage, T, workspace, workspace_bytes_, &p);
+  polylla_status st =
+      new_ctx(probe.xy_stage, V, probe.tri_stage, T, 3 * T, true, workspace, workspace_bytes_, &p);
   if (st != POLYLLA_OK) return st;
   Ctx* c = &p->c;
   cudaStream_t s = S(stream);

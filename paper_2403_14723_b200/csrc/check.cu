@@ -16,6 +16,8 @@
 
 namespace polylla {
 
+constexpr uint32_t kPaired = 0x80000000u;  // flag in the slots (half-edge ids < 2^31: see polylla_check_manifold)
+
 __global__ void k_dup_clear(uint32_t* slots, int64_t cap) {
   uint4* s4 = reinterpret_cast<uint4*>(slots);
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < cap / 4; i += (int64_t)gridDim.x * blockDim.x)

@@ -28,15 +28,17 @@ constexpr int kEmitQ = POLYLLA_EMIT_Q;  // queue capacity (polygons per tile; a 
 
 __global__ void __launch_bounds__(kEmitThreads)
     k_emit(int64_t T, int64_t n_words, const uint32_t* __restrict__ C, const int32_t* __restrict__ len,
-           const int32_t* __restrict__ tb, const int32_t* __restrict__ origin, const int32_t* __restrict__ next,
-           int32_t* __restrict__ seeds, int32_t* __restrict__ offsets, int64_t offsets_cap, int32_t* __restrict__ loops,
+           const uint32_t* __restrict__ tb, const int32_t* __restrict__ origin, const hid* __restrict__ next,
+           hid* __restrict__ seeds, uint32_t* __restrict__ offsets, int64_t offsets_cap, int32_t* __restrict__ loops,
            int64_t loops_cap, DevCounters* ctr) {
-  __shared__ int32_t qe[kEmitQ], qo[kEmitQ];
+  __shared__ hid qe[kEmitQ];
+  __shared__ uint32_t qo[kEmitQ];
   __shared__ int32_t wbase[kEmitWords];
   __shared__ int32_t chunk[kEmitThreads / 32 + 1];
   __shared__ int32_t npoly;
   if (ctr->status) return;
-  const int32_t P = ctr->P, L = ctr->L;
+  const int32_t P = ctr->P;
+  const uint32_t L = ctr->L;
   if ((int64_t)P + 1 > offsets_cap || (int64_t)L > loops_cap) {
     if (blockIdx.x == 0 && threadIdx.x == 0) raise_status(ctr, ST_CAPACITY);
     return;
@@ -69,21 +71,22 @@ __global__ void __launch_bounds__(kEmitThreads)
   }
   __syncthreads();
   const int np = npoly;
-  const int32_t rbase = tb[2 * tile], obase = tb[2 * tile + 1];
+  const uint32_t rbase = tb[2 * tile], obase = tb[2 * tile + 1];
   if (np > kEmitQ) {  // (dense tile) one thread per word walks its polygons in order
     for (int wl = tid; wl < kEmitWords && wt + wl < n_words; wl += kEmitThreads) {
       // offset of the word's first polygon: tile base + lengths of the earlier polygons
-      int32_t o = obase;
+      uint32_t o = obase;
       for (int64_t ww = wt; ww < wt + wl; ++ww)
         for (uint32_t b = C[ww]; b; b &= b - 1) o += len[ww * 32 + __ffs(b) - 1];
-      int32_t r = rbase + wbase[wl];
+      uint32_t r = rbase + wbase[wl];
       for (uint32_t b = C[wt + wl]; b; b &= b - 1, ++r) {
-        const int32_t e = (int32_t)((wt + wl) * 32 + __ffs(b) - 1);
+        const hid e = (hid)((wt + wl) * 32 + __ffs(b) - 1);
         const int32_t n = len[e];
         seeds[r] = e;
         offsets[r] = o;
-        int32_t x = e;
-        for (int32_t i = 0; i < n; ++i, x = next[x]) loops[o + i] = origin[x];
+        hid x = e;
+        int32_t* dst = loops + o;  // (a pointer walk: unsigned o + i would be re-extended every step)
+        for (int32_t i = 0; i < n; ++i, x = next[x]) dst[i] = origin[x];
         o += n;
       }
     }
@@ -92,16 +95,16 @@ __global__ void __launch_bounds__(kEmitThreads)
     // per thread (independent loads instead of a chain per word)
     for (int wl = tid; wl < kEmitWords && wt + wl < n_words; wl += kEmitThreads) {
       int p = wbase[wl];
-      for (uint32_t b = C[wt + wl]; b; b &= b - 1, ++p) qe[p] = (int32_t)((wt + wl) * 32 + __ffs(b) - 1);
+      for (uint32_t b = C[wt + wl]; b; b &= b - 1, ++p) qe[p] = (hid)((wt + wl) * 32 + __ffs(b) - 1);
     }
     __syncthreads();
-    for (int i = tid; i < np; i += kEmitThreads) qo[i] = len[qe[i]];
+    for (int i = tid; i < np; i += kEmitThreads) qo[i] = (uint32_t)len[qe[i]];
     __syncthreads();
     // exclusive scan of the lengths: thread t owns queue entries [t*per, (t+1)*per)
     const int per = (np + kEmitThreads - 1) / kEmitThreads;
     const int q0 = tid * per, q1 = min(q0 + per, np);
     int sum = 0;
-    for (int i = q0; i < q1; ++i) sum += qo[i];
+    for (int i = q0; i < q1; ++i) sum += (int)qo[i];
     int inc = sum;
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
@@ -115,38 +118,41 @@ __global__ void __launch_bounds__(kEmitThreads)
       for (int k = 0; k < kEmitThreads / 32; ++k) { const int v = chunk[k]; chunk[k] = acc; acc += v; }
     }
     __syncthreads();
-    int run = obase + chunk[warp] + inc - sum;
-    for (int i = q0; i < q1; ++i) { const int n = qo[i]; qo[i] = run; run += n; }
-    if (q1 == np && q0 < q1) chunk[kEmitThreads / 32] = run;  // end of the tile's last loop
+    // (tile-local sums fit int; the tile base may exceed 2^31: unsigned from here)
+    uint32_t run = obase + (uint32_t)(chunk[warp] + inc - sum);
+    for (int i = q0; i < q1; ++i) { const uint32_t n = qo[i]; qo[i] = run; run += n; }
+    if (q1 == np && q0 < q1) chunk[kEmitThreads / 32] = (int32_t)(run - obase);  // end of the tile's last loop
     __syncthreads();
-    const int32_t run_end = chunk[kEmitThreads / 32];
+    const uint32_t run_end = obase + (uint32_t)chunk[kEmitThreads / 32];
     // one polygon per thread
     for (int i = tid; i < np; i += kEmitThreads) {
-      const int32_t e = qe[i], o = qo[i];
-      const int32_t n = (i + 1 < np ? qo[i + 1] : run_end) - o;
+      const hid e = qe[i];
+      const uint32_t o = qo[i];
+      const int32_t n = (int32_t)((i + 1 < np ? qo[i + 1] : run_end) - o);
       seeds[rbase + i] = e;
       offsets[rbase + i] = o;
-      int32_t x = e;
-      for (int32_t k = 0; k < n; ++k, x = next[x]) loops[o + k] = origin[x];
+      hid x = e;
+      int32_t* dst = loops + o;  // (a pointer walk: unsigned o + k would be re-extended every step)
+      for (int32_t k = 0; k < n; ++k, x = next[x]) dst[k] = origin[x];
     }
   }
   if (tile == (int64_t)gridDim.x - 1 && tid == 0) offsets[P] = L;
 }
 
-__global__ void k_prev(int64_t T, const int32_t* __restrict__ next, const uint32_t* __restrict__ F1,
-                       int32_t* __restrict__ prev, DevCounters* ctr) {
+__global__ void k_prev(int64_t T, const hid* __restrict__ next, const uint32_t* __restrict__ F1,
+                       hid* __restrict__ prev, DevCounters* ctr) {
   if (ctr->status) return;
   const int64_t T3 = 3 * T;
   const int64_t H = T3 + ctr->n_border;
   for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < H; e += (int64_t)gridDim.x * blockDim.x) {
-    const int32_t ei = (int32_t)e;
+    const hid ei = (hid)e;
     if (e >= T3 || bit_of(F1, ei)) prev[next[ei]] = ei;
     else prev[ei] = prev_in(ei);
   }
 }
 
-int launch_extract(Ctx* c, int32_t* offsets, int64_t offsets_cap, int32_t* loops, int64_t loops_cap,
-                   int32_t* prev, cudaStream_t s) {
+int launch_extract(Ctx* c, uint32_t* offsets, int64_t offsets_cap, int32_t* loops, int64_t loops_cap,
+                   hid* prev, cudaStream_t s) {
   int n = 0;
   prof_mark(s, "k_extract");
   if (loops) {

@@ -21,7 +21,7 @@
 
 namespace polylla {
 
-__device__ __forceinline__ bool f1_of(const uint32_t* __restrict__ F1, int64_t T3, int32_t x) {
+__device__ __forceinline__ bool f1_of(const uint32_t* __restrict__ F1, int64_t T3, hid x) {
   return x >= T3 || bit_of(F1, x);
 }
 
@@ -32,24 +32,24 @@ __device__ __forceinline__ bool f1_of(const uint32_t* __restrict__ F1, int64_t T
 #endif
 constexpr int kRepairThreads = POLYLLA_REPAIR_THREADS;
 __global__ void __launch_bounds__(kRepairThreads)
-    k_repair_mid(int64_t T, int64_t n_words, const uint32_t* __restrict__ TB, const int32_t* __restrict__ twin,
-                 uint32_t* F1, uint32_t* SDB, int32_t* __restrict__ tips, int32_t* __restrict__ aff, DevCounters* ctr) {
-  __shared__ int32_t queue[kRepairThreads / 32][kBitQueue];
+    k_repair_mid(int64_t T, int64_t n_words, const uint32_t* __restrict__ TB, const hid* __restrict__ twin,
+                 uint32_t* F1, uint32_t* SDB, hid* __restrict__ tips, hid* __restrict__ aff, DevCounters* ctr) {
+  __shared__ hid queue[kRepairThreads / 32][kBitQueue];
   if (ctr->status) return;
   const int64_t T3 = 3 * T;
   const int lane = threadIdx.x & 31;
-  warp_foreach_bit(TB, n_words, queue[threadIdx.x >> 5], [&](int32_t e, bool valid) {
+  warp_foreach_bit(TB, n_words, queue[threadIdx.x >> 5], [&](hid e, bool valid) {
     const uint32_t m32 = __ballot_sync(0xffffffffu, valid);
     int base = 0;
     if (lane == 0) base = atomicAdd(&ctr->n_tips, __popc(m32));
     const int i = __shfl_sync(0xffffffffu, base, 0) + __popc(m32 & ((1u << lane) - 1));
     if (!valid) return;
-    const int32_t e0 = twin[e];  // the tip's only outgoing frontier half-edge
-    int32_t x = e0;
+    const hid e0 = twin[e];  // the tip's only outgoing frontier half-edge
+    hid x = e0;
     int64_t d = 0;
     bool ok = true;
     do {  // degree(v): rotation closure about v (an interior vertex); deg(v) <= 3T
-      const int32_t tx = twin[x];
+      const hid tx = twin[x];
       if (tx >= T3 || ++d > T3) { ok = false; break; }
       x = next_in(tx);
     } while (x != e0);
@@ -59,9 +59,9 @@ __global__ void __launch_bounds__(kRepairThreads)
       aff[2 * i] = aff[2 * i + 1] = e0;
       return;
     }
-    int32_t m = e0;
+    hid m = e0;
     for (int64_t k = 0; k < (d - 1) / 2; ++k) m = next_in(twin[m]);  // CWvertexEdge steps (R1, R5)
-    const int32_t tm = twin[m];
+    const hid tm = twin[m];
     atomicOr(&F1[m >> 5], 1u << (m & 31));
     atomicOr(&F1[tm >> 5], 1u << (tm & 31));
     atomicOr(&SDB[m >> 5], 1u << (m & 31));  // both halves seed the split polygons
@@ -71,21 +71,21 @@ __global__ void __launch_bounds__(kRepairThreads)
   });
 }
 
-__global__ void k_repair_rewire(int64_t T, const int32_t* __restrict__ twin, const uint32_t* __restrict__ F1,
-                                const int32_t* __restrict__ aff, int32_t* next, DevCounters* ctr) {
+__global__ void k_repair_rewire(int64_t T, const hid* __restrict__ twin, const uint32_t* __restrict__ F1,
+                                const hid* __restrict__ aff, hid* next, DevCounters* ctr) {
   if (ctr->status) return;
   const int64_t T3 = 3 * T;
   const int64_t H = T3 + ctr->n_border;  // walk bound (a rotation about w has <= deg(w) <= H steps)
   const int32_t n = 2 * ctr->n_tips;
   for (int32_t j = blockIdx.x * blockDim.x + threadIdx.x; j < n; j += gridDim.x * blockDim.x) {
-    const int32_t o = aff[j];
-    int32_t y = o;
+    const hid o = aff[j];
+    hid y = o;
     int64_t guard = 0;
     do {
       if (y < T3) {
-        const int32_t p = prev_in(y);  // incoming to w in y's triangle; next_in(p) = y
+        const hid p = prev_in(y);  // incoming to w in y's triangle; next_in(p) = y
         if (f1_of(F1, T3, p)) {
-          int32_t x = y;
+          hid x = y;
           int64_t steps = 0;
           while (!f1_of(F1, T3, x) && ++steps <= H) x = next_in(twin[x]);
           if (steps > H) {  // the rotation to the next F1 half-edge did not close
@@ -95,7 +95,7 @@ __global__ void k_repair_rewire(int64_t T, const int32_t* __restrict__ twin, con
           next[p] = x;
         }
       }
-      const int32_t ty = twin[y];
+      const hid ty = twin[y];
       y = ty >= T3 ? next[ty] : next_in(ty);  // full rotation about w (border chain at the hull)
       if (++guard > H) { raise_status(ctr, ST_WALK); break; }
     } while (y != o);
@@ -107,16 +107,16 @@ __global__ void k_repair_rewire(int64_t T, const int32_t* __restrict__ twin, con
 #endif
 constexpr int kSeedThreads = POLYLLA_SEED_THREADS;
 
-__device__ __forceinline__ void process_seed(int32_t s, int64_t T3, int64_t H, const int32_t* __restrict__ twin,
-                                             const int32_t* __restrict__ next, const uint32_t* __restrict__ F1,
+__device__ __forceinline__ void process_seed(hid s, int64_t T3, int64_t H, const hid* __restrict__ twin,
+                                             const hid* __restrict__ next, const uint32_t* __restrict__ F1,
                                              uint32_t* C, int32_t* len, int32_t* wlen, DevCounters* ctr) {
-  int32_t x = s;
+  hid x = s;
   int64_t steps = 0;
   while (!f1_of(F1, T3, x)) {  // Alg. 12: rotate (sweep_out) to a frontier half-edge (<= deg <= 3T steps)
     x = next_in(twin[x]);
     if (++steps > T3 || x == s) { raise_status(ctr, ST_WALK); return; }
   }
-  int32_t mn = x, y = x;
+  hid mn = x, y = x;
   int64_t n = 0;
   do {  // Overwrite seeds: walk the polygon, keep the minimum index
     mn = min(mn, y);
@@ -132,17 +132,17 @@ __device__ __forceinline__ void process_seed(int32_t s, int64_t T3, int64_t H, c
 // the label fixup found, and both halves of every middle edge of the repair; balanced
 // over warps (warp_foreach_bit), one seed per lane.
 __global__ void __launch_bounds__(kSeedThreads)
-    k_seed_walk(int64_t T, int64_t n_words, const uint32_t* __restrict__ SDB, const int32_t* __restrict__ twin,
-                const int32_t* __restrict__ next, const uint32_t* __restrict__ F1, uint32_t* C, int32_t* len,
+    k_seed_walk(int64_t T, int64_t n_words, const uint32_t* __restrict__ SDB, const hid* __restrict__ twin,
+                const hid* __restrict__ next, const uint32_t* __restrict__ F1, uint32_t* C, int32_t* len,
                 int32_t* wlen, DevCounters* ctr) {
-  __shared__ int32_t queue[kSeedThreads / 32][kBitQueue];
+  __shared__ hid queue[kSeedThreads / 32][kBitQueue];
   if (ctr->status) return;
   const int64_t T3 = 3 * T;
   const int64_t H = T3 + ctr->n_border;
-  const int n = warp_foreach_bit(SDB, n_words, queue[threadIdx.x >> 5], [&](int32_t s, bool valid) {
+  const int n = warp_foreach_bit(SDB, n_words, queue[threadIdx.x >> 5], [&](hid s, bool valid) {
     if (valid) process_seed(s, T3, H, twin, next, F1, C, len, wlen, ctr);
   });
-  if ((threadIdx.x & 31) == 0 && n) atomicAdd(&ctr->n_sdef, n);
+  if ((threadIdx.x & 31) == 0 && n) atomicAdd(&ctr->n_sdef, (uint32_t)n);
 }
 
 // "Scan and compact" at tile granularity: per build tile (192 words
@@ -184,7 +184,7 @@ __global__ void k_canon_tiles(int64_t n_words, int64_t ntiles, const uint32_t* _
 // per tile -> tb[2 * tile + {0, 1}]; totals -> P, L; the R12 check sum(len) == #F1
 constexpr int kTopThreads = 1024;
 __global__ void __launch_bounds__(kTopThreads)
-    k_tiles_scan(int64_t ntiles, const int32_t* __restrict__ ts, int32_t* __restrict__ tb, int32_t* __restrict__ offsets,
+    k_tiles_scan(int64_t ntiles, const int32_t* __restrict__ ts, uint32_t* __restrict__ tb, uint32_t* __restrict__ offsets,
                  DevCounters* ctr) {
   constexpr int NW = kTopThreads / 32;
   __shared__ long long wsum[3][NW];
@@ -215,10 +215,10 @@ __global__ void __launch_bounds__(kTopThreads)
     wsum[1][lane] = ib - b;
     if (lane == 31) {
       ctr->P = (int32_t)ia;
-      ctr->L = (int32_t)ib;
-      ctr->n_f1 = (int32_t)ic;
+      ctr->L = (uint32_t)ib;
+      ctr->n_f1 = (uint32_t)ic;
       if (ib != ic) raise_status(ctr, ST_UNSEEDED);  // R12: a frontier loop without a seed
-      offsets[ia] = (int32_t)ib;
+      offsets[ia] = (uint32_t)ib;
     }
   }
   __syncthreads();
@@ -233,8 +233,8 @@ __global__ void __launch_bounds__(kTopThreads)
       if (lane >= o) { ip += x; il += y; }
     }
     if (t < t1) {
-      tb[2 * t] = (int32_t)(cp + ip - vp);
-      tb[2 * t + 1] = (int32_t)(cl + il - vl);
+      tb[2 * t] = (uint32_t)(cp + ip - vp);
+      tb[2 * t + 1] = (uint32_t)(cl + il - vl);
     }
     cp += __shfl_sync(0xffffffffu, ip, 31);
     cl += __shfl_sync(0xffffffffu, il, 31);

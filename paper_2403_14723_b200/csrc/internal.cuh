@@ -17,6 +17,13 @@
 
 namespace polylla {
 
+// Half-edge ids are UNSIGNED 32-bit (capacity beyond int32):
+// H = 3T + B <= 2^32 - 2, so 0xFFFFFFFF stays free as the "none" sentinel.  Vertex ids
+// (origin, loops, the input triangles) and triangle ids stay int32 (V, T < 2^31).
+using hid = uint32_t;
+constexpr hid kNoHe = 0xFFFFFFFFu;
+constexpr int64_t kMaxHalfedges = 0xFFFFFFFELL;  // 3T + B must not exceed this
+
 // ------------------------------------------------------------------ status bits
 enum : uint32_t {
   ST_DANGLING = 1u << 0,
@@ -28,21 +35,22 @@ enum : uint32_t {
   ST_CAPACITY = 1u << 6,
   ST_OVERFLOW = 1u << 7,
   ST_INTERNAL = 1u << 8,
+  ST_BORDER_CAP = 1u << 9,  // B exceeds the workspace's border bound (polylla_workspace_bytes_ex)
 };
 
 // device-side counters (zeroed at the start of every build)
 struct DevCounters {
   uint32_t status;
-  int32_t n_left;    // leftover half-edges (twin not in the build tile)
-  int32_t n_border;  // B
+  uint32_t n_left;   // leftover half-edges (twin not in the build tile)
+  uint32_t n_border; // B
   int32_t n_tips;
   int32_t n_flips;
-  int32_t P;         // polygons
-  int32_t L;         // loop entries
-  int32_t n_f1;      // #interior F1 half-edges
+  int32_t P;         // polygons (<= T < 2^31)
+  uint32_t L;        // loop entries (<= 3T)
+  uint32_t n_f1;     // #interior F1 half-edges
   uint32_t hash_cap; // capacity (pow2 <= 2^31) of the leftover hash for this run
-  int32_t n_def;     // half-edges deferred by k_tile to the label fixup
-  int32_t n_sdef;    // seeds walked by k_seed_walk (deferred + repair halves)
+  uint32_t n_def;    // half-edges deferred by k_tile to the label fixup
+  uint32_t n_sdef;   // seeds walked by k_seed_walk (deferred + repair halves)
   uint32_t pad0;
   unsigned long long hash_scale;  // leftover-hash home slot = (lo * hash_scale) >> 32 (cap / V in 32.32 fixed point)
   int32_t pad[2];
@@ -53,38 +61,41 @@ struct Ctx {
   const double* xy;
   const int32_t* tri;
   int64_t V, T;
-  int64_t Hmax;  // 6T
+  int64_t Hmax;  // 3T + the border bound (6T by default)
+  int64_t Bmax;  // border bound of the workspace layout
+  bool staging;  // the layout holds run_host's staging regions
   // workspace views
-  int32_t *origin, *twin, *next;
+  int32_t* origin;   // vertex ids
+  hid *twin, *next;
   uint8_t* lcode;
   uint32_t *F0, *F1, *S, *C;
   int32_t* len;     // [3T] loop length, at canonical seeds
   int32_t* wlen;    // [n_words] sum of loop lengths of the canonical seeds of each C word
   unsigned long long* left_key;
-  int32_t* left_e;
-  int32_t* def_e;   // [3T] half-edges deferred by k_tile (per-tile segments at 3 * tile * 2048)
+  hid* left_e;
+  hid* def_e;       // [3T] half-edges deferred by k_tile (per-tile segments at 3 * tile * 2048)
   uint32_t* SDB;    // [n_words] seeds for the global seed walk (deferred by k_tile / the fixup, repair halves)
   uint32_t* TB;     // [n_words] barrier tips (incoming frontier half-edge e, next[e] == twin[e])
   int32_t* cnt_ld;  // [2 * tiles] per-tile leftover / deferred counts
   int32_t* tsum;    // [3 * tiles] per-tile #canonical seeds, sum of loop lengths, #F1
-  int32_t* tbase;   // [2 * tiles] per-tile exclusive prefix of polygons / loop entries
-  int32_t* bcnt;    // [tiles] per-tile border half-edge count, then (in place) its base
-  uint32_t* ehash;  // leftover-edge hash slots [hash_cap_max] (capacity chosen on device)
-  int32_t* vmap;    // [V] border half-edge leaving each border vertex (written at border vertices only)
+  uint32_t* tbase;  // [2 * tiles] per-tile exclusive prefix of polygons / loop entries
+  uint32_t* bcnt;   // [tiles] per-tile border half-edge count, then (in place) its base
+  void* ehash;      // leftover-edge hash slots [hash_cap_max], u32 (3T < 2^31) or u64 (capacity chosen on device)
+  hid* vmap;        // [V] border half-edge leaving each border vertex (written at border vertices only)
   int64_t hash_cap_max;
-  int32_t* tips;    // [V]
-  int32_t* aff;     // [2V] affected (outgoing half-edge) per tip side
-  int32_t* mids;    // [2V]
+  hid* tips;        // [V]
+  hid* aff;         // [2V] affected (outgoing half-edge) per tip side
+  hid* mids;        // [2V]
   long long* scan_a;  // per-block sums (count)
   long long* scan_b;  // per-block sums (aux)
   long long* scan_c;  // per-block sums (F1 popcount)
-  int32_t* seeds;     // [T]
-  int32_t* offsets;   // [T+1]
+  hid* seeds;         // [T]
+  uint32_t* offsets;  // [T+1]
   int32_t* loops;     // [3T]  (run_host staging)
   double* xy_stage;   // [2V]  (run_host staging)
   int32_t* tri_stage; // [3T]
   DevCounters* ctr;
-  int32_t* next_pre;  // optional debug copy
+  hid* next_pre;      // optional debug copy
   // host state
   int stage;          // 1 built, 2 labelled, 3 generated, 4 counted
   bool extracted;     // polylla_get_polygons wrote the polygon seeds
@@ -99,8 +110,8 @@ void prof_mark(cudaStream_t s, const char* name);  // start of kernel `name` (en
 void prof_end(cudaStream_t s);
 
 // workspace
-size_t workspace_bytes(int64_t V, int64_t T);
-bool carve(Ctx* c, void* ws, size_t bytes);
+size_t workspace_bytes(int64_t V, int64_t T, int64_t Bmax, bool staging);
+bool carve(Ctx* c, void* ws, size_t bytes);  // layout from c->V, c->T, c->Bmax, c->staging
 
 // launchers (each returns the number of kernel launches issued, < 0 on CUDA error)
 int launch_build(Ctx* c, cudaStream_t s);  // = begin + tiles [0, ntiles) + rest
@@ -109,22 +120,22 @@ int launch_build_tiles(Ctx* c, cudaStream_t s, int64_t t0, int64_t t1);
 int launch_build_rest(Ctx* c, cudaStream_t s);
 int launch_label(Ctx* c, cudaStream_t s);
 int launch_generate(Ctx* c, cudaStream_t s);
-int launch_extract(Ctx* c, int32_t* offsets, int64_t offsets_cap, int32_t* loops, int64_t loops_cap,
-                   int32_t* prev, cudaStream_t s);
+int launch_extract(Ctx* c, uint32_t* offsets, int64_t offsets_cap, int32_t* loops, int64_t loops_cap,
+                   hid* prev, cudaStream_t s);
 int launch_regions(Ctx* c, int32_t* out, int mode, cudaStream_t s);  // mode 0: polygon ids, 1: F0 regions
 int launch_check_manifold(Ctx* c, cudaStream_t s);
 int launch_paper(Ctx* c, cudaStream_t s);  // the paper's LLK..OSK + Scan sequence (NEXT-2 ablation)
 
 // ------------------------------------------------------------------ device helpers
-__device__ __forceinline__ int32_t next_in(int32_t e) {  // 3f + (k+1)%3
-  const int32_t k = e % 3;
+__device__ __forceinline__ hid next_in(hid e) {  // 3f + (k+1)%3
+  const hid k = e % 3u;
   return k == 2 ? e - 2 : e + 1;
 }
-__device__ __forceinline__ int32_t prev_in(int32_t e) {  // 3f + (k+2)%3
-  const int32_t k = e % 3;
+__device__ __forceinline__ hid prev_in(hid e) {  // 3f + (k+2)%3
+  const hid k = e % 3u;
   return k == 0 ? e + 2 : e - 1;
 }
-__device__ __forceinline__ bool bit_of(const uint32_t* w, int32_t e) { return (w[e >> 5] >> (e & 31)) & 1u; }
+__device__ __forceinline__ bool bit_of(const uint32_t* w, hid e) { return (w[e >> 5] >> (e & 31)) & 1u; }
 
 __device__ __forceinline__ void raise_status(DevCounters* c, uint32_t bits) { atomicOr(&c->status, bits); }
 
@@ -139,7 +150,6 @@ __device__ __forceinline__ uint32_t mix32(uint32_t a, uint32_t b) {
 }
 
 constexpr uint32_t kEmpty = 0xFFFFFFFFu;   // empty hash slot
-constexpr uint32_t kPaired = 0x80000000u;  // flag in hash slots (slot values < 2^31 - 1)
 constexpr int kBuildTileTris = 2048;     // triangles per k_tile tile (list segments are 3 * 2048 wide)
 
 // Block -> tile schedule of the per-tile kernels.  POLYLLA_REVERSE_TILES (a test variant,
@@ -157,7 +167,7 @@ __device__ __forceinline__ int64_t sched_tile(int64_t i, int64_t ntiles) {
 // chunks g, g + G, ... and expands the set bits into its shared queue q (kBitQueue
 // entries); each full (or final) queue is handed to f(e, valid) in warp-uniform rounds of
 // 32 (all lanes present, so f may use warp collectives; valid is false on the padding
-// lanes of the last round).  Returns the number of set bits this warp saw.
+// lanes of the last round; e is then kNoHe).  Returns the number of set bits this warp saw.
 constexpr int kBitQueue = 128;  // small: the walks that follow live on L1 hits (shared memory shrinks L1)
 #ifndef POLYLLA_BIT_CHUNK
 #define POLYLLA_BIT_CHUNK 32
@@ -165,14 +175,14 @@ constexpr int kBitQueue = 128;  // small: the walks that follow live on L1 hits 
 constexpr int kBitChunk = POLYLLA_BIT_CHUNK;  // words per warp chunk (<= 32; 8 and 4 measured slower)
 static_assert(kBitChunk >= 1 && kBitChunk <= 32, "one word per lane");
 template <class F>
-__device__ __forceinline__ int warp_foreach_bit(const uint32_t* __restrict__ bv, int64_t n_words, int32_t* q, F f) {
+__device__ __forceinline__ int warp_foreach_bit(const uint32_t* __restrict__ bv, int64_t n_words, hid* q, F f) {
   const int lane = threadIdx.x & 31;
   const int64_t nwarps = (int64_t)gridDim.x * (blockDim.x >> 5);
   const int64_t gwarp = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   int fill = 0, seen = 0;
   auto flush = [&]() {
     __syncwarp();
-    for (int base = 0; base < fill; base += 32) f(base + lane < fill ? q[base + lane] : -1, base + lane < fill);
+    for (int base = 0; base < fill; base += 32) f(base + lane < fill ? q[base + lane] : kNoHe, base + lane < fill);
     __syncwarp();
     fill = 0;
   };
@@ -196,7 +206,7 @@ __device__ __forceinline__ int warp_foreach_bit(const uint32_t* __restrict__ bv,
       const int room = kBitQueue - fill, excl = incl - c;
       int take = room - excl;
       take = take < 0 ? 0 : (take > c ? c : take);
-      for (int p = fill + excl, k = 0; k < take; ++k, bits &= bits - 1) q[p++] = (int32_t)(w * 32 + __ffs(bits) - 1);
+      for (int p = fill + excl, k = 0; k < take; ++k, bits &= bits - 1) q[p++] = (hid)(w * 32 + __ffs(bits) - 1);
       const int added = tot < room ? tot : room;
       fill += added;
       seen += added;

@@ -19,9 +19,9 @@ namespace polylla {
 #endif
 constexpr int kLabelThreads = POLYLLA_FIX_THREADS;
 
-__device__ __forceinline__ bool is_longest(const uint8_t* __restrict__ lcode, int32_t x) {
-  const int32_t f = x / 3;
-  return (int32_t)lcode[f] == x - 3 * f;
+__device__ __forceinline__ bool is_longest(const uint8_t* __restrict__ lcode, hid x) {
+  const hid f = x / 3u;
+  return (hid)lcode[f] == x - 3u * f;
 }
 
 // One thread per half-edge deferred by k_tile (its twin, or a twin met by its rotation
@@ -30,8 +30,8 @@ __device__ __forceinline__ bool is_longest(const uint8_t* __restrict__ lcode, in
 // phase) are completed with atomicOr.  The deferred half-edges of tile t are entries
 // [3 * 2048 * t, + cnt_ld[2t + 1]) of def_e; one block per tile segment.
 __global__ void __launch_bounds__(kLabelThreads)
-    k_label_fixup(int64_t T, int64_t ntiles, const int32_t* __restrict__ cnt_ld, const int32_t* __restrict__ def_e,
-                  const int32_t* __restrict__ twin, const uint8_t* __restrict__ lcode, int32_t* __restrict__ next,
+    k_label_fixup(int64_t T, int64_t ntiles, const int32_t* __restrict__ cnt_ld, const hid* __restrict__ def_e,
+                  const hid* __restrict__ twin, const uint8_t* __restrict__ lcode, hid* __restrict__ next,
                   uint32_t* __restrict__ F0, uint32_t* __restrict__ F1, uint32_t* __restrict__ S,
                   uint32_t* __restrict__ TB, uint32_t* __restrict__ SDB, DevCounters* ctr) {
   if (ctr->status) return;
@@ -40,24 +40,24 @@ __global__ void __launch_bounds__(kLabelThreads)
   for (int64_t it = blockIdx.x; it < ntiles; it += gridDim.x) {
     const int64_t tile = sched_tile(it, ntiles);
     const int32_t n = cnt_ld[2 * tile + 1];
-    const int32_t seg = (int32_t)(3 * kBuildTileTris * tile);
+    const int64_t seg = 3 * kBuildTileTris * tile;
     for (int32_t base = 0; base < n; base += kLabelThreads) {  // warp-uniform trip count
       const int32_t i = base + threadIdx.x;
       bool tip = false, walk_err = false, sd = false, fr = false;
-      int32_t e = -1;
+      hid e = kNoHe;
       if (i < n) {
         e = def_e[seg + i];
-        const int32_t t = twin[e];
+        const hid t = twin[e];
         const bool tb = t >= T3;
         const bool Le = is_longest(lcode, e);
         const bool Lt = !tb && is_longest(lcode, t);
         fr = tb || (!Le && !Lt);
         sd = Le && (tb || (Lt && e < t));
-        int32_t nx = next_in(e);
+        hid nx = next_in(e);
         if (fr) {
-          int32_t x = nx;
+          hid x = nx;
           for (int64_t steps = 0;; ++steps) {  // bound: a rotation has <= deg(v) <= 3T steps
-            const int32_t tx = twin[x];
+            const hid tx = twin[x];
             if (tx >= T3) break;                                         // border edge: frontier
             if (!is_longest(lcode, x) && !is_longest(lcode, tx)) break;  // frontier edge
             x = next_in(tx);                                             // cross the edge (sweep_out)
@@ -70,13 +70,13 @@ __global__ void __launch_bounds__(kLabelThreads)
       }
       // bit-vector words: deferred entries are in ascending order per tile, so
       // neighbouring lanes usually share a word -> one atomicOr per distinct word
-      const uint32_t word = e >= 0 ? (uint32_t)(e >> 5) : 0xFFFFFFFFu;
+      const uint32_t word = e != kNoHe ? (uint32_t)(e >> 5) : 0xFFFFFFFFu;
       const uint32_t peers = __match_any_sync(0xffffffffu, word);
-      const uint32_t bit = e >= 0 ? 1u << (e & 31) : 0u;
+      const uint32_t bit = e != kNoHe ? 1u << (e & 31) : 0u;
       const uint32_t fbits = __reduce_or_sync(peers, fr ? bit : 0u);
       const uint32_t sbits = __reduce_or_sync(peers, sd ? bit : 0u);
       const uint32_t tbits = __reduce_or_sync(peers, tip ? bit : 0u);
-      if (e >= 0 && lane == __ffs(peers) - 1) {
+      if (e != kNoHe && lane == __ffs(peers) - 1) {
         if (fbits) { atomicOr(&F0[word], fbits); atomicOr(&F1[word], fbits); }
         if (sbits) { atomicOr(&S[word], sbits); atomicOr(&SDB[word], sbits); }  // seeds found here: global walk
         if (tbits) atomicOr(&TB[word], tbits);

@@ -214,9 +214,13 @@ int launch_canon_scan(Ctx* c, cudaStream_t s);  // generate.cu: "Scan and compac
 
 int launch_paper(Ctx* c, cudaStream_t s) {
   const int64_t T = c->T, V = c->V, nw = c->n_words;
+  // (this ablation keeps int32 half-edge ids: polylla_label_generate_paper refuses
+  // meshes with 3T + max_border > INT32_MAX, where both readings agree)
+  int32_t* twin = reinterpret_cast<int32_t*>(c->twin);
+  int32_t* next = reinterpret_cast<int32_t*>(c->next);
   const unsigned g = 148 * 8;
   uint32_t* Lb = c->TB;  // the longest-edge bit-vector (TB is unused on this path)
-  int32_t* incident = c->vmap;  // dead after the build's border chaining
+  int32_t* incident = reinterpret_cast<int32_t*>(c->vmap);  // dead after the build's border chaining
   int32_t* prev = reinterpret_cast<int32_t*>(c->left_key);  // CaK's prev (scratch: 24T B >= 4H)
   prof_mark(s, "p_LLK");
   cudaMemsetAsync(Lb, 0, (size_t)nw * 4, s);
@@ -224,20 +228,20 @@ int launch_paper(Ctx* c, cudaStream_t s) {
   cudaMemsetAsync(c->wlen, 0, (size_t)nw * 4, s);
   k_p_llk<<<g, 256, 0, s>>>(T, reinterpret_cast<const double2*>(c->xy), c->origin, Lb, c->ctr);
   prof_mark(s, "p_LFK");
-  k_p_lfk<<<g, 256, 0, s>>>(T, c->twin, Lb, c->F0, c->ctr);
+  k_p_lfk<<<g, 256, 0, s>>>(T, twin, Lb, c->F0, c->ctr);
   prof_mark(s, "p_LSK");
-  k_p_lsk<<<g, 256, 0, s>>>(T, c->twin, Lb, c->S, c->ctr);
+  k_p_lsk<<<g, 256, 0, s>>>(T, twin, Lb, c->S, c->ctr);
   prof_mark(s, "p_LEK");
   cudaMemsetAsync(incident, 0xFF, (size_t)V * 4, s);
   k_p_incident<<<g, 256, 0, s>>>(T, c->origin, incident);
   cudaMemcpyAsync(c->F1, c->F0, (size_t)nw * 4, cudaMemcpyDeviceToDevice, s);
-  k_p_lek<<<g, 256, 0, s>>>(V, T, incident, c->twin, c->next, c->F0, c->F1, c->S, c->ctr);
+  k_p_lek<<<g, 256, 0, s>>>(V, T, incident, twin, next, c->F0, c->F1, c->S, c->ctr);
   prof_mark(s, "p_CaK");
-  k_p_cak<<<g, 256, 0, s>>>(T, c->twin, c->F1, c->next, prev, c->ctr);
+  k_p_cak<<<g, 256, 0, s>>>(T, twin, c->F1, next, prev, c->ctr);
   prof_mark(s, "p_SFK");
-  k_p_sfk<<<g, 256, 0, s>>>(T, c->twin, c->F1, c->S, nw, c->ctr);
+  k_p_sfk<<<g, 256, 0, s>>>(T, twin, c->F1, c->S, nw, c->ctr);
   prof_mark(s, "p_OSK");
-  k_p_osk<<<g, 256, 0, s>>>(T, c->next, c->S, c->C, c->len, c->wlen, nw, c->ctr);
+  k_p_osk<<<g, 256, 0, s>>>(T, next, c->S, c->C, c->len, c->wlen, nw, c->ctr);
   prof_end(s);
   int n = 8;
   const int m = launch_canon_scan(c, s);

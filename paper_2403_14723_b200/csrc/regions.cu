@@ -71,7 +71,7 @@ __device__ __forceinline__ int32_t uf_find_s(int32_t* p, int32_t x) {
 #endif
 constexpr int kUfTile = kBuildTileTris, kUfThreads = POLYLLA_UF_THREADS;
 static_assert(3 * kUfTile % kUfThreads == 0, "half-edges per thread");
-__global__ void __launch_bounds__(kUfThreads) k_uf_local(int64_t T, const int32_t* __restrict__ twin,
+__global__ void __launch_bounds__(kUfThreads) k_uf_local(int64_t T, const hid* __restrict__ twin,
                                                   const uint32_t* __restrict__ F1, int32_t* __restrict__ parent,
                                                   int32_t* __restrict__ slot, const DevCounters* ctr) {
   __shared__ int32_t p[kUfTile];
@@ -80,22 +80,22 @@ __global__ void __launch_bounds__(kUfThreads) k_uf_local(int64_t T, const int32_
   const int nt = T - t0 < kUfTile ? (int)(T - t0) : kUfTile;
   for (int i = threadIdx.x; i < nt; i += blockDim.x) p[i] = i;
   __syncthreads();
-  const int32_t e0 = (int32_t)(3 * t0);
+  const hid e0 = (hid)(3 * t0);
   constexpr int kIt = 3 * kUfTile / kUfThreads;
-  int32_t tws[kIt];
+  hid tws[kIt];
 #pragma unroll
   // a thread takes kIt consecutive half-edges (4 triangles): neighbouring lanes then unite
   // different pieces (interleaved lanes all hook the same few roots and retry their CAS)
   for (int k = 0; k < kIt; ++k) {  // all of the thread's loads first (independent)
     const int j = threadIdx.x * kIt + k;
-    tws[k] = j < 3 * nt && !bit_of(F1, e0 + j) ? __ldcs(twin + e0 + j) : -1;
+    tws[k] = j < 3 * nt && !bit_of(F1, e0 + j) ? __ldcs(twin + e0 + j) : kNoHe;
   }
 #pragma unroll
   for (int k = 0; k < kIt; ++k) {
     const int j = threadIdx.x * kIt + k;
-    const int32_t e = e0 + j, tw = tws[k];
-    if (tw < e || tw >= e0 + 3 * nt) continue;  // frontier; once per pair; cross-tile pairs: k_uf_hook
-    int32_t a = j / 3, b = (tw - e0) / 3;
+    const hid e = e0 + j, tw = tws[k];
+    if (tw < e || tw >= e0 + 3 * nt) continue;  // frontier (kNoHe); once per pair; cross-tile pairs: k_uf_hook
+    int32_t a = j / 3, b = (int32_t)((tw - e0) / 3);
     while (true) {
       a = uf_find_s(p, a);
       b = uf_find_s(p, b);
@@ -113,19 +113,19 @@ __global__ void __launch_bounds__(kUfThreads) k_uf_local(int64_t T, const int32_
 
 // the cross-tile pairs: both halves of each are in k_tile's leftover lists (tile t:
 // entries [3 * kBuildTileTris * t, + cnt_ld[2t]) of left_e); one block per tile segment
-__global__ void k_uf_hook(int64_t ntiles, const int32_t* __restrict__ cnt_ld, const int32_t* __restrict__ left_e,
-                          const int32_t* __restrict__ twin, const uint32_t* __restrict__ F1, int32_t* parent,
+__global__ void k_uf_hook(int64_t ntiles, const int32_t* __restrict__ cnt_ld, const hid* __restrict__ left_e,
+                          const hid* __restrict__ twin, const uint32_t* __restrict__ F1, int32_t* parent,
                           const DevCounters* ctr) {
   if (ctr->status) return;
   for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
     const int32_t n = cnt_ld[2 * tile];
     const int64_t base = 3 * (int64_t)kBuildTileTris * tile;
     for (int32_t k = threadIdx.x; k < n; k += blockDim.x) {
-      const int32_t e = left_e[base + k];
+      const hid e = left_e[base + k];
       if (bit_of(F1, e)) continue;  // frontier (incl. the border ones)
-      const int32_t tw = twin[e];
+      const hid tw = twin[e];
       if (tw < e) continue;  // once per pair, from its lower half
-      int32_t a = e / 3, b = tw / 3;
+      int32_t a = (int32_t)(e / 3), b = (int32_t)(tw / 3);
       while (true) {
         a = uf_find(parent, a);
         b = uf_find(parent, b);
@@ -137,12 +137,12 @@ __global__ void k_uf_hook(int64_t ntiles, const int32_t* __restrict__ cnt_ld, co
   }
 }
 
-__global__ void k_uf_seed(const int32_t* __restrict__ seeds, int32_t* parent, int32_t* __restrict__ slot,
+__global__ void k_uf_seed(const hid* __restrict__ seeds, int32_t* parent, int32_t* __restrict__ slot,
                           const DevCounters* ctr) {
   if (ctr->status) return;
   const int32_t P = ctr->P;
   for (int32_t p = blockIdx.x * blockDim.x + threadIdx.x; p < P; p += gridDim.x * blockDim.x)
-    atomicMin(slot + uf_find(parent, seeds[p] / 3), p);
+    atomicMin(slot + uf_find(parent, (int32_t)(seeds[p] / 3)), p);
 }
 
 __global__ void k_uf_out(int64_t T, int32_t* parent, const int32_t* __restrict__ slot, int32_t* __restrict__ out,

@@ -30,7 +30,10 @@ EXPORTS = (
     "polylla_run_host", "polylla_destroy", "polylla_status_string", "polylla_launch_count",
     "polylla_profile_enable", "polylla_profile_read", "polylla_get_triangle_polygons",
     "polylla_check_manifold", "polylla_get_triangle_regions", "polylla_label_generate_paper",
+    "polylla_workspace_bytes_ex", "polylla_build_halfedges_ex",
 )
+
+WS_STAGING = 1  # POLYLLA_WS_STAGING
 
 
 class PolyllaError(RuntimeError):
@@ -79,6 +82,12 @@ def lib():
         L.polylla_workspace_bytes.argtypes = [i64, i64]
         L.polylla_build_halfedges.restype = ctypes.c_int
         L.polylla_build_halfedges.argtypes = [vp, i64, vp, i64, vp, ctypes.c_size_t, vp, ctypes.POINTER(vp)]
+        if hasattr(L, "polylla_build_halfedges_ex"):  # (older builds, loaded for A/B timing, lack it)
+            L.polylla_workspace_bytes_ex.restype = ctypes.c_size_t
+            L.polylla_workspace_bytes_ex.argtypes = [i64, i64, i64, ctypes.c_uint32]
+            L.polylla_build_halfedges_ex.restype = ctypes.c_int
+            L.polylla_build_halfedges_ex.argtypes = [vp, i64, vp, i64, i64, ctypes.c_uint32, vp, ctypes.c_size_t,
+                                                     vp, ctypes.POINTER(vp)]
         for n in ("polylla_label", "polylla_generate", "polylla_check_manifold", "polylla_label_generate_paper"):
             getattr(L, n).restype = ctypes.c_int
             getattr(L, n).argtypes = [vp, vp]
@@ -142,22 +151,38 @@ class Context:
             destroy(self)
 
 
-def workspace_bytes(n_vertices: int, n_triangles: int) -> int:
-    return int(lib().polylla_workspace_bytes(n_vertices, n_triangles))
+def workspace_bytes(n_vertices: int, n_triangles: int, max_border: int | None = None, staging: bool = True) -> int:
+    """polylla_workspace_bytes, or polylla_workspace_bytes_ex when a border bound is given
+    (or staging=False): the smaller layout of the capacity path."""
+    if max_border is None and staging:
+        return int(lib().polylla_workspace_bytes(n_vertices, n_triangles))
+    mb = 3 * n_triangles if max_border is None else max_border
+    return int(lib().polylla_workspace_bytes_ex(n_vertices, n_triangles, mb, WS_STAGING if staging else 0))
 
 
-def alloc_workspace(n_vertices: int, n_triangles: int, device="cuda") -> torch.Tensor:
-    return torch.empty(workspace_bytes(n_vertices, n_triangles), dtype=torch.uint8, device=device)
+def alloc_workspace(n_vertices: int, n_triangles: int, device="cuda", max_border: int | None = None,
+                    staging: bool = True) -> torch.Tensor:
+    return torch.empty(workspace_bytes(n_vertices, n_triangles, max_border, staging), dtype=torch.uint8,
+                       device=device)
 
 
-def build_halfedges(xy: torch.Tensor, tri: torch.Tensor, workspace: torch.Tensor, stream=None) -> Context:
+def build_halfedges(xy: torch.Tensor, tri: torch.Tensor, workspace: torch.Tensor, stream=None,
+                    max_border: int | None = None, staging: bool = True) -> Context:
+    """polylla_build_halfedges; with a border bound (or staging=False) polylla_build_halfedges_ex
+    over a workspace from alloc_workspace(..., max_border, staging) (the same arguments)."""
     if not (xy.is_cuda and tri.is_cuda and workspace.is_cuda):
         raise ValueError("xy, tri and workspace must be CUDA tensors")
     if xy.dtype != torch.float64 or tri.dtype != torch.int32 or not xy.is_contiguous() or not tri.is_contiguous():
         raise ValueError("xy must be contiguous float64 [V,2], tri contiguous int32 [T,3]")
     h = ctypes.c_void_p()
-    rc = lib().polylla_build_halfedges(_ptr(xy), xy.shape[0], _ptr(tri), tri.shape[0], _ptr(workspace),
-                                       workspace.numel(), _stream(stream), ctypes.byref(h))
+    if max_border is None and staging:
+        rc = lib().polylla_build_halfedges(_ptr(xy), xy.shape[0], _ptr(tri), tri.shape[0], _ptr(workspace),
+                                           workspace.numel(), _stream(stream), ctypes.byref(h))
+    else:
+        mb = 3 * tri.shape[0] if max_border is None else max_border
+        rc = lib().polylla_build_halfedges_ex(_ptr(xy), xy.shape[0], _ptr(tri), tri.shape[0], mb,
+                                              WS_STAGING if staging else 0, _ptr(workspace), workspace.numel(),
+                                              _stream(stream), ctypes.byref(h))
     _check(rc, "polylla_build_halfedges")
     return Context(h, xy, tri, workspace)
 
