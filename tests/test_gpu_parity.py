@@ -401,27 +401,35 @@ def test_config5_jittered_full():
     assert_parity(xy, tri, stages=False, invariants=False)
 
 
+def u32(t):
+    """An int32 tensor of unsigned 32-bit half-edge ids / offsets (include/polylla.h) as int64."""
+    return t.long() & 0xFFFFFFFF
+
+
 def device_invariants(xy, tri, origin, twin, nxt, offsets, loops, seeds, chunk=1 << 26):
     """Invariants that hold at any size (north_star / SPEC.md L187-193), evaluated on the
-    device with plain torch ops in chunks (test infrastructure).  Returns P."""
+    device with plain torch ops in chunks (test infrastructure).  Half-edge ids and
+    offsets are read as unsigned (H may exceed 2^31, NEXT-3).  Returns P."""
     T = tri.shape[0]
     H = origin.numel()
     dev = origin.device
     for a in range(0, H, chunk):
         b = min(H, a + chunk)
         ids = torch.arange(a, b, device=dev)
-        tw = twin[a:b].long()
-        assert torch.equal(twin[tw].long(), ids) and not torch.any(tw == ids)   # twin involution
-        assert torch.equal(origin[nxt[a:b].long()], origin[tw])                 # origin(next e) = target(e)
+        tw = u32(twin[a:b])
+        assert torch.equal(u32(twin[tw]), ids) and not torch.any(tw == ids)     # twin involution
+        assert torch.equal(origin[u32(nxt[a:b])], origin[tw])                    # origin(next e) = target(e)
     P = seeds.numel()
-    off = offsets.long()
+    off = u32(offsets)
     assert int(off[0]) == 0 and int(off[-1]) == loops.numel() and bool(torch.all(off[1:] > off[:-1]))
-    assert bool(torch.all(seeds[1:] > seeds[:-1])) and bool(torch.all(seeds < 3 * T))
+    sdall = u32(seeds)
+    assert bool(torch.all(sdall[1:] > sdall[:-1])) and bool(torch.all(sdall < 3 * T))
+    del sdall
     poly_area = 0.0
     xyd = xy.double()
     for a in range(0, P, chunk):
         b = min(P, a + chunk)
-        sd = seeds[a:b].long()
+        sd = u32(seeds[a:b])
         o0, o1 = off[a:b], off[a + 1:b + 1]
         lens = o1 - o0
         assert torch.equal(loops[o0].long(), origin[sd].long())                 # loops start at origin[seed]
@@ -437,7 +445,7 @@ def device_invariants(xy, tri, origin, twin, nxt, offsets, loops, seeds, chunk=1
             assert torch.equal(origin[xi].long(), loops[o0[live] + i].long())
             assert not torch.any(nxt[xi] == twin[xi])
             assert bool(torch.all(xi >= sd[live]))
-            x[live] = nxt[xi].long()
+            x[live] = u32(nxt[xi])
             cur = px[live]
             nx_pt = torch.where((lens[live] > i + 1).unsqueeze(1), xyd[origin[x[live]].long()], first[live])
             area[live] += cur[:, 0] * nx_pt[:, 1] - nx_pt[:, 0] * cur[:, 1]
