@@ -177,8 +177,7 @@ def alg_bytes(T, V, P, L, c=None):
     """Algorithmic bytes per launch of each kernel group (DESIGN.md section 6 states each
     model).  "pipeline" is SURVEY.md 8(d)'s B_alg = 60T + 16V + 12L + 4P, the method's
     compulsory HBM traffic for one mesh; the group models split the same accounting over
-    the kernels (what each must read or write once), plus the FP32 coordinate copy that
-    this design adds (k_xy32, not part of B_alg).  c: the mesh's polylla counts."""
+    the kernels (what each must read or write once).  c: the mesh's polylla counts."""
     c = c or {}
     n_left, n_def = c.get("n_leftover", 0), c.get("n_deferred", 0)
     n_sdef, tips, B = c.get("n_seed_deferred", 0), c.get("n_tips", 0), c.get("n_border", 0)
@@ -186,11 +185,9 @@ def alg_bytes(T, V, P, L, c=None):
     mean_loop = L / P if P else 0.0
     return {
         "pipeline": 60 * T + 16 * V + 12 * L + 4 * P,
-        # 16 B per vertex in, 8 B out
-        "k_xy32": 24 * V,
-        # B_alg's build rows: tri in (12T), origin/twin/next out (36T), the coordinates once
-        # (the 8-B FP32 copy; the FP64 array is read only for the few undecided triangles)
-        "k_tile": 48 * T + 8 * V,
+        # B_alg's build rows: tri in (12T), origin/twin/next out (36T),
+        # the FP64 coordinates once (16V)
+        "k_tile": 48 * T + 16 * V,
         # per leftover: key + id in (12 B), twin out (4 B), border ranking re-reads id + twin (8 B)
         "k_left_match": 24 * n_left,
         # per border half-edge: blist, twin[e], origin[target] in; twin[e], twin[b], origin[b], vmap out
