@@ -40,8 +40,9 @@ constexpr int kTriIters = (kTileTris + kTileThreads - 1) / kTileThreads;  // 768
 static_assert(kTileThreads % 32 == 0 && (kTileTris - (kTriIters - 1) * kTileThreads) % 32 == 0,
               "warp-uniform last triangle iteration");
 static_assert(4 * kTriIters <= 32, "per-lane pending bit masks");
-constexpr int kHeIters = kTileHE / kTileThreads;                           // 768: 8 exactly
-static_assert(kTileHE % kTileThreads == 0 && kTileThreads % 3 != 2, "half-edge loops: q_step below");
+constexpr int kHeIters = (kTileHE + kTileThreads - 1) / kTileThreads;     // 768: 8 exactly
+constexpr bool kHePartial = kTileHE % kTileThreads != 0;                  // (other thread counts)
+static_assert(kTileThreads % 3 != 2 && (kTileHE % kTileThreads) % 32 == 0, "half-edge loops: q_step below");
 // quad of half-edge j + kTileThreads from the quad q of j (no division): 768 = 3 * 256
 // -> q + 1024; 1024 = 3 * 341 + 1 -> q + 1365, skipping the padding slot k = 3
 constexpr int kQStep = 4 * (kTileThreads / 3) + kTileThreads % 3;
@@ -453,6 +454,7 @@ __device__ __forceinline__ void tile_body(
 #pragma unroll 4
     for (int i = 0; i < kHeIters; ++i, q = q_step(q)) {
       const int j = tid + i * kTileThreads;
+      if (kHePartial && j - lane >= kTileHE) break;  // (warp-uniform)
       bool sd = false, left = false;
       if (FULL || j < nhe) {
         const int k = q & 3, t = q >> 2;
@@ -611,7 +613,7 @@ __device__ __forceinline__ void tile_body(
 #pragma unroll 4
     for (int i = 0; i < kHeIters; ++i, q = q_step(q)) {
       const int j = tid + i * kTileThreads;
-      if (!FULL && j >= nhe) break;
+      if ((!FULL || kHePartial) && j >= nhe) break;
       const int32_t nl = nx_q[q];
       if (nl != -1) __stcs(next + e0 + j, (hid)(e0 + j_of(nl == -2 ? tw_s[q] : nl)));
     }
@@ -623,10 +625,10 @@ __device__ __forceinline__ void tile_body(
   // a deferred half-edge or a barrier tip (repaired later) are handed to the global
   // seed walk (bit-vector SDB).  kSeedLanes threads per word take its seeds in turn.
   {
-    static_assert(kTileThreads % kTileWords == 0, "threads per word");
-    constexpr int kSeedLanes = kTileThreads / kTileWords;  // 4
+    constexpr int kSeedLanes = kTileThreads / kTileWords;  // 4 (the threads past kSeedLanes * 192 idle)
+    static_assert(kSeedLanes >= 1, "threads per word");
     const int wsd = tid / kSeedLanes, sub = tid % kSeedLanes;
-    uint32_t sb = Sw[wsd];
+    uint32_t sb = wsd < kTileWords ? Sw[wsd] : 0u;
     for (int k = 0; k < sub && sb; ++k) sb &= sb - 1;
     while (sb) {
       const int32_t sj = wsd * 32 + __ffs(sb) - 1;
