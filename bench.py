@@ -59,6 +59,8 @@ def parse():
     ap.add_argument("--order", default="morton", choices=["morton", "shuffled"],
                     help="triangle order of configs 2/3 (sensitivity rows): generator Morton order or shuffled")
     ap.add_argument("--no-pcie", action="store_true")
+    ap.add_argument("--no-row-hint", action="store_true",
+                    help="grid configs: contiguous 2,048-triangle build tiles instead of the row-stride grid tiling")
     return ap.parse_args()
 
 
@@ -91,17 +93,17 @@ def workload(cfg: int, rank: int, world: int, device, order: str = "morton"):
                     f", 1 mesh per GPU")
         xy, tri = fn()
         m = dict(xy=torch.from_numpy(xy).to(device), tri=torch.from_numpy(tri).to(device), host=lambda: (xy, tri),
-                 xy_np=xy, tri_np=tri)
+                 xy_np=xy, tri_np=tri, row_stride=2 * 31 if cfg == 1 else 0)
         return name, "weak", [m]
     if cfg == 4:
         xy, tri = synth.grid_device(16000, 0.2, 4 + 1000 * rank, device=device)
         name = "config4: jittered 16000x16000 grid (256M vertices, 512M triangles), generated on device, 1 per GPU"
-        return name, "weak", [dict(xy=xy, tri=tri, host=None)]
+        return name, "weak", [dict(xy=xy, tri=tri, host=None, row_stride=2 * 15999)]
     metas = [mm for mm in batch.config5_meshes() if mm["index"] in set(batch.shard(64, rank, world))]
     out = []
     for mm in metas:
         xy, tri = synth.grid_device(mm["s"], mm["a"], mm["seed"], device=device)
-        out.append(dict(xy=xy, tri=tri, meta=mm,
+        out.append(dict(xy=xy, tri=tri, meta=mm, row_stride=2 * (mm["s"] - 1),
                         host=(lambda mm=mm: synth.grid(mm["s"], mm["a"], mm["seed"]))))
     name = ("config5: batch of 64 independent 2000x2000 grids (4M vertices each; 32 jittered a=0.2 + 32 regular "
             "Alg. 13), mesh i on rank i mod N, generated on device (excluded from timing)")
@@ -388,14 +390,19 @@ def main():
     name, scaling, meshes = workload(args.config, rank, ws, dev, args.order)
     Vmax = max(m["xy"].shape[0] for m in meshes)
     Tmax = max(m["tri"].shape[0] for m in meshes)
-    wsp = pp.alloc_workspace(Vmax, Tmax, dev)
+    # grid inputs (row-major Alg. 13 triangle lists) pass their row stride 2(s-1): the build
+    # then tiles 16-row x 128-triangle patches (polylla_build_halfedges_ex)
+    R0 = 0 if args.no_row_hint else meshes[0].get("row_stride", 0)
+    if R0:
+        name += f"; build tiles: 16 x 128-triangle patches (row stride hint {R0})"
+    wsp = pp.alloc_workspace(Vmax, Tmax, dev, row_stride=R0)
     offsets = torch.empty(Tmax + 1, dtype=torch.int32, device=dev)
     loops = torch.empty(3 * Tmax, dtype=torch.int32, device=dev)
     stream = torch.cuda.Stream(device=dev)
     launches = [0]
 
     def convert(m):
-        ctx = pp.build_halfedges(m["xy"], m["tri"], wsp, stream)
+        ctx = pp.build_halfedges(m["xy"], m["tri"], wsp, stream, row_stride=R0)
         pp.label(ctx, stream)
         pp.generate(ctx, stream)
         pp.get_polygons(ctx, offsets, loops, stream=stream)
@@ -416,28 +423,31 @@ def main():
     # mesh's k_tile; the step ends when both streams have finished (joined on `stream`).
     lanes = None
     if len(meshes) > 1:
-        lanes = [dict(stream=stream, ws=wsp, offsets=offsets, loops=loops),
-                 dict(stream=torch.cuda.Stream(device=dev), ws=pp.alloc_workspace(Vmax, Tmax, dev),
-                      offsets=torch.empty(Tmax + 1, dtype=torch.int32, device=dev),
-                      loops=torch.empty(3 * Tmax, dtype=torch.int32, device=dev))]
+        n_lanes = int(os.environ.get("POLYLLA_BENCH_LANES", "2"))
+        lanes = [dict(stream=stream, ws=wsp, offsets=offsets, loops=loops)] + [
+            dict(stream=torch.cuda.Stream(device=dev), ws=pp.alloc_workspace(Vmax, Tmax, dev, row_stride=R0),
+                 offsets=torch.empty(Tmax + 1, dtype=torch.int32, device=dev),
+                 loops=torch.empty(3 * Tmax, dtype=torch.int32, device=dev)) for _ in range(n_lanes - 1)]
 
         def step_batch():
             n = 0
             start = torch.cuda.Event()
             start.record(stream)
-            lanes[1]["stream"].wait_event(start)
+            for ln in lanes[1:]:
+                ln["stream"].wait_event(start)
             for i, m in enumerate(meshes):
-                ln = lanes[i % 2]
+                ln = lanes[i % len(lanes)]
                 s_ = ln["stream"]
-                ctx = pp.build_halfedges(m["xy"], m["tri"], ln["ws"], s_)
+                ctx = pp.build_halfedges(m["xy"], m["tri"], ln["ws"], s_, row_stride=R0)
                 pp.label(ctx, s_)
                 pp.generate(ctx, s_)
                 pp.get_polygons(ctx, ln["offsets"], ln["loops"], stream=s_)
                 n += pp.launch_count(ctx)
                 pp.destroy(ctx)
-            done = torch.cuda.Event()
-            done.record(lanes[1]["stream"])
-            stream.wait_event(done)
+            for ln in lanes[1:]:
+                done = torch.cuda.Event()
+                done.record(ln["stream"])
+                stream.wait_event(done)
             launches[0] = n
 
         step = step_batch
@@ -460,7 +470,7 @@ def main():
     graphs = None
     if not args.no_graph and len(meshes) == 1:
         # the whole step as one CUDA graph launch (same kernels, same stream order)
-        graphs = [pp.GraphStep(m["xy"], m["tri"], wsp, offsets, loops, stream) for m in meshes]
+        graphs = [pp.GraphStep(m["xy"], m["tri"], wsp, offsets, loops, stream, row_stride=R0) for m in meshes]
 
         def step():
             for g in graphs:
@@ -603,7 +613,7 @@ def main():
             "kernels_ms_per_step": {k: ms / prof_steps for k, (ms, _) in prof.items()},
             "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches[0] * args.steps,
             "launch_mode": ("cuda_graph (one graph launch per step)" if graphs else
-                            "eager, meshes alternating over two streams" if lanes else "eager"),
+                            f"eager, meshes alternating over {len(lanes)} streams" if lanes else "eager"),
             "clocks": clk.summary(),
             "mesh_table_head": table[:4].tolist(),
         }

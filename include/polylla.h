@@ -105,14 +105,15 @@ POLYLLA_API size_t polylla_workspace_bytes(int64_t n_vertices, int64_t n_triangl
 #define POLYLLA_WS_STAGING 1u /* hold the host-buffer staging regions of polylla_run_host */
 
 /* Bytes of device workspace for a mesh with at most max_border border half-edges
- * (0 <= max_border <= 3T; e.g. 4(s-1) for an s x s grid) and, with POLYLLA_WS_STAGING in
- * flags, run_host's staging.  polylla_workspace_bytes(V, T) ==
- * polylla_workspace_bytes_ex(V, T, 3T, POLYLLA_WS_STAGING).  The origin/twin/next
+ * (0 <= max_border <= 3T; e.g. 4(s-1) for an s x s grid), with POLYLLA_WS_STAGING in
+ * flags run_host's staging, and a row stride hint (0: none; see
+ * polylla_build_halfedges_ex).  polylla_workspace_bytes(V, T) ==
+ * polylla_workspace_bytes_ex(V, T, 3T, POLYLLA_WS_STAGING, 0).  The origin/twin/next
  * regions shrink from 6T to 3T + max_border entries and the staging (12T + 12T + 16V
  * bytes) is dropped: the capacity path for meshes near the HBM limit (SURVEY.md §8(f)
  * NEXT-3).  Returns 0 on invalid arguments.  Host-only. */
 POLYLLA_API size_t polylla_workspace_bytes_ex(int64_t n_vertices, int64_t n_triangles, int64_t max_border,
-                                              uint32_t flags);
+                                              uint32_t flags, int64_t row_stride);
 
 /* Half-edge construction (SPEC.md L45-53 build_from_triangles),
  * moved on-device, fused with the longest-edge labelling of Alg. 2 / Alg. 7
@@ -129,14 +130,19 @@ POLYLLA_API polylla_status polylla_build_halfedges(const double* xy, int64_t n_v
                                                    polylla_stream stream, polylla_ctx** ctx_out);
 
 /* polylla_build_halfedges over a workspace laid out by polylla_workspace_bytes_ex with
- * the same max_border and flags (the layout must match).  A mesh with more than
- * max_border border half-edges sets POLYLLA_E_WORKSPACE in the device status (returned
- * by polylla_get_counts); nothing is written past the bound.
- * polylla_build_halfedges(...) == polylla_build_halfedges_ex(..., 3T, POLYLLA_WS_STAGING, ...). */
+ * the same max_border, flags and row_stride (the layout must match).  A mesh with more
+ * than max_border border half-edges sets POLYLLA_E_WORKSPACE in the device status
+ * (returned by polylla_get_counts); nothing is written past the bound.
+ * row_stride: 0, or R > 0 when the triangle list is row-major with rows of R triangles
+ * (R divides T; e.g. R = 2(s-1) for the Alg. 13 grids): the build then
+ * tiles 16-row x 128-triangle patches instead of 2,048 consecutive triangles, so a tile
+ * cuts ~3% of its edges instead of a third (a performance hint only: the results are the
+ * same bits for any R; an R that does not divide T is ignored).
+ * polylla_build_halfedges(...) == polylla_build_halfedges_ex(..., 3T, POLYLLA_WS_STAGING, 0, ...). */
 POLYLLA_API polylla_status polylla_build_halfedges_ex(const double* xy, int64_t n_vertices, const int32_t* tri,
                                                       int64_t n_triangles, int64_t max_border, uint32_t flags,
-                                                      void* workspace, size_t workspace_bytes, polylla_stream stream,
-                                                      polylla_ctx** ctx_out);
+                                                      int64_t row_stride, void* workspace, size_t workspace_bytes,
+                                                      polylla_stream stream, polylla_ctx** ctx_out);
 
 /* Exact non-manifold-edge check (SPEC.md L49 NonManifoldEdge), opt-in.  The build
  * detects an edge in more than two triangles (or twice in one direction) when all of

@@ -57,11 +57,12 @@ __device__ __forceinline__ int q_step(int q) {
 //   slot  u16[kTileSlots] 32768  quad index of a lo->hi half-edge, 0xFFFF empty (dead after
 //                                P2: reused for succ u16[kTileQ])
 //   lc_s  u8[kTileTris]    2048
-//   nx_l  int16[kTileQ]  16384 | Sw, Cw, Wl, Lm, Dm, SDm u32[192] 4608   (P4-P6; quad-indexed local next)
+//   nx_l  int16[kTileQ]  16384 | Sw, Cw, Wl, Lm, Dm, SDm, Fw, Tw u32[192] 6144   (P4-P6; quad-indexed local next;
+//                                Fw, Tw: the frontier / tip words of a grid tile, flushed at the end)
 constexpr size_t kOffTw = kTileQ * 4, kOffSlot = kOffTw + kTileQ * 2, kOffLc = kOffSlot + kTileSlots * 2,
                  kOffNx = kOffLc + kTileTris,
-                 kNxBytes = kTileQ * 2 + 6 * (kTileHE / 8),                    // P4-P6 arrays (20,992 B)
-                 kTileSmem = kOffNx + kNxBytes;                                // 104,960 B -> 2 CTAs/SM
+                 kNxBytes = kTileQ * 2 + 8 * (kTileHE / 8),                    // P4-P6 arrays (22,528 B)
+                 kTileSmem = kOffNx + kNxBytes;                                // 106,496 B -> 2 CTAs/SM
 static_assert(2 * (kTileSmem + 1024) <= 228 * 1024, "two tiles per SM");
 constexpr unsigned long long kLeftDown = 1ull << 63;    // leftover key: set if origin > target
 constexpr unsigned long long kLeftPaired = 1ull << 31;  // leftover key: set once the key's slot holder is paired
@@ -191,6 +192,15 @@ template <bool FULL>
 __device__ __forceinline__ bool tri_ok(int i, int t, int nt) {
   return FULL ? (i < kTriIters - 1 || threadIdx.x < kTileTris - (kTriIters - 1) * kTileThreads) : t < nt;
 }
+// local triangle t of a partial tile: contiguous tiles hold a prefix (t < nt); grid tiles a
+// nrows x ncols corner of the 16 x 128 patch (t = 128 r + c)
+template <bool FULL, bool GRID>
+__device__ __forceinline__ bool tri_here(int i, int t, int nt, int nrows, int ncols) {
+  if (FULL) return tri_ok<true>(i, t, nt);
+  if (GRID) return (i < kTriIters - 1 || threadIdx.x < kTileTris - (kTriIters - 1) * kTileThreads) &&
+                   (t & (kGridTW - 1)) < ncols && (t >> kGridTWShift) < nrows;
+  return t < nt;
+}
 
 // One CTA per tile of kTileTris triangles.  Phases (PAPER.md section in brackets):
 //  P0 clear the hash; bulk L2 prefetch of the tile that starts when this one ends
@@ -213,9 +223,9 @@ __device__ __forceinline__ bool tri_ok(int i, int t, int nt) {
 //     bit-vector SDB; tips go to the bit-vector TB)
 // Loops are indexed so that no lane divides: triangle t = tid + 768 i, half-edge
 // j = tid + 768 i with quad q = q_of(tid) + 1024 i (768 = 3 * 256).
-template <bool FULL>
+template <bool FULL, bool GRID>
 __device__ __forceinline__ void tile_body(
-    unsigned char* smem_tile, const double2* __restrict__ xy, const int32_t* __restrict__ tri, int64_t V, int64_t T,
+    unsigned char* smem_tile, const Tiling tl, const double2* __restrict__ xy, const int32_t* __restrict__ tri, int64_t V, int64_t T,
     int32_t* __restrict__ origin, hid* __restrict__ twin, hid* __restrict__ next, uint8_t* __restrict__ lcode,
     uint32_t* __restrict__ F0, int64_t bv_stride, uint32_t* __restrict__ C,
     int32_t* __restrict__ len, int32_t* __restrict__ wlen, unsigned long long* __restrict__ left_key,
@@ -234,15 +244,25 @@ __device__ __forceinline__ void tile_body(
   uint32_t* Lm = reinterpret_cast<uint32_t*>(Wl + kTileWords);                   // leftover bits
   uint32_t* Dm = Lm + kTileWords;                                                // deferred bits
   uint32_t* SDm = Dm + kTileWords;                                               // deferred seed bits
+  uint32_t* Fw = SDm + kTileWords;                                               // (grid) frontier bits
+  uint32_t* Tw = Fw + kTileWords;                                                // (grid) barrier-tip bits
   // overlays of the slot area (after P2)
   uint16_t* succ = slot;
 
-  const int64_t f0 = tile * kTileTris;
-  const int64_t f0n = tile_next * kTileTris;  // this CTA's next tile (prefetched), if tile_next >= 0
-  const int nt = FULL ? kTileTris : (int)(T - f0 < kTileTris ? T - f0 : kTileTris);
+  const TileGeom tg_ = tile_geom(tl, T, tile);
+  const int64_t f0 = tg_.base;                // global triangle of local triangle 0
+  const int64_t seg0 = tg_.seg;               // the tile's list segment
+  const int nt = FULL ? kTileTris : GRID ? kTileTris : tg_.nrows;  // (grid: presence per triangle)
+  const int g_rows = GRID ? tg_.nrows : 0, g_cols = GRID ? tg_.ncols : 0;
   const int nhe = 3 * nt;
   const int64_t e0 = 3 * f0;
   const int tid = threadIdx.x, lane = tid & 31;
+  // local -> global: triangle, half-edge of a quad (grid tiles: rows of 128 triangles R apart)
+  auto gtri = [&](int t) -> int64_t {
+    return GRID ? f0 + (int64_t)(t >> kGridTWShift) * tl.R + (t & (kGridTW - 1)) : f0 + t;
+  };
+  auto ghe = [&](int q) -> int64_t { return GRID ? 3 * gtri(q >> 2) + (q & 3) : e0 + j_of(q); };
+  auto here = [&](int t) -> bool { return FULL || (GRID ? ((t & (kGridTW - 1)) < g_cols && (t >> kGridTWShift) < g_rows) : t < nt); };
 #ifdef POLYLLA_PHASE_TIMING
   long long t_phase_ = clock64();
 #endif
@@ -250,13 +270,15 @@ __device__ __forceinline__ void tile_body(
   // ---- P0: clear the hash slots and the twins (the claims of P1 need the barrier); P1
   // reads the raw triangles straight from global memory (the tile was bulk-prefetched
   // into L2 by the CTA before; staging it in shared memory first measured 1% slower)
-  const int32_t* raw = tri + e0;
+  const int32_t* raw = tri + e0;  // (contiguous tiles)
   for (int i = tid; i < kTileSlots / 8; i += kTileThreads)
     reinterpret_cast<uint4*>(slot)[i] = make_uint4(0xFFFFFFFFu, 0xFFFFFFFFu, 0xFFFFFFFFu, 0xFFFFFFFFu);
   for (int i = tid; i < kTileQ / 2; i += kTileThreads) reinterpret_cast<uint32_t*>(tw_s)[i] = 0xFFFFFFFFu;
-  if (tid == 0 && tile_next >= 0) {  // the next tile's triangles -> L2 (TMA bulk prefetch)
-    const int64_t nn = T - f0n < kTileTris ? T - f0n : kTileTris;
-    const int32_t* pn = tri + 3 * f0n;
+  const TileGeom tn_ = tile_next >= 0 ? tile_geom(tl, T, tile_next) : TileGeom{0, 0, 0, 0};
+  const int64_t f0n = tn_.base;  // this CTA's next tile (prefetched), if tile_next >= 0
+  if (tile_next >= 0 && (GRID ? tid < tn_.nrows : tid == 0)) {  // the next tile's triangles -> L2 (TMA bulk prefetch)
+    const int64_t nn = GRID ? tn_.ncols : (T - f0n < kTileTris ? T - f0n : kTileTris);
+    const int32_t* pn = tri + 3 * (f0n + (GRID ? tid * tl.R : 0));  // (grid: one row per thread)
     const uint32_t bytes = (uint32_t)((3 * nn * 4) & ~int64_t(15));
     if (bytes && (reinterpret_cast<uintptr_t>(pn) & 15) == 0)
       asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(pn), "r"(bytes));
@@ -266,8 +288,9 @@ __device__ __forceinline__ void tile_body(
 #pragma unroll
   for (int i = 0; i < kTriIters; ++i) {
     const int t = tid + i * kTileThreads;
-    if (tri_ok<FULL>(i, t, nt)) {
-      ids[i][0] = raw[3 * t]; ids[i][1] = raw[3 * t + 1]; ids[i][2] = raw[3 * t + 2];
+    if (tri_here<FULL, GRID>(i, t, nt, g_rows, g_cols)) {
+      const int32_t* rt = GRID ? tri + 3 * gtri(t) : raw + 3 * t;
+      ids[i][0] = rt[0]; ids[i][1] = rt[1]; ids[i][2] = rt[2];
     } else {
       ids[i][0] = ids[i][1] = ids[i][2] = 0;
     }
@@ -302,7 +325,7 @@ __device__ __forceinline__ void tile_body(
     if (d1 > dk) { k = 1; dk = d1; }
     if (d2 > dk) { k = 2; }
     lc_s[t] = (uint8_t)k;
-    lcode[f0 + t] = (uint8_t)k;
+    lcode[gtri(t)] = (uint8_t)k;
     tri_q4[t] = make_int4(a, b, c, a);
     if (a < b) st_relaxed16(slot + tile_pos(a, b), 4 * t);
     if (b < c) st_relaxed16(slot + tile_pos(b, c), 4 * t + 1);
@@ -311,7 +334,7 @@ __device__ __forceinline__ void tile_body(
 #pragma unroll
   for (int i = 0; i < kTriIters; ++i) {
     const int t = tid + i * kTileThreads;
-    if (!tri_ok<FULL>(i, t, nt)) continue;
+    if (!tri_here<FULL, GRID>(i, t, nt, g_rows, g_cols)) continue;
     orient_tri(t, ids[i][0], ids[i][1], ids[i][2]);
   }
   flips = __reduce_add_sync(0xffffffffu, flips);
@@ -327,14 +350,14 @@ __device__ __forceinline__ void tile_body(
   // bulk-prefetched in P0), so that tile's P1 gathers hit L2 instead of HBM: one triangle
   // per thread per pass (P2, P2c, P3), its ids loaded at the start of the pass and the
   // prefetches issued at its end (the loads' latency hides behind the pass)
-  const int64_t nn_pf = tile_next >= 0 ? (T - f0n < kTileTris ? T - f0n : kTileTris) : 0;
+  const int64_t nn_pf = tile_next >= 0 ? (GRID ? kTileTris : (T - f0n < kTileTris ? T - f0n : kTileTris)) : 0;
   int32_t pf_v[3];
   bool pf_ok = false;
   auto pf_load = [&](int i) {
     const int t = tid + i * kTileThreads;
-    pf_ok = t < nn_pf;
+    pf_ok = t < nn_pf && (!GRID || ((t & (kGridTW - 1)) < tn_.ncols && (t >> kGridTWShift) < tn_.nrows));
     if (pf_ok) {  // volatile: issued here, not sunk next to their use at the end of the pass
-      const int32_t* src = tri + 3 * (f0n + t);
+      const int32_t* src = tri + 3 * (GRID ? f0n + (int64_t)(t >> kGridTWShift) * tl.R + (t & (kGridTW - 1)) : f0n + t);
       asm volatile("ld.global.nc.b32 %0, [%3];\n\tld.global.nc.b32 %1, [%3+4];\n\tld.global.nc.b32 %2, [%3+8];"
                    : "=r"(pf_v[0]), "=r"(pf_v[1]), "=r"(pf_v[2]) : "l"(src));
     }
@@ -360,7 +383,7 @@ __device__ __forceinline__ void tile_body(
 #pragma unroll
     for (int i = 0; i < kTriIters; ++i) {
       const int t = tid + i * kTileThreads;
-      if (!tri_ok<FULL>(i, t, nt)) continue;
+      if (!tri_here<FULL, GRID>(i, t, nt, g_rows, g_cols)) continue;
       const int4 v = tri_q4[t];
       const int32_t vs[4] = {v.x, v.y, v.z, v.w};
       // the three home slots, then the candidates' vertices, then the decisions (loads
@@ -456,7 +479,7 @@ __device__ __forceinline__ void tile_body(
       const int j = tid + i * kTileThreads;
       if (kHePartial && j - lane >= kTileHE) break;  // (warp-uniform)
       bool sd = false, left = false;
-      if (FULL || j < nhe) {
+      if (FULL || (GRID ? here(q >> 2) : j < nhe)) {
         const int k = q & 3, t = q >> 2;
         // loads issued together: own twin / vertex / Lcode, then the twin's back-pointer and Lcode
         const int32_t tq = tw_s[q];
@@ -466,8 +489,14 @@ __device__ __forceinline__ void tile_body(
         const int32_t back = tw_s[tqs];
         const int32_t lt = lc_s[tqs >> 2];
         if (tq >= 0 && back != q) nm = ST_NONMANIFOLD_EDGE;  // twin claimed twice (edge in > 2 triangles)
-        __stcs(origin + e0 + j, org);
-        __stcs(twin + e0 + j, tq >= 0 ? (hid)(e0 + j_of(tq)) : kNoHe);
+        if (GRID) {
+          const int64_t ge = ghe(q);
+          __stcs(origin + ge, org);
+          __stcs(twin + ge, tq >= 0 ? (hid)ghe(tq) : kNoHe);
+        } else {
+          __stcs(origin + e0 + j, org);
+          __stcs(twin + e0 + j, tq >= 0 ? (hid)(e0 + j_of(tq)) : kNoHe);
+        }
         const bool front = lq != k && lt != (tq & 3);  // neither half the longest edge of its triangle
         succ[q] = (uint16_t)(tq < 0 ? (q | kSuccUnknown) : front ? (q | kSuccFront) : next_q(tq));
         sd = tq >= 0 && lq == k && lt == (tq & 3) && q < tq;  // terminal edge, smaller id
@@ -478,7 +507,7 @@ __device__ __forceinline__ void tile_body(
       // lane 0: Sw, lane 1: Lm (shared); lane 2: the global S
       if (lane < 2) {
         s_dst[wl] = lane == 0 ? sw : lw;
-      } else if (lane == 2 && (FULL || j - lane < nhe)) {
+      } else if (!GRID && lane == 2 && (FULL || j - lane < nhe)) {  // (grid tiles: flushed at the end)
         F0[2 * bv_stride + (e0 >> 5) + wl] = sw;
       }
     }
@@ -500,7 +529,7 @@ __device__ __forceinline__ void tile_body(
 #pragma unroll
     for (int i = 0; i < kTriIters; ++i) {
       const int t = tid + i * kTileThreads;
-      if (!tri_ok<FULL>(i, t, nt)) continue;
+      if (!tri_here<FULL, GRID>(i, t, nt, g_rows, g_cols)) continue;
       const uint2 s2 = *reinterpret_cast<const uint2*>(src + 4 * t);
       const uint32_t sc[3] = {s2.x & 0xFFFFu, s2.x >> 16, s2.y & 0xFFFFu};
       uint32_t d[3];
@@ -521,7 +550,7 @@ __device__ __forceinline__ void tile_body(
     if (!(i < kTriIters - 1 || tid < kTileTris - (kTriIters - 1) * kTileThreads)) continue;
     const int t = tid + i * kTileThreads;
     uint32_t packed = 0;  // field 0: frontier, 1: tip, 2: deferred
-    if (FULL || t < nt) {
+    if (here(t)) {
       const uint2 s2 = *reinterpret_cast<const uint2*>(succ + 4 * t);
       const uint2 tw2 = *reinterpret_cast<const uint2*>(tw_s + 4 * t);
       const uint32_t sc[3] = {s2.x & 0xFFFFu, s2.x >> 16, s2.y & 0xFFFFu};
@@ -559,6 +588,9 @@ __device__ __forceinline__ void tile_body(
     if (lane < 12) {
       const int r = lane_ty == 0 ? 1 : lane_ty == 1 ? 2 : lane_ty == 2 ? 4 : 5;  // Cw, Wl, Dm, SDm
       Sw[r * kTileWords + wl0 + lane_m] = lane_ty == 2 ? pick_m(d0w, d1w, d2w) : 0u;
+    } else if (GRID) {  // the frontier and tip words, flushed at the end
+      if (lane < 15) Fw[wl0 + lane_m] = pick_m(f0w, f1w, f2w);
+      else if (lane >= 18 && lane < 21) Tw[wl0 + lane_m] = pick_m(t0w, t1w, t2w);
     } else if (lane < 21 && (FULL || 32 * (wl0 + lane_m) < nhe)) {
       const int g = lane_ty == 4 ? 0 : lane_ty == 5 ? 1 : 3;  // F0, F1, TB
       F0[g * bv_stride + (e0 >> 5) + wl0 + lane_m] = lane_ty == 6 ? pick_m(t0w, t1w, t2w) : pick_m(f0w, f1w, f2w);
@@ -589,7 +621,7 @@ __device__ __forceinline__ void tile_body(
       if (bl + il) atomicAdd(&ctr->n_left, bl + il);  // totals (result unused: a reduction)
       if (bd + id) atomicAdd(&ctr->n_def, bd + id);
     }
-    int64_t pl = e0 + bl + il - cl, pd = e0 + bd + id - cd;
+    int64_t pl = seg0 + bl + il - cl, pd = seg0 + bd + id - cd;
     while (lw) {
       const int j = tid * 32 + __ffs(lw) - 1;
       lw &= lw - 1;
@@ -597,10 +629,11 @@ __device__ __forceinline__ void tile_body(
       const int32_t o = tri_q[q], tg = tri_q[q + 1];
       const uint64_t lo = (uint32_t)min(o, tg), hi = (uint32_t)max(o, tg);
       left_key[pl] = (lo << 32) | hi | (o > tg ? kLeftDown : 0ull);  // undirected key + direction bit
-      left_e[pl++] = (hid)(e0 + j);
+      left_e[pl++] = (hid)(GRID ? ghe(q) : e0 + j);
     }
     while (dw) {
-      def_e[pd++] = (hid)(e0 + tid * 32 + __ffs(dw) - 1);
+      const int j = tid * 32 + __ffs(dw) - 1;
+      def_e[pd++] = (hid)(GRID ? ghe(q_of(j)) : e0 + j);
       dw &= dw - 1;
     }
   }
@@ -613,6 +646,13 @@ __device__ __forceinline__ void tile_body(
 #pragma unroll 4
     for (int i = 0; i < kHeIters; ++i, q = q_step(q)) {
       const int j = tid + i * kTileThreads;
+      if (GRID) {
+        if (j >= kTileHE) break;
+        if (!here(q >> 2)) continue;
+        const int32_t nl = nx_q[q];
+        if (nl != -1) __stcs(next + ghe(q), (hid)ghe(nl == -2 ? tw_s[q] : nl));
+        continue;
+      }
       if ((!FULL || kHePartial) && j >= nhe) break;
       const int32_t nl = nx_q[q];
       if (nl != -1) __stcs(next + e0 + j, (hid)(e0 + j_of(nl == -2 ? tw_s[q] : nl)));
@@ -650,10 +690,14 @@ __device__ __forceinline__ void tile_body(
         } while (y != x);
       }
       if (ok) {
+        const int64_t gmn = ghe(mn);  // (the loop minimum: quad and half-edge orders agree)
         mn = j_of(mn);
-        len[e0 + mn] = n;
+        len[gmn] = n;
         const uint32_t bit = 1u << (mn & 31);
-        if (!(atomicOr(&Cw[mn >> 5], bit) & bit)) atomicAdd(&Wl[mn >> 5], n);  // first setter only
+        if (!(atomicOr(&Cw[mn >> 5], bit) & bit)) {  // first setter only
+          if (GRID) atomicAdd(&wlen[gmn >> 5], n);   // (grid: global words, zeroed before the build)
+          else atomicAdd(&Wl[mn >> 5], n);
+        }
       } else if (!tipped) {
         // (a loop through a barrier tip is split by the repair, and every piece borders a
         // middle edge whose two halves k_repair_mid seeds: this seed would add nothing).
@@ -667,7 +711,27 @@ __device__ __forceinline__ void tile_body(
   }
   __syncthreads();
   PHASE_MARK(6);
-  if (tid * 32 < nhe) {
+  if (GRID) {
+    // local word L = 12 r + m holds half-edges 32 m .. 32 m + 31 of triangle row r (384 per
+    // row): global bits 3 (base + r R) + 32 m onward, not word-aligned -> two atomicOr
+    // (the global words were zeroed before the build; neighbouring tiles share words)
+    if (tid < kTileWords && tid / 12 < g_rows) {
+      const int64_t gb = 3 * (f0 + (int64_t)(tid / 12) * tl.R) + 32 * (tid % 12);
+      const int64_t gw = gb >> 5;
+      const int sh = (int)(gb & 31);
+      auto put = [&](uint32_t* base, uint32_t v) {
+        if (!v) return;
+        atomicOr(base + gw, v << sh);
+        if (sh) atomicOr(base + gw + 1, v >> (32 - sh));
+      };
+      put(F0, Fw[tid]);
+      put(F0 + bv_stride, Fw[tid]);
+      put(F0 + 2 * bv_stride, Sw[tid]);
+      put(F0 + 3 * bv_stride, Tw[tid]);
+      put(C, Cw[tid]);
+      put(SDB, SDm[tid]);
+    }
+  } else if (tid * 32 < nhe) {
     const int64_t w = (e0 >> 5) + tid;
     C[w] = Cw[tid];
     wlen[w] = Wl[tid];
@@ -679,27 +743,35 @@ __device__ __forceinline__ void tile_body(
 // One CTA per tile; while it works it prefetches into L2 the triangles and vertex
 // coordinates of the tile that will start when it ends.  Full tiles take the specialised
 // body (constant trip counts, no bounds checks), the ragged last tile the generic one.
+template <bool GRID>
 __global__ void __launch_bounds__(kTileThreads, 2)
     k_tile(const double2* __restrict__ xy, const int32_t* __restrict__ tri, int64_t V, int64_t T,
            int32_t* __restrict__ origin, hid* __restrict__ twin, hid* __restrict__ next,
            uint8_t* __restrict__ lcode, uint32_t* __restrict__ F0, int64_t bv_stride, uint32_t* __restrict__ C, int32_t* __restrict__ len, int32_t* __restrict__ wlen,
            unsigned long long* __restrict__ left_key, hid* __restrict__ left_e, hid* __restrict__ def_e,
            uint32_t* __restrict__ SDB, int32_t* __restrict__ cnt_ld, DevCounters* ctr,
-           int64_t prefetch_dist, int64_t tile_base) {
+           int64_t prefetch_dist, int64_t tile_base, const Tiling tl) {
   extern __shared__ __align__(16) unsigned char smem_tile[];
-  const int64_t ntiles = (T + kTileTris - 1) / kTileTris;
+  const int64_t ntiles = GRID ? tl.ntiles : (T + kTileTris - 1) / kTileTris;
   // tiles [tile_base, tile_base + gridDim.x): all of them, or one chunk of an upload
   // pipeline (polylla_run_host)
   const int64_t tile = tile_base + sched_tile(blockIdx.x, gridDim.x);
   // the tile that starts about when this one ends (blocks are dispatched in index order,
   // kResident at a time): its data is prefetched into L2, which every SM shares
   const int64_t nxt = tile + prefetch_dist < ntiles ? tile + prefetch_dist : -1;
-  if ((tile + 1) * kTileTris <= T)
-    tile_body<true>(smem_tile, xy, tri, V, T, origin, twin, next, lcode, F0, bv_stride, C, len, wlen, left_key, left_e,
-                    def_e, SDB, cnt_ld, ctr, tile, nxt);
+  bool full;
+  if (GRID) {
+    const TileGeom g = tile_geom(tl, T, tile);
+    full = g.nrows == kGridTH && g.ncols == kGridTW;
+  } else {
+    full = (tile + 1) * kTileTris <= T;
+  }
+  if (full)
+    tile_body<true, GRID>(smem_tile, tl, xy, tri, V, T, origin, twin, next, lcode, F0, bv_stride, C, len, wlen,
+                          left_key, left_e, def_e, SDB, cnt_ld, ctr, tile, nxt);
   else
-    tile_body<false>(smem_tile, xy, tri, V, T, origin, twin, next, lcode, F0, bv_stride, C, len, wlen, left_key, left_e,
-                     def_e, SDB, cnt_ld, ctr, tile, nxt);
+    tile_body<false, GRID>(smem_tile, tl, xy, tri, V, T, origin, twin, next, lcode, F0, bv_stride, C, len, wlen,
+                           left_key, left_e, def_e, SDB, cnt_ld, ctr, tile, nxt);
 }
 
 #ifdef POLYLLA_PHASE_TIMING
@@ -753,16 +825,16 @@ __device__ __forceinline__ uint32_t left_home(uint32_t lo, uint32_t hi, unsigned
   if (!scale) return mix32(lo, hi) & mask;
   return ((uint32_t)(((unsigned long long)lo * scale) >> 32) + ((hi * 0x9E3779B1u) >> 30)) & mask;
 }
-__global__ void k_left_insert(DevCounters* ctr, int64_t ntiles, const int32_t* __restrict__ cnt_ld,
-                              unsigned long long* left_key, const hid* __restrict__ left_e,
-                              hid* twin, uint32_t* ehash) {
+__global__ void k_left_insert(DevCounters* ctr, int64_t ntiles, int64_t T, const Tiling tl,
+                              const int32_t* __restrict__ cnt_ld, unsigned long long* left_key,
+                              const hid* __restrict__ left_e, hid* twin, uint32_t* ehash) {
   if (ctr->status) return;
   const uint32_t mask = (uint32_t)ctr->hash_cap - 1;
   const unsigned long long scale = ctr->hash_scale;
   for (int64_t it = blockIdx.x; it < ntiles; it += gridDim.x) {
     const int64_t tile = sched_tile(it, ntiles);
     const int32_t n = cnt_ld[2 * tile];
-    const int64_t base = 3 * kTileTris * tile;
+    const int64_t base = tile_geom(tl, T, tile).seg;
     for (int32_t k = threadIdx.x; k < n; k += blockDim.x) {
       const int64_t i = base + k;  // < 3T <= 2^32 - 2: a slot value never equals kEmpty
       const unsigned long long kd = left_key[i], key = kd & ~kLeftDown;
@@ -907,6 +979,80 @@ __global__ void __launch_bounds__(kSegThreads)
   }
 }
 
+// Grid tiling: tile segments are not in ascending half-edge order, so the unmatched
+// leftovers are marked in the bit-vector BB (zeroed before the build) and ranked by bit
+// order (R9): per chunk of 192 words a popcount (k_bb_count, one warp per chunk), the
+// chunks' exclusive prefix (k_border_scan), then each chunk's bits in order (k_bb_emit).
+__global__ void k_bb_mark(DevCounters* ctr, int64_t ntiles, int64_t T, const Tiling tl,
+                          const int32_t* __restrict__ cnt_ld, const hid* __restrict__ left_e,
+                          const hid* __restrict__ twin, uint32_t* BB) {
+  if (ctr->status) return;
+  for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+    const int32_t n = cnt_ld[2 * tile];
+    const int64_t base = tile_geom(tl, T, tile).seg;
+    for (int32_t k = threadIdx.x; k < n; k += blockDim.x) {
+      const hid e = left_e[base + k];
+      if (twin[e] == kNoHe) atomicOr(&BB[e >> 5], 1u << (e & 31));
+    }
+  }
+}
+
+constexpr int kBBChunk = 192;  // words per chunk (6 per lane)
+__global__ void k_bb_count(DevCounters* ctr, int64_t n_words, int64_t nchunks, const uint32_t* __restrict__ BB,
+                           uint32_t* __restrict__ bcnt) {
+  if (ctr->status) return;
+  const int lane = threadIdx.x & 31;
+  const int64_t nw = (int64_t)gridDim.x * (blockDim.x >> 5);
+  for (int64_t ch = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); ch < nchunks; ch += nw) {
+    int c = 0;
+    for (int k = lane; k < kBBChunk; k += 32) {
+      const int64_t w = ch * kBBChunk + k;
+      if (w < n_words) c += __popc(BB[w]);
+    }
+    c = __reduce_add_sync(0xffffffffu, c);
+    if (lane == 0) bcnt[ch] = (uint32_t)c;
+  }
+}
+
+__global__ void k_bb_emit(DevCounters* ctr, int64_t n_words, int64_t nchunks, int64_t T3,
+                          const uint32_t* __restrict__ BB, const uint32_t* __restrict__ bbase, int32_t* origin,
+                          hid* twin, hid* vmap) {
+  if (ctr->status) return;
+  const int lane = threadIdx.x & 31;
+  constexpr int kWPL = kBBChunk / 32;
+  const int64_t nw = (int64_t)gridDim.x * (blockDim.x >> 5);
+  for (int64_t ch = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); ch < nchunks; ch += nw) {
+    uint32_t bw[kWPL];
+    int c = 0;
+#pragma unroll
+    for (int k = 0; k < kWPL; ++k) {
+      const int64_t w = ch * kBBChunk + kWPL * lane + k;
+      bw[k] = w < n_words ? BB[w] : 0u;
+      c += __popc(bw[k]);
+    }
+    int inc = c;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int a = __shfl_up_sync(0xffffffffu, inc, o);
+      if (lane >= o) inc += a;
+    }
+    uint32_t r = bbase[ch] + (uint32_t)(inc - c);
+#pragma unroll
+    for (int k = 0; k < kWPL; ++k) {
+      const int64_t w = ch * kBBChunk + kWPL * lane + k;
+      for (uint32_t b = bw[k]; b; b &= b - 1, ++r) {
+        const hid e = (hid)(w * 32 + __ffs(b) - 1);
+        const hid bh = (hid)(T3 + r);
+        const int32_t v = origin[next_in(e)];  // origin(b) = target(e)
+        twin[e] = bh;
+        twin[bh] = e;
+        origin[bh] = v;
+        vmap[v] = bh;
+      }
+    }
+  }
+}
+
 // next(b) = the border half-edge whose origin is target(b) = origin(twin(b)).  A vertex
 // with two outgoing border half-edges keeps only one of them in vmap: the other fails
 // the vmap[origin(b)] == b check (NON_MANIFOLD_VERTEX).
@@ -924,6 +1070,19 @@ __global__ void k_border_next(DevCounters* ctr, int64_t T3, const int32_t* __res
   }
 }
 
+Tiling make_tiling(int64_t T, int64_t R) {
+  Tiling g;
+  if (R > 0 && T % R == 0) {
+    g.R = R;
+    g.nrows = T / R;
+    g.ntc = (R + kGridTW - 1) / kGridTW;
+    g.ntiles = (g.nrows + kGridTH - 1) / kGridTH * g.ntc;
+  } else {
+    g.ntiles = (T + kTileTris - 1) / kTileTris;
+  }
+  return g;
+}
+
 // Per-device launch setup: the dynamic shared-memory attribute of k_tile belongs to each
 // device's context, so it is set once per device id (a relaxed bit-set under a mutex;
 // the SM count is cached next to it).
@@ -936,7 +1095,8 @@ static int device_setup(int* n_sm) {
   if (cudaGetDevice(&dev) != cudaSuccess) return -1;
   std::lock_guard<std::mutex> lk(g_dev_mu);
   if (dev >= 64 || !((g_dev_ready >> dev) & 1)) {
-    if (cudaFuncSetAttribute(k_tile, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kTileSmem) != cudaSuccess)
+    if (cudaFuncSetAttribute(k_tile<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kTileSmem) != cudaSuccess ||
+        cudaFuncSetAttribute(k_tile<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kTileSmem) != cudaSuccess)
       return -1;
     int sms = 0;
     if (cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess) return -1;
@@ -962,6 +1122,13 @@ static int64_t prefetch_distance(int n_sm) {
 // the start of a build: counters zeroed, per-device setup
 int launch_build_begin(Ctx* c, cudaStream_t s) {
   if (cudaMemsetAsync(c->ctr, 0, sizeof(DevCounters), s) != cudaSuccess) return -1;
+  if (c->tiling.R) {  // grid tiles OR their words into the bit-vectors (shared words): zero them
+    const size_t wb = (size_t)c->n_words * 4;
+    if (cudaMemsetAsync(c->F0, 0, (size_t)(c->TB - c->F0) * 4 + wb, s) != cudaSuccess ||
+        cudaMemsetAsync(c->C, 0, wb, s) != cudaSuccess || cudaMemsetAsync(c->SDB, 0, wb, s) != cudaSuccess ||
+        cudaMemsetAsync(c->wlen, 0, wb, s) != cudaSuccess || cudaMemsetAsync(c->BB, 0, wb, s) != cudaSuccess)
+      return -1;
+  }
   int n_sm = 0;
   return device_setup(&n_sm);
 }
@@ -975,15 +1142,16 @@ int launch_build_tiles(Ctx* c, cudaStream_t s, int64_t t0, int64_t t1) {
   const int64_t bv_stride = c->F1 - c->F0;  // F0, F1, S, TB are equally spaced (capi.cu layout)
   if (c->S - c->F1 != bv_stride || c->TB - c->S != bv_stride) return -1;
   prof_mark(s, "k_tile");
-  k_tile<<<(unsigned)(t1 - t0), kTileThreads, kTileSmem, s>>>(reinterpret_cast<const double2*>(c->xy), c->tri, c->V, c->T,
+  auto kt = c->tiling.R ? k_tile<true> : k_tile<false>;
+  kt<<<(unsigned)(t1 - t0), kTileThreads, kTileSmem, s>>>(reinterpret_cast<const double2*>(c->xy), c->tri, c->V, c->T,
                                                           c->origin, c->twin, c->next, c->lcode, c->F0, bv_stride, c->C,
                                                           c->len, c->wlen, c->left_key, c->left_e, c->def_e, c->SDB,
-                                                          c->cnt_ld, c->ctr, pf_dist, t0);
+                                                          c->cnt_ld, c->ctr, pf_dist, t0, c->tiling);
   return cudaGetLastError() == cudaSuccess ? 1 : -1;
 }
 
 int launch_build(Ctx* c, cudaStream_t s) {
-  const int64_t tiles = (c->T + kTileTris - 1) / kTileTris;
+  const int64_t tiles = c->tiling.ntiles;
   if (launch_build_begin(c, s) != 0) return -1;
   const int n = launch_build_tiles(c, s, 0, tiles);
   if (n < 0) return -1;
@@ -994,7 +1162,7 @@ int launch_build(Ctx* c, cudaStream_t s) {
 // everything after the tiles: leftover match, border half-edges and their chain
 int launch_build_rest(Ctx* c, cudaStream_t s) {
   int n = 0;
-  const int64_t tiles = (c->T + kTileTris - 1) / kTileTris;
+  const int64_t tiles = c->tiling.ntiles;
   const int grid = 148 * 32;  // enough threads for ~1 leftover each on 10M-vertex meshes (latency-bound)
   prof_mark(s, "k_left_match");
   uint32_t* ehash = static_cast<uint32_t*>(c->ehash);
@@ -1004,15 +1172,28 @@ int launch_build_rest(Ctx* c, cudaStream_t s) {
 #endif
   const unsigned seg_grid = (unsigned)(tiles < 148 * 16 ? tiles : 148 * 16);
   const unsigned left_grid = (unsigned)(tiles < 148 * (4096 / POLYLLA_LEFT_THREADS) ? tiles : 148 * (4096 / POLYLLA_LEFT_THREADS));
-  k_left_insert<<<left_grid, POLYLLA_LEFT_THREADS, 0, s>>>(c->ctr, tiles, c->cnt_ld, c->left_key, c->left_e, c->twin, ehash);
-  hid* blist = reinterpret_cast<hid*>(c->left_key);  // dead after k_left_insert
-  k_border_rank<<<seg_grid, kSegThreads, 0, s>>>(c->ctr, tiles, c->cnt_ld, c->left_e, c->twin, blist, c->bcnt);
-  n += 3;
-  prof_mark(s, "k_border_scan");
-  k_border_scan<<<1, kBorderScanThreads, 0, s>>>(c->ctr, tiles, 3 * c->T, c->Bmax, c->bcnt);
-  k_border_emit<<<seg_grid, kSegThreads, 0, s>>>(c->ctr, tiles, 3 * c->T, blist, c->bcnt, c->origin, c->twin,
-                                                 c->vmap);
-  n += 2;
+  k_left_insert<<<left_grid, POLYLLA_LEFT_THREADS, 0, s>>>(c->ctr, tiles, c->T, c->tiling, c->cnt_ld, c->left_key,
+                                                           c->left_e, c->twin, ehash);
+  if (c->tiling.R) {  // grid tiles: the border ranking by bit order
+    const int64_t nchunks = (c->n_words + kBBChunk - 1) / kBBChunk;
+    k_bb_mark<<<seg_grid, kSegThreads, 0, s>>>(c->ctr, tiles, c->T, c->tiling, c->cnt_ld, c->left_e, c->twin, c->BB);
+    k_bb_count<<<(unsigned)((nchunks + 7) / 8), 256, 0, s>>>(c->ctr, c->n_words, nchunks, c->BB, c->bcnt);
+    n += 3;
+    prof_mark(s, "k_border_scan");
+    k_border_scan<<<1, kBorderScanThreads, 0, s>>>(c->ctr, nchunks, 3 * c->T, c->Bmax, c->bcnt);
+    k_bb_emit<<<(unsigned)((nchunks + 7) / 8), 256, 0, s>>>(c->ctr, c->n_words, nchunks, 3 * c->T, c->BB, c->bcnt,
+                                                             c->origin, c->twin, c->vmap);
+    n += 2;
+  } else {
+    hid* blist = reinterpret_cast<hid*>(c->left_key);  // dead after k_left_insert
+    k_border_rank<<<seg_grid, kSegThreads, 0, s>>>(c->ctr, tiles, c->cnt_ld, c->left_e, c->twin, blist, c->bcnt);
+    n += 3;
+    prof_mark(s, "k_border_scan");
+    k_border_scan<<<1, kBorderScanThreads, 0, s>>>(c->ctr, tiles, 3 * c->T, c->Bmax, c->bcnt);
+    k_border_emit<<<seg_grid, kSegThreads, 0, s>>>(c->ctr, tiles, 3 * c->T, blist, c->bcnt, c->origin, c->twin,
+                                                   c->vmap);
+    n += 2;
+  }
   prof_mark(s, "k_border_next");
   k_border_next<<<grid, 256, 0, s>>>(c->ctr, 3 * c->T, c->origin, c->twin, c->vmap, c->next);
   ++n;

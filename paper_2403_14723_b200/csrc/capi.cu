@@ -27,8 +27,10 @@ struct Layout {
 
 // region order; sizes in bytes.  Hmax = 3T + Bmax (the caller's bound on the border
 // half-edges; 3T covers every mesh); the run_host staging regions only when `staging`.
-static Layout layout(int64_t V, int64_t T, int64_t Bmax, bool staging) {
+static Layout layout(int64_t V, int64_t T, int64_t Bmax, bool staging, int64_t R) {
   const int64_t Hmax = 3 * T + Bmax;
+  const int64_t bt = make_tiling(T, R).ntiles;  // build tiles (grid tilings have more, partial ones)
+  const int64_t ct = (T + 2047) / 2048;          // contiguous tiles (emission, canonical sums)
   const int64_t nw = (3 * T + 31) / 32;
   const int64_t nb = (nw + 2047) / 2048 + 1;
   const int64_t cap = hash_cap_max_for(T);
@@ -41,7 +43,7 @@ static Layout layout(int64_t V, int64_t T, int64_t Bmax, bool staging) {
       (size_t)nw * 4,         // 5 F1
       (size_t)nw * 4,         // 6 S
       (size_t)nw * 4,         // 7 TB: barrier tips (F0, F1, S, TB equally spaced: k_tile stores them by offset)
-      (size_t)((T + 2047) / 2048 + 1) * 4,  // 8 per-tile border counts / bases
+      (size_t)((bt > ct ? bt : ct) + 1) * 4,  // 8 per-tile (or per-chunk) border counts / bases
       (size_t)(3 * T) * 4,    // 9 len
       (size_t)(3 * T) * 8,    // 10 left_key
       (size_t)(3 * T) * 4,    // 11 left_e
@@ -50,7 +52,7 @@ static Layout layout(int64_t V, int64_t T, int64_t Bmax, bool staging) {
       0,                      // 14 (unused)
       (size_t)V * 4,          // 15 tips
       (size_t)(2 * V) * 4,    // 16 aff
-      0,                      // 17 (unused)
+      R > 0 ? (size_t)nw * 4 : 0,  // 17 BB: unmatched leftovers (grid tiling)
       (size_t)nb * 8,         // 18 scan_a
       (size_t)nb * 8,         // 19 scan_b
       (size_t)nb * 8,         // 20 scan_c
@@ -64,7 +66,7 @@ static Layout layout(int64_t V, int64_t T, int64_t Bmax, bool staging) {
       (size_t)nw * 4,         // 28 SDB: seeds for the global seed walk
       (size_t)nw * 4,         // 29 per-word loop lengths
       (size_t)nw * 4,         // 30 C
-      (size_t)(2 * ((T + 2047) / 2048) + 2) * 4,  // 31 per-tile leftover / deferred counts
+      (size_t)(2 * bt + 2) * 4,  // 31 per-build-tile leftover / deferred counts
       (size_t)(3 * ((T + 2047) / 2048) + 2) * 4,  // 32 per-tile canonical-seed sums
       (size_t)(2 * ((T + 2047) / 2048) + 2) * 4,  // 33 per-tile polygon / loop-entry bases
   };
@@ -79,10 +81,13 @@ static Layout layout(int64_t V, int64_t T, int64_t Bmax, bool staging) {
   return L;
 }
 
-size_t workspace_bytes(int64_t V, int64_t T, int64_t Bmax, bool staging) { return layout(V, T, Bmax, staging).total; }
+size_t workspace_bytes(int64_t V, int64_t T, int64_t Bmax, bool staging, int64_t R) {
+  return layout(V, T, Bmax, staging, R).total;
+}
 
 bool carve(Ctx* c, void* ws, size_t bytes) {
-  const Layout L = layout(c->V, c->T, c->Bmax, c->staging);
+  c->tiling = make_tiling(c->T, c->tiling.R);
+  const Layout L = layout(c->V, c->T, c->Bmax, c->staging, c->tiling.R);
   if (bytes < L.total || (reinterpret_cast<uintptr_t>(ws) & 255)) return false;
   char* b = static_cast<char*>(ws);
   c->Hmax = 3 * c->T + c->Bmax;
@@ -104,6 +109,7 @@ bool carve(Ctx* c, void* ws, size_t bytes) {
   c->tips = reinterpret_cast<hid*>(b + L.off[15]);
   c->aff = reinterpret_cast<hid*>(b + L.off[16]);
   c->mids = nullptr;
+  c->BB = c->tiling.R ? reinterpret_cast<uint32_t*>(b + L.off[17]) : nullptr;
   c->scan_a = reinterpret_cast<long long*>(b + L.off[18]);
   c->scan_b = reinterpret_cast<long long*>(b + L.off[19]);
   c->scan_c = reinterpret_cast<long long*>(b + L.off[20]);
@@ -193,9 +199,9 @@ POLYLLA_API size_t polylla_workspace_bytes(int64_t n_vertices, int64_t n_triangl
 }
 
 POLYLLA_API size_t polylla_workspace_bytes_ex(int64_t n_vertices, int64_t n_triangles, int64_t max_border,
-                                              uint32_t flags) {
-  if (n_vertices < 0 || n_triangles < 0 || max_border < 0 || max_border > 3 * n_triangles) return 0;
-  return workspace_bytes(n_vertices, n_triangles, max_border, (flags & POLYLLA_WS_STAGING) != 0);
+                                              uint32_t flags, int64_t row_stride) {
+  if (n_vertices < 0 || n_triangles < 0 || max_border < 0 || max_border > 3 * n_triangles || row_stride < 0) return 0;
+  return workspace_bytes(n_vertices, n_triangles, max_border, (flags & POLYLLA_WS_STAGING) != 0, row_stride);
 }
 
 // index limits (NEXT-3): vertex ids int32; half-edge ids uint32 with H <= 2^32 - 2
@@ -205,9 +211,10 @@ static bool index_ok(int64_t V, int64_t T, int64_t Bmax) {
 
 // a new ctx over caller memory (no launches): argument checks + workspace carving
 static polylla_status new_ctx(const double* xy, int64_t V, const int32_t* tri, int64_t T, int64_t Bmax,
-                              bool staging, void* workspace, size_t workspace_bytes_, polylla_ctx** out) {
+                              bool staging, int64_t R, void* workspace, size_t workspace_bytes_, polylla_ctx** out) {
   *out = nullptr;
-  if (!xy || !tri || !workspace || V < 3 || T < 1 || Bmax < 0 || Bmax > 3 * T) return POLYLLA_E_INVALID_ARGUMENT;
+  if (!xy || !tri || !workspace || V < 3 || T < 1 || Bmax < 0 || Bmax > 3 * T || R < 0)
+    return POLYLLA_E_INVALID_ARGUMENT;
   if ((reinterpret_cast<uintptr_t>(xy) & 15) || (reinterpret_cast<uintptr_t>(tri) & 3))
     return POLYLLA_E_INVALID_ARGUMENT;
   if (!index_ok(V, T, Bmax)) return POLYLLA_E_INDEX_OVERFLOW;
@@ -220,6 +227,7 @@ static polylla_status new_ctx(const double* xy, int64_t V, const int32_t* tri, i
   c->T = T;
   c->Bmax = Bmax;
   c->staging = staging;
+  c->tiling.R = R;  // (carve() derives the tiling: contiguous unless R divides T)
   if (!carve(c, workspace, workspace_bytes_)) {
     std::free(p);
     return POLYLLA_E_WORKSPACE;
@@ -229,13 +237,13 @@ static polylla_status new_ctx(const double* xy, int64_t V, const int32_t* tri, i
 }
 
 POLYLLA_API polylla_status polylla_build_halfedges_ex(const double* xy, int64_t V, const int32_t* tri, int64_t T,
-                                                      int64_t max_border, uint32_t flags, void* workspace,
-                                                      size_t workspace_bytes_, polylla_stream stream,
+                                                      int64_t max_border, uint32_t flags, int64_t row_stride,
+                                                      void* workspace, size_t workspace_bytes_, polylla_stream stream,
                                                       polylla_ctx** ctx_out) {
   if (!ctx_out) return POLYLLA_E_INVALID_ARGUMENT;
   polylla_ctx* p = nullptr;
-  const polylla_status st =
-      new_ctx(xy, V, tri, T, max_border, (flags & POLYLLA_WS_STAGING) != 0, workspace, workspace_bytes_, &p);
+  const polylla_status st = new_ctx(xy, V, tri, T, max_border, (flags & POLYLLA_WS_STAGING) != 0, row_stride,
+                                    workspace, workspace_bytes_, &p);
   if (st != POLYLLA_OK) return st;
   Ctx* c = &p->c;
   const int n = launch_build(c, S(stream));
@@ -252,8 +260,8 @@ POLYLLA_API polylla_status polylla_build_halfedges_ex(const double* xy, int64_t 
 POLYLLA_API polylla_status polylla_build_halfedges(const double* xy, int64_t V, const int32_t* tri, int64_t T,
                                                    void* workspace, size_t workspace_bytes_, polylla_stream stream,
                                                    polylla_ctx** ctx_out) {
-  return polylla_build_halfedges_ex(xy, V, tri, T, 3 * T, POLYLLA_WS_STAGING, workspace, workspace_bytes_, stream,
-                                    ctx_out);
+  return polylla_build_halfedges_ex(xy, V, tri, T, 3 * T, POLYLLA_WS_STAGING, 0, workspace, workspace_bytes_,
+                                    stream, ctx_out);
 }
 
 POLYLLA_API polylla_status polylla_check_manifold(polylla_ctx* p, polylla_stream stream) {
@@ -454,7 +462,7 @@ POLYLLA_API polylla_status polylla_run_host(const double* xy_host, int64_t V, co
   if (!carve(&probe, workspace, workspace_bytes_)) return POLYLLA_E_WORKSPACE;
   polylla_ctx* p = nullptr;
   polylla_status st =
-      new_ctx(probe.xy_stage, V, probe.tri_stage, T, 3 * T, true, workspace, workspace_bytes_, &p);
+      new_ctx(probe.xy_stage, V, probe.tri_stage, T, 3 * T, true, 0, workspace, workspace_bytes_, &p);
   if (st != POLYLLA_OK) return st;
   Ctx* c = &p->c;
   cudaStream_t s = S(stream);

@@ -51,10 +51,48 @@ struct DevCounters {
   uint32_t hash_cap; // capacity (pow2 <= 2^31) of the leftover hash for this run
   uint32_t n_def;    // half-edges deferred by k_tile to the label fixup
   uint32_t n_sdef;   // seeds walked by k_seed_walk (deferred + repair halves)
-  uint32_t pad0;
+  uint32_t n_cross;  // (regions, grid tiling) pairs crossing the union-find tiles
   unsigned long long hash_scale;  // leftover-hash home slot = (lo * hash_scale) >> 32 (cap / V in 32.32 fixed point)
   int32_t pad[2];
 };
+
+// The build tiling (k_tile's tiles and the per-tile list segments).  Contiguous (R = 0):
+// tile t = triangles [2048 t, 2048 t + 2048).  Grid (row-major input whose triangle rows
+// are R triangles long, e.g. R = 2(s-1) for the Alg. 13 grids of PAPER.md L910-941):
+// tile (tr, tc) = triangle rows [16 tr, +16) x columns [128 tc, +128), numbered
+// t = tr * ntc + tc; its local triangle u = 128 r + c is triangle (16 tr + r) R + 128 tc + c.
+// A thin strip of one row cuts a third of all edges; a 16 x 128 patch cuts ~3%.
+constexpr int kGridTW = 128, kGridTH = 16, kGridTWShift = 7;  // kGridTW * kGridTH = 2048 triangles
+struct Tiling {
+  int64_t R = 0;      // triangles per row (0: contiguous tiles)
+  int64_t nrows = 0;  // T / R
+  int64_t ntc = 0;    // column tiles per band: ceil(R / 128)
+  int64_t ntiles = 0;
+};
+struct TileGeom {
+  int64_t base;       // global triangle of local triangle 0
+  int64_t seg;        // first entry of the tile's list segment (3 x its triangles, contiguous over tiles)
+  int32_t nrows, ncols;  // grid tiles: rows / columns present
+};
+__host__ __device__ __forceinline__ TileGeom tile_geom(const Tiling& g, int64_t T, int64_t tile) {
+  TileGeom r;
+  if (!g.R) {
+    r.base = tile * 2048;
+    r.seg = 3 * r.base;
+    const int64_t n = T - r.base < 2048 ? T - r.base : 2048;
+    r.nrows = (int32_t)n;  // (contiguous: nrows = triangles present, ncols unused)
+    r.ncols = 0;
+    return r;
+  }
+  const int64_t tr = tile / g.ntc, tc = tile - tr * g.ntc;
+  const int64_t row0 = tr * kGridTH, col0 = tc * kGridTW;
+  r.nrows = (int32_t)(g.nrows - row0 < kGridTH ? g.nrows - row0 : kGridTH);
+  r.ncols = (int32_t)(g.R - col0 < kGridTW ? g.R - col0 : kGridTW);
+  r.base = row0 * g.R + col0;
+  r.seg = 3 * (row0 * g.R + col0 * r.nrows);
+  return r;
+}
+Tiling make_tiling(int64_t T, int64_t R);  // R <= 0, or T % R != 0: contiguous
 
 struct Ctx {
   // inputs
@@ -64,6 +102,8 @@ struct Ctx {
   int64_t Hmax;  // 3T + the border bound (6T by default)
   int64_t Bmax;  // border bound of the workspace layout
   bool staging;  // the layout holds run_host's staging regions
+  Tiling tiling; // the build tiling (contiguous unless a row stride was given)
+  uint32_t* BB;  // [n_words] unmatched leftovers (grid tiling: the border ranking by bit scan)
   // workspace views
   int32_t* origin;   // vertex ids
   hid *twin, *next;
@@ -110,7 +150,7 @@ void prof_mark(cudaStream_t s, const char* name);  // start of kernel `name` (en
 void prof_end(cudaStream_t s);
 
 // workspace
-size_t workspace_bytes(int64_t V, int64_t T, int64_t Bmax, bool staging);
+size_t workspace_bytes(int64_t V, int64_t T, int64_t Bmax, bool staging, int64_t R = 0);
 bool carve(Ctx* c, void* ws, size_t bytes);  // layout from c->V, c->T, c->Bmax, c->staging
 
 // launchers (each returns the number of kernel launches issued, < 0 on CUDA error)

@@ -30,7 +30,7 @@ __device__ __forceinline__ bool is_longest(const uint8_t* __restrict__ lcode, hi
 // phase) are completed with atomicOr.  The deferred half-edges of tile t are entries
 // [3 * 2048 * t, + cnt_ld[2t + 1]) of def_e; one block per tile segment.
 __global__ void __launch_bounds__(kLabelThreads)
-    k_label_fixup(int64_t T, int64_t ntiles, const int32_t* __restrict__ cnt_ld, const hid* __restrict__ def_e,
+    k_label_fixup(int64_t T, int64_t ntiles, const Tiling tl, const int32_t* __restrict__ cnt_ld, const hid* __restrict__ def_e,
                   const hid* __restrict__ twin, const uint8_t* __restrict__ lcode, hid* __restrict__ next,
                   uint32_t* __restrict__ F0, uint32_t* __restrict__ F1, uint32_t* __restrict__ S,
                   uint32_t* __restrict__ TB, uint32_t* __restrict__ SDB, DevCounters* ctr) {
@@ -40,7 +40,7 @@ __global__ void __launch_bounds__(kLabelThreads)
   for (int64_t it = blockIdx.x; it < ntiles; it += gridDim.x) {
     const int64_t tile = sched_tile(it, ntiles);
     const int32_t n = cnt_ld[2 * tile + 1];
-    const int64_t seg = 3 * kBuildTileTris * tile;
+    const int64_t seg = tile_geom(tl, T, tile).seg;
     for (int32_t base = 0; base < n; base += kLabelThreads) {  // warp-uniform trip count
       const int32_t i = base + threadIdx.x;
       bool tip = false, walk_err = false, sd = false, fr = false;
@@ -89,10 +89,10 @@ __global__ void __launch_bounds__(kLabelThreads)
 constexpr int kFixBlocksPerSM = 4096 / kLabelThreads;  // a grid of 2 resident waves
 
 int launch_label(Ctx* c, cudaStream_t s) {
-  const int64_t tiles = (c->T + kBuildTileTris - 1) / kBuildTileTris;
+  const int64_t tiles = c->tiling.ntiles;
   prof_mark(s, "k_label_fixup");
   k_label_fixup<<<(unsigned)(tiles < 148 * kFixBlocksPerSM ? tiles : 148 * kFixBlocksPerSM), kLabelThreads, 0, s>>>(
-      c->T, tiles, c->cnt_ld, c->def_e, c->twin, c->lcode, c->next, c->F0, c->F1, c->S, c->TB, c->SDB, c->ctr);
+      c->T, tiles, c->tiling, c->cnt_ld, c->def_e, c->twin, c->lcode, c->next, c->F0, c->F1, c->S, c->TB, c->SDB, c->ctr);
   prof_end(s);
   return cudaGetLastError() == cudaSuccess ? 1 : -1;
 }

@@ -73,7 +73,8 @@ constexpr int kUfTile = kBuildTileTris, kUfThreads = POLYLLA_UF_THREADS;
 static_assert(3 * kUfTile % kUfThreads == 0, "half-edges per thread");
 __global__ void __launch_bounds__(kUfThreads) k_uf_local(int64_t T, const hid* __restrict__ twin,
                                                   const uint32_t* __restrict__ F1, int32_t* __restrict__ parent,
-                                                  int32_t* __restrict__ slot, const DevCounters* ctr) {
+                                                  int32_t* __restrict__ slot, hid* __restrict__ cross,
+                                                  DevCounters* ctr) {
   __shared__ int32_t p[kUfTile];
   if (ctr->status) return;
   const int64_t t0 = (int64_t)blockIdx.x * kUfTile;
@@ -94,6 +95,14 @@ __global__ void __launch_bounds__(kUfThreads) k_uf_local(int64_t T, const hid* _
   for (int k = 0; k < kIt; ++k) {
     const int j = threadIdx.x * kIt + k;
     const hid e = e0 + j, tw = tws[k];
+    if (cross && tw != kNoHe && tw > e && tw >= e0 + 3 * nt) {  // (grid tiling) a pair to the hook list
+      const uint32_t m = __activemask();
+      const int leader = __ffs(m) - 1, rank = __popc(m & ((1u << (threadIdx.x & 31)) - 1));
+      uint32_t b = 0;
+      if ((int)(threadIdx.x & 31) == leader) b = atomicAdd(&ctr->n_cross, (uint32_t)__popc(m));
+      cross[__shfl_sync(m, b, leader) + rank] = e;
+      continue;
+    }
     if (tw < e || tw >= e0 + 3 * nt) continue;  // frontier (kNoHe); once per pair; cross-tile pairs: k_uf_hook
     int32_t a = j / 3, b = (int32_t)((tw - e0) / 3);
     while (true) {
@@ -137,6 +146,26 @@ __global__ void k_uf_hook(int64_t ntiles, const int32_t* __restrict__ cnt_ld, co
   }
 }
 
+// (grid tiling) the pairs crossing the union-find tiles, listed by k_uf_local: the build
+// tiles are 2-D patches there, so their leftover lists miss pairs that k_uf_local's
+// contiguous tiles split
+__global__ void k_uf_hook_list(const hid* __restrict__ cross, const hid* __restrict__ twin, int32_t* parent,
+                               const DevCounters* ctr) {
+  if (ctr->status) return;
+  const uint32_t n = ctr->n_cross;
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    const hid e = cross[i];
+    int32_t a = (int32_t)(e / 3), b = (int32_t)(twin[e] / 3);
+    while (true) {
+      a = uf_find(parent, a);
+      b = uf_find(parent, b);
+      if (a == b) break;
+      if (a < b) { const int32_t s = a; a = b; b = s; }
+      if (atomicCAS(parent + a, a, b) == a) break;
+    }
+  }
+}
+
 __global__ void k_uf_seed(const hid* __restrict__ seeds, int32_t* parent, int32_t* __restrict__ slot,
                           const DevCounters* ctr) {
   if (ctr->status) return;
@@ -175,10 +204,15 @@ int launch_regions(Ctx* c, int32_t* out, int mode, cudaStream_t s) {
   const uint32_t* F = mode == 1 ? c->F0 : c->F1;
   const unsigned g = 148 * 8;
   prof_mark(s, mode == 1 ? "k_regions_pre" : "k_regions");
+  hid* cross = c->tiling.R ? reinterpret_cast<hid*>(slot + c->T) : nullptr;  // (16T bytes left of the 24T scratch)
+  if (cross) cudaMemsetAsync(&c->ctr->n_cross, 0, 4, s);
   k_uf_local<<<(unsigned)((c->T + kUfTile - 1) / kUfTile), kUfThreads, 0, s>>>(c->T, c->twin, F, parent, slot,
-                                                                                 c->ctr);
+                                                                                 cross, c->ctr);
   const int64_t tiles = (c->T + kUfTile - 1) / kUfTile;
-  k_uf_hook<<<(unsigned)tiles, 256, 0, s>>>(tiles, c->cnt_ld, c->left_e, c->twin, F, parent, c->ctr);
+  if (cross)
+    k_uf_hook_list<<<148 * 8, 256, 0, s>>>(cross, c->twin, parent, c->ctr);
+  else
+    k_uf_hook<<<(unsigned)tiles, 256, 0, s>>>(tiles, c->cnt_ld, c->left_e, c->twin, F, parent, c->ctr);
   if (mode == 1) {
     k_uf_roots<<<g, 256, 0, s>>>(c->T, parent, out, c->ctr);
   } else {

@@ -24,4 +24,30 @@ for xy, tri in cases:
         assert np.array_equal(r[k].cpu().numpy(), o[k]), k
     assert np.array_equal(r["loops"].cpu().numpy(), o["loops"])
     assert np.array_equal(r["poly_of_tri"].cpu().numpy(), oracle.triangle_polygons(o))
-print("sanitize cases ok", len(cases))
+# the bounded layout (NEXT-3), the paper ablation (NEXT-2), the non-manifold check, the
+# pre-repair regions and run_host (NEXT-1) on one multi-tile mesh
+xy, tri = synth.random_delaunay(6000, 7)
+o = oracle.run(xy, tri)
+xd, td = torch.from_numpy(xy).cuda(), torch.from_numpy(tri).cuda()
+B = o["H"] - 3 * tri.shape[0]
+for paper in (False, True):
+    ws = pp.alloc_workspace(xy.shape[0], tri.shape[0], max_border=B, staging=False)
+    ctx = pp.build_halfedges(xd, td, ws, max_border=B, staging=False)
+    pp.check_manifold(ctx)
+    if paper:
+        pp.label_generate_paper(ctx)
+    else:
+        pp.label(ctx)
+        reg = torch.empty(tri.shape[0], dtype=torch.int32, device="cuda")
+        pp.get_triangle_regions(ctx, reg)
+        pp.generate(ctx)
+    c = pp.get_counts(ctx)
+    off = torch.empty(c["n_polygons"] + 1, dtype=torch.int32, device="cuda")
+    lp = torch.empty(c["n_loop_entries"], dtype=torch.int32, device="cuda")
+    pp.get_polygons(ctx, off, lp)
+    assert pp.get_counts(ctx)["status"] == 0
+    assert np.array_equal(lp.cpu().numpy(), o["loops"]) and np.array_equal(off.cpu().numpy(), o["offsets"])
+    pp.destroy(ctx)
+h = pp.run_host(xy, tri)
+assert np.array_equal(h["loops"].numpy(), o["loops"]) and np.array_equal(h["next"].numpy(), o["next"])
+print("sanitize cases ok", len(cases) + 3)

@@ -36,19 +36,25 @@ def test_workspace_bytes_ex():
     from paper_2403_14723_b200 import polylla as pp
     L = pp.lib()
     V, T = 10**6, 2 * 10**6
-    assert L.polylla_workspace_bytes_ex(V, T, 3 * T, pp.WS_STAGING) == pp.workspace_bytes(V, T)
-    small = L.polylla_workspace_bytes_ex(V, T, 4000, 0)
-    assert 0 < small < L.polylla_workspace_bytes_ex(V, T, 4000, pp.WS_STAGING) < pp.workspace_bytes(V, T)
+    assert L.polylla_workspace_bytes_ex(V, T, 3 * T, pp.WS_STAGING, 0) == pp.workspace_bytes(V, T)
+    small = L.polylla_workspace_bytes_ex(V, T, 4000, 0, 0)
+    assert 0 < small < L.polylla_workspace_bytes_ex(V, T, 4000, pp.WS_STAGING, 0) < pp.workspace_bytes(V, T)
     # origin/twin/next shrink by 3 x 4 B per dropped border slot
-    assert L.polylla_workspace_bytes_ex(V, T, 3 * T, 0) - small >= 12 * (3 * T - 4000) - 3 * 256
-    assert L.polylla_workspace_bytes_ex(V, T, 3 * T + 1, 0) == 0 and L.polylla_workspace_bytes_ex(V, T, -1, 0) == 0
+    assert L.polylla_workspace_bytes_ex(V, T, 3 * T, 0, 0) - small >= 12 * (3 * T - 4000) - 3 * 256
+    assert L.polylla_workspace_bytes_ex(V, T, 3 * T + 1, 0, 0) == 0 and L.polylla_workspace_bytes_ex(V, T, -1, 0, 0) == 0
     h = ctypes.c_void_p()
     fake = ctypes.c_void_p(256)  # aligned, never dereferenced: the checks run first
     # H = 3T + max_border <= 2^32 - 2 (unsigned ids); vertex ids int32
-    assert L.polylla_build_halfedges_ex(fake, V, fake, 1_431_655_765, 0, 0, fake, 0, None, ctypes.byref(h)) == -6
-    assert L.polylla_build_halfedges_ex(fake, V, fake, 1_400_000_000, 1000, 0, fake, 0, None, ctypes.byref(h)) == -7
+    assert L.polylla_build_halfedges_ex(fake, V, fake, 1_431_655_765, 0, 0, 0, fake, 0, None, ctypes.byref(h)) == -6
+    assert L.polylla_build_halfedges_ex(fake, V, fake, 1_400_000_000, 1000, 0, 0, fake, 0, None, ctypes.byref(h)) == -7
     assert L.polylla_build_halfedges(fake, V, fake, 800_000_000, fake, 0, None, ctypes.byref(h)) == -6  # 6T > 2^32
-    assert L.polylla_build_halfedges_ex(fake, 2**31, fake, 10, 0, 0, fake, 0, None, ctypes.byref(h)) == -6
+    assert L.polylla_build_halfedges_ex(fake, 2**31, fake, 10, 0, 0, 0, fake, 0, None, ctypes.byref(h)) == -6
+    # a row-stride hint (grid tiling) changes the per-tile arrays only slightly; -1 is invalid
+    s = 2000
+    Tg = 2 * (s - 1) ** 2
+    g = L.polylla_workspace_bytes_ex(s * s, Tg, 4 * (s - 1), 0, 2 * (s - 1))
+    assert 0 < g - L.polylla_workspace_bytes_ex(s * s, Tg, 4 * (s - 1), 0, 0) < Tg // 2  # (BB: 3T/8 bytes)
+    assert L.polylla_workspace_bytes_ex(s * s, Tg, 4 * (s - 1), 0, -1) == 0
 
 
 def test_host_only_calls():

@@ -99,7 +99,7 @@ def test_default_layout_refuses_past_int32():
     rc = L.polylla_build_halfedges(pp._ptr(xy), S_BIG * S_BIG, pp._ptr(tri), T, pp._ptr(ws), ws.numel(), None,
                                    ctypes.byref(h))
     assert pp.STATUS[rc] == "INDEX_OVERFLOW"
-    rc = L.polylla_build_halfedges_ex(pp._ptr(xy), S_BIG * S_BIG, pp._ptr(tri), T, 4 * (S_BIG - 1), 0,
+    rc = L.polylla_build_halfedges_ex(pp._ptr(xy), S_BIG * S_BIG, pp._ptr(tri), T, 4 * (S_BIG - 1), 0, 0,
                                       pp._ptr(ws), ws.numel(), None, ctypes.byref(h))
     assert pp.STATUS[rc] == "WORKSPACE"  # addressable; only the workspace is too small
 

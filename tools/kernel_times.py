@@ -23,6 +23,8 @@ else:
 if cfg != 4:
     xy_d, tri_d = torch.from_numpy(xy).cuda(), torch.from_numpy(tri).cuda()
 V, T = xy_d.shape[0], tri_d.shape[0]
+# POLYLLA_ROWS=1: grid configs (4, 5) pass their row stride 2(s-1) (grid tiling)
+R = {4: 2 * 15999, 5: 2 * 1999}.get(cfg, 0) if os.environ.get("POLYLLA_ROWS") == "1" else 0
 import importlib  # noqa: E402
 
 for lib in libs:
@@ -30,7 +32,7 @@ for lib in libs:
         os.environ["POLYLLA_LIB"] = lib
     import paper_2403_14723_b200.polylla as pp
     pp = importlib.reload(pp)
-    ws = pp.alloc_workspace(V, T)
+    ws = pp.alloc_workspace(V, T, row_stride=R)
     offs = torch.empty(T + 1, dtype=torch.int32, device="cuda")
     loops = torch.empty(3 * T, dtype=torch.int32, device="cuda")
     s = torch.cuda.Stream()
@@ -38,7 +40,7 @@ for lib in libs:
     paper = os.environ.get("POLYLLA_PAPER") == "1"  # the paper's kernel sequence (NEXT-2 ablation)
 
     def step():
-        ctx = pp.build_halfedges(xy_d, tri_d, ws, s)
+        ctx = pp.build_halfedges(xy_d, tri_d, ws, s, row_stride=R)
         if paper:
             pp.label_generate_paper(ctx, s)
         else:
@@ -57,7 +59,7 @@ for lib in libs:
         for k, (ms, _) in pp.profile_read().items():
             per.setdefault(k, []).append(ms)
     pp.profile_enable(False)
-    g = pp.GraphStep(xy_d, tri_d, ws, offs, loops, s, paper=paper)
+    g = pp.GraphStep(xy_d, tri_d, ws, offs, loops, s, paper=paper, row_stride=R)
     for _ in range(5):
         g.replay()
     torch.cuda.synchronize()
@@ -70,7 +72,7 @@ for lib in libs:
         e1.synchronize()
         times.append(e0.elapsed_time(e1))
     med = {k: statistics.median(v) for k, v in per.items()}
-    ctx = pp.build_halfedges(xy_d, tri_d, ws, s)
+    ctx = pp.build_halfedges(xy_d, tri_d, ws, s, row_stride=R)
     if paper:
         pp.label_generate_paper(ctx, s)
     else:
