@@ -48,6 +48,13 @@ for paper in (False, True):
     assert pp.get_counts(ctx)["status"] == 0
     assert np.array_equal(lp.cpu().numpy(), o["loops"]) and np.array_equal(off.cpu().numpy(), o["offsets"])
     pp.destroy(ctx)
+# grid tiling (row-stride hint): a jittered grid with partial tiles, regions included
+gx, gt = synth.grid(150, 0.2, 9)
+go = oracle.run(gx, gt)
+gr = pp.run(torch.from_numpy(gx).cuda(), torch.from_numpy(gt).cuda(), row_stride=2 * 149, prev=True, regions=True)
+for k in ("origin", "twin", "next", "prev"):
+    assert np.array_equal(gr[k].cpu().numpy(), go[k]), k
+assert np.array_equal(gr["poly_of_tri"].cpu().numpy(), oracle.triangle_polygons(go))
 h = pp.run_host(xy, tri)
 assert np.array_equal(h["loops"].numpy(), o["loops"]) and np.array_equal(h["next"].numpy(), o["next"])
-print("sanitize cases ok", len(cases) + 3)
+print("sanitize cases ok", len(cases) + 4)

@@ -52,6 +52,13 @@ def test_variant_bit_exact(variant, variant_paths):
             res, _ = assert_parity(xy, tri, invariants=False)
             if variant == "fallback" and name in ("random", "jittered"):
                 assert res["n_seed_deferred"] > 0.5 * res["P"], name  # the global walk did the work
+        # grid tiling (row-stride hint) under the same variant: partial tiles, arbitrary stride
+        from test_gpu_grid_tiles import _check
+        for s_, a_ in ((150, 0.2), (131, 0.0)):
+            gx, gt = synth.grid(s_, a_, 3)
+            _check(gx, gt, 2 * (s_ - 1))
+        rx, rt = synth.random_delaunay(8000, 41)
+        _check(rx, rt, next(d for d in range(100, rt.shape[0] + 1) if rt.shape[0] % d == 0))
     finally:
         pp.set_library(prev)
 
@@ -99,6 +106,37 @@ def test_garbage_workspace_and_interleaved_kernels():
         np.testing.assert_array_equal(loops[:L].cpu().numpy(), ref["loops"])
         for k in ("origin", "twin", "next", "prev"):
             np.testing.assert_array_equal(arr[k].cpu().numpy(), ref[k], err_msg=k)
+
+
+def test_garbage_workspace_grid_tiling():
+    """The grid tiling ORs its words into bit-vectors it zeroes first: a workspace of random
+    bytes must not leak into any output."""
+    from paper_2403_14723_b200 import polylla as pp
+    s_ = 140
+    xy, tri = synth.grid(s_, 0.2, 13)
+    R = 2 * (s_ - 1)
+    ref = oracle.run(xy, tri)
+    T = tri.shape[0]
+    xd, td = torch.from_numpy(xy).cuda(), torch.from_numpy(tri).cuda()
+    for trial in range(2):
+        ws = pp.alloc_workspace(xy.shape[0], T, row_stride=R)
+        g = torch.Generator(device="cuda").manual_seed(7 + trial)
+        ws.copy_(torch.randint(0, 256, ws.shape, dtype=torch.uint8, device="cuda", generator=g))
+        ctx = pp.build_halfedges(xd, td, ws, row_stride=R)
+        pp.label(ctx)
+        pp.generate(ctx)
+        c = pp.get_counts(ctx)
+        P, L, H = c["n_polygons"], c["n_loop_entries"], c["n_halfedges"]
+        offs = torch.empty(P + 1, dtype=torch.int32, device="cuda")
+        loops = torch.empty(L, dtype=torch.int32, device="cuda")
+        arr = {k: torch.empty(H, dtype=torch.int32, device="cuda") for k in ("origin", "twin", "next", "prev")}
+        pp.get_polygons(ctx, offs, loops, **arr)
+        assert pp.get_counts(ctx)["status"] == 0
+        np.testing.assert_array_equal(offs.cpu().numpy(), ref["offsets"])
+        np.testing.assert_array_equal(loops.cpu().numpy(), ref["loops"])
+        for k in ("origin", "twin", "next", "prev"):
+            np.testing.assert_array_equal(arr[k].cpu().numpy(), ref[k], err_msg=k)
+        pp.destroy(ctx)
 
 
 def test_host_prev_pointer():
