@@ -39,10 +39,10 @@ def _free_gb():
     return torch.cuda.mem_get_info()[0] / 1e9
 
 
-def _run(pp, xy, tri, max_border, staging=False):
+def _run(pp, xy, tri, max_border, staging=False, row_stride=0):
     T = tri.shape[0]
-    ws = pp.alloc_workspace(xy.shape[0], T, max_border=max_border, staging=staging)
-    ctx = pp.build_halfedges(xy, tri, ws, max_border=max_border, staging=staging)
+    ws = pp.alloc_workspace(xy.shape[0], T, max_border=max_border, staging=staging, row_stride=row_stride)
+    ctx = pp.build_halfedges(xy, tri, ws, max_border=max_border, staging=staging, row_stride=row_stride)
     pp.label(ctx)
     pp.generate(ctx)
     return ws, ctx
@@ -156,7 +156,8 @@ def _closed_form_check(ctx, pp, s, offsets, loops, chunk=1 << 24):
 
 
 @pytest.mark.slow
-def test_regular_grid_beyond_int32_closed_form():
+@pytest.mark.parametrize("tiling", ["contiguous", "grid"])
+def test_regular_grid_beyond_int32_closed_form(tiling):
     pp = _pp()
     if _free_gb() < 140:
         pytest.skip("needs ~130 GB of free device memory")
@@ -166,7 +167,7 @@ def test_regular_grid_beyond_int32_closed_form():
     H = 3 * T + 4 * n
     assert H > 2**31 - 1 and H <= 2**32 - 2
     xy, tri = synth.grid_device(s, 0.0, 0)
-    ws, ctx = _run(pp, xy, tri, max_border=4 * n)
+    ws, ctx = _run(pp, xy, tri, max_border=4 * n, row_stride=2 * n if tiling == "grid" else 0)
     c = pp.get_counts(ctx)
     assert (c["n_halfedges"], c["n_border"], c["n_polygons"], c["n_loop_entries"], c["n_tips"]) == (
         H, 4 * n, P, 4 * P, 0)
@@ -175,7 +176,8 @@ def test_regular_grid_beyond_int32_closed_form():
     pp.get_polygons(ctx, offsets, loops)
     assert pp.get_counts(ctx)["status"] == 0
     _closed_form_check(ctx, pp, s, offsets, loops)
-    print(f"regular s={s}: T={T} H={H} (> 2^31 - 1) P={P}: every array = the closed form", flush=True)
+    print(f"regular s={s} ({tiling} tiles): T={T} H={H} (> 2^31 - 1) P={P}: every array = the closed form",
+          flush=True)
     pp.destroy(ctx)
 
 

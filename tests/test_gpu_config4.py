@@ -6,6 +6,7 @@ The oracle needs ~100 GB of host memory (its [H] arrays trimmed to the known H =
 B200 host: 202 s, profiles/r02/config4_oracle_bitexact.txt), so the test is skipped on a
 host with less than 150 GB of available memory.  The device-side invariant check of
 the same mesh runs too (tests/test_gpu_parity.py::test_config4_capacity_invariants)."""
+import gc
 import os
 import time
 
@@ -49,6 +50,9 @@ def _eq_chunked(dev_arr, host_arr, name, chunk=1 << 27):
 
 @pytest.mark.skipif(_mem_available_gb() < 150, reason="needs ~100 GB of host RAM (150 GB available)")
 def test_config4_bit_exact_vs_oracle():
+    """Both build tilings of the GPU path -- contiguous 2,048-triangle tiles and the grid
+    tiling that bench.py uses for this row-major input (row stride 2(s-1)) -- against one
+    oracle run, every array element by element."""
     from paper_2403_14723_b200 import polylla as pp
     print(_host_info(), flush=True)
     s = 16000
@@ -58,39 +62,43 @@ def test_config4_bit_exact_vs_oracle():
     assert T == 511_936_002
     H = 3 * T + 4 * (s - 1)
     print(f"generated in {time.time() - t0:.0f} s", flush=True)
-    # GPU first (its inputs from the host arrays: the same mesh the oracle reads)
-    xd, td = torch.from_numpy(xy).cuda(), torch.from_numpy(tri).cuda()
-    ws = pp.alloc_workspace(xy.shape[0], T)
-    t0 = time.time()
-    ctx = pp.build_halfedges(xd, td, ws)
-    pp.label(ctx)
-    pp.generate(ctx)
-    c = pp.get_counts(ctx)
-    assert c["n_halfedges"] == H
-    P, L = c["n_polygons"], c["n_loop_entries"]
-    offsets = torch.empty(P + 1, dtype=torch.int32, device="cuda")
-    loops = torch.empty(L, dtype=torch.int32, device="cuda")
-    pp.get_polygons(ctx, offsets, loops)
-    assert pp.get_counts(ctx)["status"] == 0
-    torch.cuda.synchronize()
-    print(f"gpu: {time.time() - t0:.1f} s (incl. first launches) P={P} L={L} tips={c['n_tips']}", flush=True)
-    del xd, td
-    # the oracle
     t0 = time.time()
     ref = oracle.run(xy, tri, hcap=H)
     print(f"oracle: {time.time() - t0:.0f} s, phases {ref['times']}", flush=True)
-    assert (ref["H"], ref["P"], ref["L"], ref["n_tips"]) == (H, P, L, c["n_tips"])
-    v = pp.get_views(ctx)
-    view = lambda k, n: pp.view_tensor(ctx, v[k], n, torch.int32)  # noqa: E731
-    for k in ("origin", "twin", "next"):
-        _eq_chunked(view(k, H), ref[k], k)
-    _eq_chunked(view("seeds", P), ref["seeds"], "seeds")
-    _eq_chunked(offsets, ref["offsets"], "offsets")
-    _eq_chunked(loops, ref["loops"], "loops")
-    lc = pp.view_tensor(ctx, v["lcode"], T, torch.uint8)
-    _eq_chunked(lc, ref["lcode"], "lcode")
-    print(f"config 4 bit-exact: origin/twin/next [{H}], lcode [{T}], seeds [{P}], offsets, loops [{L}]", flush=True)
-    pp.destroy(ctx)
+    for R in (0, 2 * (s - 1)):
+        xd, td = torch.from_numpy(xy).cuda(), torch.from_numpy(tri).cuda()
+        ws = pp.alloc_workspace(xy.shape[0], T, row_stride=R)
+        t0 = time.time()
+        ctx = pp.build_halfedges(xd, td, ws, row_stride=R)
+        pp.label(ctx)
+        pp.generate(ctx)
+        c = pp.get_counts(ctx)
+        assert c["n_halfedges"] == H
+        P, L = c["n_polygons"], c["n_loop_entries"]
+        offsets = torch.empty(P + 1, dtype=torch.int32, device="cuda")
+        loops = torch.empty(L, dtype=torch.int32, device="cuda")
+        pp.get_polygons(ctx, offsets, loops)
+        assert pp.get_counts(ctx)["status"] == 0
+        torch.cuda.synchronize()
+        print(f"gpu (row stride {R}): {time.time() - t0:.1f} s (incl. first launches) P={P} L={L} "
+              f"tips={c['n_tips']} leftovers={c['n_leftover']}", flush=True)
+        del xd, td
+        assert (ref["H"], ref["P"], ref["L"], ref["n_tips"]) == (H, P, L, c["n_tips"])
+        v = pp.get_views(ctx)
+        view = lambda k, n: pp.view_tensor(ctx, v[k], n, torch.int32)  # noqa: E731
+        for k in ("origin", "twin", "next"):
+            _eq_chunked(view(k, H), ref[k], k)
+        _eq_chunked(view("seeds", P), ref["seeds"], "seeds")
+        _eq_chunked(offsets, ref["offsets"], "offsets")
+        _eq_chunked(loops, ref["loops"], "loops")
+        lc = pp.view_tensor(ctx, v["lcode"], T, torch.uint8)
+        _eq_chunked(lc, ref["lcode"], "lcode")
+        print(f"config 4 bit-exact (row stride {R}): origin/twin/next [{H}], lcode [{T}], seeds [{P}], offsets, "
+              f"loops [{L}]", flush=True)
+        pp.destroy(ctx)
+        del ws, offsets, loops, v, lc, view, ctx  # (the Context holds the workspace tensor)
+        gc.collect()
+        torch.cuda.empty_cache()
 
 
 def test_int32_ceiling_invariants():
