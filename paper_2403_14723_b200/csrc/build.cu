@@ -62,8 +62,9 @@ __device__ __forceinline__ int q_step(int q) {
 constexpr size_t kOffTw = kTileQ * 4, kOffSlot = kOffTw + kTileQ * 2, kOffLc = kOffSlot + kTileSlots * 2,
                  kOffNx = kOffLc + kTileTris,
                  kNxBytes = kTileQ * 2 + 8 * (kTileHE / 8),                    // P4-P6 arrays (22,528 B)
-                 kTileSmem = kOffNx + kNxBytes;                                // 106,496 B -> 2 CTAs/SM
-static_assert(2 * (kTileSmem + 1024) <= 228 * 1024, "two tiles per SM");
+                 kTileSmemGrid = kOffNx + kNxBytes,                            // 106,496 B -> 2 CTAs/SM
+                 kTileSmem = kTileSmemGrid - 2 * (kTileHE / 8);               // 104,960 B: contiguous tiles need no Fw/Tw
+static_assert(2 * (kTileSmemGrid + 1024) <= 228 * 1024, "two tiles per SM");
 constexpr unsigned long long kLeftDown = 1ull << 63;    // leftover key: set if origin > target
 constexpr unsigned long long kLeftPaired = 1ull << 31;  // leftover key: set once the key's slot holder is paired
 constexpr uint32_t kEmpty16 = 0xFFFFu;             // empty 16-bit slot (quad indices are < 8192)
@@ -249,7 +250,7 @@ __device__ __forceinline__ void tile_body(
   // overlays of the slot area (after P2)
   uint16_t* succ = slot;
 
-  const TileGeom tg_ = tile_geom(tl, T, tile);
+  const TileGeom tg_ = GRID ? tile_geom(tl, T, tile) : contig_geom(T, tile);
   const int64_t f0 = tg_.base;                // global triangle of local triangle 0
   const int64_t seg0 = tg_.seg;               // the tile's list segment
   const int nt = FULL ? kTileTris : GRID ? kTileTris : tg_.nrows;  // (grid: presence per triangle)
@@ -274,7 +275,7 @@ __device__ __forceinline__ void tile_body(
   for (int i = tid; i < kTileSlots / 8; i += kTileThreads)
     reinterpret_cast<uint4*>(slot)[i] = make_uint4(0xFFFFFFFFu, 0xFFFFFFFFu, 0xFFFFFFFFu, 0xFFFFFFFFu);
   for (int i = tid; i < kTileQ / 2; i += kTileThreads) reinterpret_cast<uint32_t*>(tw_s)[i] = 0xFFFFFFFFu;
-  const TileGeom tn_ = tile_next >= 0 ? tile_geom(tl, T, tile_next) : TileGeom{0, 0, 0, 0};
+  const TileGeom tn_ = tile_next < 0 ? TileGeom{0, 0, 0, 0} : GRID ? tile_geom(tl, T, tile_next) : contig_geom(T, tile_next);
   const int64_t f0n = tn_.base;  // this CTA's next tile (prefetched), if tile_next >= 0
   if (tile_next >= 0 && (GRID ? tid < tn_.nrows : tid == 0)) {  // the next tile's triangles -> L2 (TMA bulk prefetch)
     const int64_t nn = GRID ? tn_.ncols : (T - f0n < kTileTris ? T - f0n : kTileTris);
@@ -1096,7 +1097,7 @@ static int device_setup(int* n_sm) {
   std::lock_guard<std::mutex> lk(g_dev_mu);
   if (dev >= 64 || !((g_dev_ready >> dev) & 1)) {
     if (cudaFuncSetAttribute(k_tile<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kTileSmem) != cudaSuccess ||
-        cudaFuncSetAttribute(k_tile<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kTileSmem) != cudaSuccess)
+        cudaFuncSetAttribute(k_tile<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kTileSmemGrid) != cudaSuccess)
       return -1;
     int sms = 0;
     if (cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess) return -1;
@@ -1143,7 +1144,7 @@ int launch_build_tiles(Ctx* c, cudaStream_t s, int64_t t0, int64_t t1) {
   if (c->S - c->F1 != bv_stride || c->TB - c->S != bv_stride) return -1;
   prof_mark(s, "k_tile");
   auto kt = c->tiling.R ? k_tile<true> : k_tile<false>;
-  kt<<<(unsigned)(t1 - t0), kTileThreads, kTileSmem, s>>>(reinterpret_cast<const double2*>(c->xy), c->tri, c->V, c->T,
+  kt<<<(unsigned)(t1 - t0), kTileThreads, c->tiling.R ? kTileSmemGrid : kTileSmem, s>>>(reinterpret_cast<const double2*>(c->xy), c->tri, c->V, c->T,
                                                           c->origin, c->twin, c->next, c->lcode, c->F0, bv_stride, c->C,
                                                           c->len, c->wlen, c->left_key, c->left_e, c->def_e, c->SDB,
                                                           c->cnt_ld, c->ctr, pf_dist, t0, c->tiling);

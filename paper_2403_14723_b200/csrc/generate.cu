@@ -31,6 +31,7 @@ __device__ __forceinline__ bool f1_of(const uint32_t* __restrict__ F1, int64_t T
 #define POLYLLA_REPAIR_THREADS 128
 #endif
 constexpr int kRepairThreads = POLYLLA_REPAIR_THREADS;
+constexpr int kRotMax = 32;  // rotations up to this degree are walked once and kept (local array)
 __global__ void __launch_bounds__(kRepairThreads)
     k_repair_mid(int64_t T, int64_t n_words, const uint32_t* __restrict__ TB, const hid* __restrict__ twin,
                  uint32_t* F1, uint32_t* SDB, hid* __restrict__ tips, hid* __restrict__ aff, DevCounters* ctr) {
@@ -48,7 +49,9 @@ __global__ void __launch_bounds__(kRepairThreads)
     hid x = e0;
     int64_t d = 0;
     bool ok = true;
+    hid rot[kRotMax];  // the rotation, recorded for the middle-edge step below (deg <= kRotMax)
     do {  // degree(v): rotation closure about v (an interior vertex); deg(v) <= 3T
+      if (d < kRotMax) rot[d] = x;
       const hid tx = twin[x];
       if (tx >= T3 || ++d > T3) { ok = false; break; }
       x = next_in(tx);
@@ -60,7 +63,9 @@ __global__ void __launch_bounds__(kRepairThreads)
       return;
     }
     hid m = e0;
-    for (int64_t k = 0; k < (d - 1) / 2; ++k) m = next_in(twin[m]);  // CWvertexEdge steps (R1, R5)
+    if (d <= kRotMax) m = rot[(d - 1) / 2];  // floor((d-1)/2) CWvertexEdge steps (R1, R5)
+    else
+      for (int64_t k = 0; k < (d - 1) / 2; ++k) m = next_in(twin[m]);
     const hid tm = twin[m];
     atomicOr(&F1[m >> 5], 1u << (m & 31));
     atomicOr(&F1[tm >> 5], 1u << (tm & 31));
@@ -79,6 +84,40 @@ __global__ void k_repair_rewire(int64_t T, const hid* __restrict__ twin, const u
   const int32_t n = 2 * ctr->n_tips;
   for (int32_t j = blockIdx.x * blockDim.x + threadIdx.x; j < n; j += gridDim.x * blockDim.x) {
     const hid o = aff[j];
+    // one walk around w collects its outgoing half-edges in sweep order (R1; the border
+    // chain at the hull); the next F1 half-edge after each incoming p = prev_in(y_i) is
+    // then the first frontier y_m, m >= i cyclically -- what a rotation from y_i finds
+    hid rot[kRotMax];
+    int d = 0;
+    bool fits = true, ok = true;
+    {
+      hid y = o;
+      int64_t guard = 0;
+      do {
+        if (d < kRotMax) rot[d] = y; else fits = false;
+        ++d;
+        const hid ty = twin[y];
+        y = ty >= T3 ? next[ty] : next_in(ty);
+        if (++guard > H) { ok = false; break; }
+      } while (y != o);
+    }
+    if (!ok) { raise_status(ctr, ST_WALK); return; }
+    if (fits) {
+      uint32_t fo = 0, fi = 0;  // bit i: y_i frontier (F1 or border) / p_i = prev_in(y_i) an interior F1 half-edge
+      for (int i = 0; i < d; ++i) {
+        fo |= (uint32_t)f1_of(F1, T3, rot[i]) << i;
+        if (rot[i] < T3) fi |= (uint32_t)f1_of(F1, T3, prev_in(rot[i])) << i;
+      }
+      if (fi && !fo) { raise_status(ctr, ST_WALK); return; }  // (a rotation without a frontier half-edge)
+      for (uint32_t b = fi; b; b &= b - 1) {
+        const int i = __ffs(b) - 1;
+        const uint32_t ahead = fo >> i;  // (i < 32)
+        const int m = ahead ? i + __ffs(ahead) - 1 : __ffs(fo) - 1;
+        next[prev_in(rot[i])] = rot[m];
+      }
+      continue;
+    }
+    // (degree above kRotMax: the rotation walked per incoming F1 half-edge)
     hid y = o;
     int64_t guard = 0;
     do {

@@ -74,16 +74,18 @@ struct TileGeom {
   int64_t seg;        // first entry of the tile's list segment (3 x its triangles, contiguous over tiles)
   int32_t nrows, ncols;  // grid tiles: rows / columns present
 };
-__host__ __device__ __forceinline__ TileGeom tile_geom(const Tiling& g, int64_t T, int64_t tile) {
+__host__ __device__ __forceinline__ TileGeom contig_geom(int64_t T, int64_t tile) {
   TileGeom r;
-  if (!g.R) {
-    r.base = tile * 2048;
-    r.seg = 3 * r.base;
-    const int64_t n = T - r.base < 2048 ? T - r.base : 2048;
-    r.nrows = (int32_t)n;  // (contiguous: nrows = triangles present, ncols unused)
-    r.ncols = 0;
-    return r;
-  }
+  r.base = tile * 2048;
+  r.seg = 3 * r.base;
+  const int64_t n = T - r.base < 2048 ? T - r.base : 2048;
+  r.nrows = (int32_t)n;  // (contiguous: nrows = triangles present, ncols unused)
+  r.ncols = 0;
+  return r;
+}
+__host__ __device__ __forceinline__ TileGeom tile_geom(const Tiling& g, int64_t T, int64_t tile) {
+  if (!g.R) return contig_geom(T, tile);
+  TileGeom r;
   const int64_t tr = tile / g.ntc, tc = tile - tr * g.ntc;
   const int64_t row0 = tr * kGridTH, col0 = tc * kGridTW;
   r.nrows = (int32_t)(g.nrows - row0 < kGridTH ? g.nrows - row0 : kGridTH);
