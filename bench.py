@@ -531,7 +531,7 @@ def main():
     roof = {"bound": "hbm", "kernel": top, "achieved": achieved, "peak": peak, "unit": "GB/s",
             "frac": achieved / peak, "traffic": traffic, "alg_bytes_per_launch": ab[top],
             "kernel_ms": per_launch[top], "share_of_step": per_launch[top] * prof[top][1] / prof_steps / prof_step_ms,
-            "peak_source": peak_src, "traffic_source": "profiles/ncu_traffic.json (ncu --set full capture of this "
+            "peak_source": peak_src, "traffic_source": "profiles/ncu_traffic.json (ncu dram__bytes of this "
                                                         "source hash)" if traffic else "no capture of this build",
             "groups_without_model": missing}
     group_roof = {k: {"ms": per_launch[k] * prof[k][1] / prof_steps, "alg_bytes": ab[k],

@@ -32,7 +32,7 @@ def main(cfg, paths):
         for r in csv.reader(open(path)):
             if len(r) < 15 or r[0] == "ID":
                 continue
-            name = r[4].split("(")[0].replace("void ", "").replace("polylla::", "")
+            name = r[4].split("(")[0].replace("void ", "").replace("polylla::", "").split("<")[0]  # (k_tile<0>)
             if r[12] in ("dram__bytes_read.sum", "dram__bytes_write.sum"):
                 launches[(r[0], name)][r[12]] = float(r[14].replace(",", "")) * SCALE.get(r[13], 1.0)
         for (lid, name), m in launches.items():
