@@ -48,6 +48,16 @@ def test_grid_tiles_alg13(s, a):
         assert res["n_leftover"] < 0.06 * 3 * tri.shape[0]
 
 
+@pytest.mark.parametrize("which", ["smallest", "whole"])
+def test_grid_tiles_degenerate_strides(which):
+    """Strides that make every tile partial: the smallest divisor > 1 of T (rows of a few
+    triangles: 16 x R patches) and R = T (one row: 1 x 128 patches)."""
+    xy, tri = synth.random_delaunay(4000, 19)
+    T = tri.shape[0]
+    R = T if which == "whole" else next(d for d in range(2, T + 1) if T % d == 0)
+    _check(xy, tri, R)
+
+
 @pytest.mark.parametrize("shuffle", [False, True])
 def test_grid_tiles_any_stride(shuffle):
     xy, tri = synth.random_delaunay(30000, 12)
