@@ -102,11 +102,12 @@ def test_config4_bit_exact_vs_oracle():
 
 
 def test_int32_ceiling_invariants():
-    """The int32 ceiling of the half-edge ids (PAPER.md L55's
-    capacity question): a jittered grid with s = 18,919 has T = 715,781,448 and
-    H = 3T + 4(s-1) = 2,147,420,016 <= 2^31 - 1 half-edges -- the largest grid the int32
-    ids address (s = 18,920 overflows).  Workspace ~144 GB + 14 GB of input on the 178 GB
-    device; checked by the properties that hold at any size, on the device."""
+    """The int32 ceiling (PAPER.md L55's capacity question): a
+    jittered grid with s = 18,919 has T = 715,781,448 and H = 3T + 4(s-1) = 2,147,420,016
+    <= 2^31 - 1 half-edges -- the largest grid signed 32-bit ids would address, and the
+    largest the default worst-case layout (6T <= 2^32 - 2) accepts.  Workspace ~144 GB +
+    14 GB of input on the 178 GB device; checked by the properties that hold at any size,
+    on the device.  (Past it: tests/test_gpu_capacity.py, unsigned ids, bounded layout.)"""
     from paper_2403_14723_b200 import polylla as pp
     from test_gpu_parity import device_invariants
     import gc
