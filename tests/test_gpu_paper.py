@@ -46,3 +46,15 @@ def test_paper_sequence_config2():
     res = gpu_run(xy, tri, paper=True)
     for k in ("next", "seeds", "offsets", "loops"):
         np.testing.assert_array_equal(res[k].cpu().numpy(), ref[k], err_msg=k)
+
+
+@pytest.mark.parametrize("s,a", [(64, 0.0), (150, 0.2)])
+def test_paper_sequence_after_grid_tiling(s, a):
+    """The ablation after a grid-tiled build (row-stride hint): the paper's kernels read
+    only the global arrays, so the result is the oracle's."""
+    xy, tri = synth.grid(s, a, 3)
+    ref = oracle.run(xy, tri)
+    res = gpu_run(xy, tri, paper=True, prev=True, regions=True, row_stride=2 * (s - 1))
+    for k in ("origin", "twin", "next", "prev", "seeds", "offsets", "loops"):
+        np.testing.assert_array_equal(res[k].cpu().numpy(), ref[k], err_msg=k)
+    np.testing.assert_array_equal(res["poly_of_tri"].cpu().numpy(), oracle.triangle_polygons(ref))
