@@ -59,6 +59,8 @@ def parse():
     ap.add_argument("--order", default="morton", choices=["morton", "shuffled"],
                     help="triangle order of configs 2/3 (sensitivity rows): generator Morton order or shuffled")
     ap.add_argument("--no-pcie", action="store_true")
+    ap.add_argument("--sort", action="store_true",
+                    help="POLYLLA_BUILD_SORT: the build orders the triangles by Morton cell first (any input order)")
     ap.add_argument("--no-row-hint", action="store_true",
                     help="grid configs: contiguous 2,048-triangle build tiles instead of the row-stride grid tiling")
     return ap.parse_args()
@@ -392,17 +394,20 @@ def main():
     Tmax = max(m["tri"].shape[0] for m in meshes)
     # grid inputs (row-major Alg. 13 triangle lists) pass their row stride 2(s-1): the build
     # then tiles 16-row x 128-triangle patches (polylla_build_halfedges_ex)
-    R0 = 0 if args.no_row_hint else meshes[0].get("row_stride", 0)
+    R0 = 0 if args.no_row_hint or args.sort else meshes[0].get("row_stride", 0)
+    SORT = bool(args.sort)
     if R0:
         name += f"; build tiles: 16 x 128-triangle patches (row stride hint {R0})"
-    wsp = pp.alloc_workspace(Vmax, Tmax, dev, row_stride=R0)
+    if SORT:
+        name += "; build tiles over the Morton-cell order of the triangle centroids (POLYLLA_BUILD_SORT, in the timed step)"
+    wsp = pp.alloc_workspace(Vmax, Tmax, dev, row_stride=R0, sort=SORT)
     offsets = torch.empty(Tmax + 1, dtype=torch.int32, device=dev)
     loops = torch.empty(3 * Tmax, dtype=torch.int32, device=dev)
     stream = torch.cuda.Stream(device=dev)
     launches = [0]
 
     def convert(m):
-        ctx = pp.build_halfedges(m["xy"], m["tri"], wsp, stream, row_stride=R0)
+        ctx = pp.build_halfedges(m["xy"], m["tri"], wsp, stream, row_stride=R0, sort=SORT)
         pp.label(ctx, stream)
         pp.generate(ctx, stream)
         pp.get_polygons(ctx, offsets, loops, stream=stream)
@@ -425,7 +430,7 @@ def main():
     if len(meshes) > 1:
         n_lanes = int(os.environ.get("POLYLLA_BENCH_LANES", "2"))
         lanes = [dict(stream=stream, ws=wsp, offsets=offsets, loops=loops)] + [
-            dict(stream=torch.cuda.Stream(device=dev), ws=pp.alloc_workspace(Vmax, Tmax, dev, row_stride=R0),
+            dict(stream=torch.cuda.Stream(device=dev), ws=pp.alloc_workspace(Vmax, Tmax, dev, row_stride=R0, sort=SORT),
                  offsets=torch.empty(Tmax + 1, dtype=torch.int32, device=dev),
                  loops=torch.empty(3 * Tmax, dtype=torch.int32, device=dev)) for _ in range(n_lanes - 1)]
 
@@ -438,7 +443,7 @@ def main():
             for i, m in enumerate(meshes):
                 ln = lanes[i % len(lanes)]
                 s_ = ln["stream"]
-                ctx = pp.build_halfedges(m["xy"], m["tri"], ln["ws"], s_, row_stride=R0)
+                ctx = pp.build_halfedges(m["xy"], m["tri"], ln["ws"], s_, row_stride=R0, sort=SORT)
                 pp.label(ctx, s_)
                 pp.generate(ctx, s_)
                 pp.get_polygons(ctx, ln["offsets"], ln["loops"], stream=s_)
@@ -470,7 +475,8 @@ def main():
     graphs = None
     if not args.no_graph and len(meshes) == 1:
         # the whole step as one CUDA graph launch (same kernels, same stream order)
-        graphs = [pp.GraphStep(m["xy"], m["tri"], wsp, offsets, loops, stream, row_stride=R0) for m in meshes]
+        graphs = [pp.GraphStep(m["xy"], m["tri"], wsp, offsets, loops, stream, row_stride=R0, sort=SORT)
+                  for m in meshes]
 
         def step():
             for g in graphs:

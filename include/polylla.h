@@ -101,8 +101,10 @@ typedef struct {
  * (worst case B = 3T; includes staging for polylla_run_host).  Host-only. */
 POLYLLA_API size_t polylla_workspace_bytes(int64_t n_vertices, int64_t n_triangles);
 
-/* Workspace flags. */
+/* Workspace / build flags. */
 #define POLYLLA_WS_STAGING 1u /* hold the host-buffer staging regions of polylla_run_host */
+#define POLYLLA_BUILD_SORT 2u /* build tiles over triangles ordered by the Morton cell of their centroid
+                                 (any input order; ignores row_stride): a performance option, same results */
 
 /* Bytes of device workspace for a mesh with at most max_border border half-edges
  * (0 <= max_border <= 3T; e.g. 4(s-1) for an s x s grid), with POLYLLA_WS_STAGING in

@@ -224,7 +224,7 @@ __device__ __forceinline__ bool tri_here(int i, int t, int nt, int nrows, int nc
 //     bit-vector SDB; tips go to the bit-vector TB)
 // Loops are indexed so that no lane divides: triangle t = tid + 768 i, half-edge
 // j = tid + 768 i with quad q = q_of(tid) + 1024 i (768 = 3 * 256).
-template <bool FULL, bool GRID>
+template <bool FULL, int MODE>
 __device__ __forceinline__ void tile_body(
     unsigned char* smem_tile, const Tiling tl, const double2* __restrict__ xy, const int32_t* __restrict__ tri, int64_t V, int64_t T,
     int32_t* __restrict__ origin, hid* __restrict__ twin, hid* __restrict__ next, uint8_t* __restrict__ lcode,
@@ -250,6 +250,9 @@ __device__ __forceinline__ void tile_body(
   // overlays of the slot area (after P2)
   uint16_t* succ = slot;
 
+  constexpr bool GRID = MODE == kTileGrid;      // 16 x 128 patches of a row-major list
+  constexpr bool SORTED = MODE == kTileSorted;  // runs of the Morton-sorted order perm[]
+  constexpr bool SCAT = MODE != kTileContig;    // outputs not one aligned range: words OR-ed
   const TileGeom tg_ = GRID ? tile_geom(tl, T, tile) : contig_geom(T, tile);
   const int64_t f0 = tg_.base;                // global triangle of local triangle 0
   const int64_t seg0 = tg_.seg;               // the tile's list segment
@@ -260,9 +263,10 @@ __device__ __forceinline__ void tile_body(
   const int tid = threadIdx.x, lane = tid & 31;
   // local -> global: triangle, half-edge of a quad (grid tiles: rows of 128 triangles R apart)
   auto gtri = [&](int t) -> int64_t {
-    return GRID ? f0 + (int64_t)(t >> kGridTWShift) * tl.R + (t & (kGridTW - 1)) : f0 + t;
+    return GRID ? f0 + (int64_t)(t >> kGridTWShift) * tl.R + (t & (kGridTW - 1))
+                : SORTED ? (int64_t)__ldg(tl.perm + f0 + t) : f0 + t;
   };
-  auto ghe = [&](int q) -> int64_t { return GRID ? 3 * gtri(q >> 2) + (q & 3) : e0 + j_of(q); };
+  auto ghe = [&](int q) -> int64_t { return SCAT ? 3 * gtri(q >> 2) + (q & 3) : e0 + j_of(q); };
   auto here = [&](int t) -> bool { return FULL || (GRID ? ((t & (kGridTW - 1)) < g_cols && (t >> kGridTWShift) < g_rows) : t < nt); };
 #ifdef POLYLLA_PHASE_TIMING
   long long t_phase_ = clock64();
@@ -277,7 +281,7 @@ __device__ __forceinline__ void tile_body(
   for (int i = tid; i < kTileQ / 2; i += kTileThreads) reinterpret_cast<uint32_t*>(tw_s)[i] = 0xFFFFFFFFu;
   const TileGeom tn_ = tile_next < 0 ? TileGeom{0, 0, 0, 0} : GRID ? tile_geom(tl, T, tile_next) : contig_geom(T, tile_next);
   const int64_t f0n = tn_.base;  // this CTA's next tile (prefetched), if tile_next >= 0
-  if (tile_next >= 0 && (GRID ? tid < tn_.nrows : tid == 0)) {  // the next tile's triangles -> L2 (TMA bulk prefetch)
+  if (!SORTED && tile_next >= 0 && (GRID ? tid < tn_.nrows : tid == 0)) {  // the next tile's triangles -> L2 (TMA bulk prefetch)
     const int64_t nn = GRID ? tn_.ncols : (T - f0n < kTileTris ? T - f0n : kTileTris);
     const int32_t* pn = tri + 3 * (f0n + (GRID ? tid * tl.R : 0));  // (grid: one row per thread)
     const uint32_t bytes = (uint32_t)((3 * nn * 4) & ~int64_t(15));
@@ -290,7 +294,7 @@ __device__ __forceinline__ void tile_body(
   for (int i = 0; i < kTriIters; ++i) {
     const int t = tid + i * kTileThreads;
     if (tri_here<FULL, GRID>(i, t, nt, g_rows, g_cols)) {
-      const int32_t* rt = GRID ? tri + 3 * gtri(t) : raw + 3 * t;
+      const int32_t* rt = SCAT ? tri + 3 * gtri(t) : raw + 3 * t;
       ids[i][0] = rt[0]; ids[i][1] = rt[1]; ids[i][2] = rt[2];
     } else {
       ids[i][0] = ids[i][1] = ids[i][2] = 0;
@@ -358,7 +362,8 @@ __device__ __forceinline__ void tile_body(
     const int t = tid + i * kTileThreads;
     pf_ok = t < nn_pf && (!GRID || ((t & (kGridTW - 1)) < tn_.ncols && (t >> kGridTWShift) < tn_.nrows));
     if (pf_ok) {  // volatile: issued here, not sunk next to their use at the end of the pass
-      const int32_t* src = tri + 3 * (GRID ? f0n + (int64_t)(t >> kGridTWShift) * tl.R + (t & (kGridTW - 1)) : f0n + t);
+      const int32_t* src = tri + 3 * (GRID ? f0n + (int64_t)(t >> kGridTWShift) * tl.R + (t & (kGridTW - 1))
+                                           : SORTED ? (int64_t)__ldg(tl.perm + f0n + t) : f0n + t);
       asm volatile("ld.global.nc.b32 %0, [%3];\n\tld.global.nc.b32 %1, [%3+4];\n\tld.global.nc.b32 %2, [%3+8];"
                    : "=r"(pf_v[0]), "=r"(pf_v[1]), "=r"(pf_v[2]) : "l"(src));
     }
@@ -490,7 +495,7 @@ __device__ __forceinline__ void tile_body(
         const int32_t back = tw_s[tqs];
         const int32_t lt = lc_s[tqs >> 2];
         if (tq >= 0 && back != q) nm = ST_NONMANIFOLD_EDGE;  // twin claimed twice (edge in > 2 triangles)
-        if (GRID) {
+        if (SCAT) {
           const int64_t ge = ghe(q);
           __stcs(origin + ge, org);
           __stcs(twin + ge, tq >= 0 ? (hid)ghe(tq) : kNoHe);
@@ -500,7 +505,9 @@ __device__ __forceinline__ void tile_body(
         }
         const bool front = lq != k && lt != (tq & 3);  // neither half the longest edge of its triangle
         succ[q] = (uint16_t)(tq < 0 ? (q | kSuccUnknown) : front ? (q | kSuccFront) : next_q(tq));
-        sd = tq >= 0 && lq == k && lt == (tq & 3) && q < tq;  // terminal edge, smaller id
+        sd = tq >= 0 && lq == k && lt == (tq & 3);  // terminal edge: the smaller id of the pair (R8)
+        if (SORTED) sd = sd && ghe(q) < ghe(tq);     // (sorted tiles: local order is not the id order)
+        else sd = sd && q < tq;
         left = tq < 0;
       }
       const uint32_t sw = __ballot_sync(0xffffffffu, sd), lw = __ballot_sync(0xffffffffu, left);
@@ -508,7 +515,7 @@ __device__ __forceinline__ void tile_body(
       // lane 0: Sw, lane 1: Lm (shared); lane 2: the global S
       if (lane < 2) {
         s_dst[wl] = lane == 0 ? sw : lw;
-      } else if (!GRID && lane == 2 && (FULL || j - lane < nhe)) {  // (grid tiles: flushed at the end)
+      } else if (!SCAT && lane == 2 && (FULL || j - lane < nhe)) {  // (grid / sorted tiles: flushed at the end)
         F0[2 * bv_stride + (e0 >> 5) + wl] = sw;
       }
     }
@@ -589,7 +596,7 @@ __device__ __forceinline__ void tile_body(
     if (lane < 12) {
       const int r = lane_ty == 0 ? 1 : lane_ty == 1 ? 2 : lane_ty == 2 ? 4 : 5;  // Cw, Wl, Dm, SDm
       Sw[r * kTileWords + wl0 + lane_m] = lane_ty == 2 ? pick_m(d0w, d1w, d2w) : 0u;
-    } else if (GRID) {  // the frontier and tip words, flushed at the end
+    } else if (SCAT) {  // the frontier and tip words, flushed at the end
       if (lane < 15) Fw[wl0 + lane_m] = pick_m(f0w, f1w, f2w);
       else if (lane >= 18 && lane < 21) Tw[wl0 + lane_m] = pick_m(t0w, t1w, t2w);
     } else if (lane < 21 && (FULL || 32 * (wl0 + lane_m) < nhe)) {
@@ -630,11 +637,11 @@ __device__ __forceinline__ void tile_body(
       const int32_t o = tri_q[q], tg = tri_q[q + 1];
       const uint64_t lo = (uint32_t)min(o, tg), hi = (uint32_t)max(o, tg);
       left_key[pl] = (lo << 32) | hi | (o > tg ? kLeftDown : 0ull);  // undirected key + direction bit
-      left_e[pl++] = (hid)(GRID ? ghe(q) : e0 + j);
+      left_e[pl++] = (hid)(SCAT ? ghe(q) : e0 + j);
     }
     while (dw) {
       const int j = tid * 32 + __ffs(dw) - 1;
-      def_e[pd++] = (hid)(GRID ? ghe(q_of(j)) : e0 + j);
+      def_e[pd++] = (hid)(SCAT ? ghe(q_of(j)) : e0 + j);
       dw &= dw - 1;
     }
   }
@@ -647,7 +654,7 @@ __device__ __forceinline__ void tile_body(
 #pragma unroll 4
     for (int i = 0; i < kHeIters; ++i, q = q_step(q)) {
       const int j = tid + i * kTileThreads;
-      if (GRID) {
+      if (SCAT) {
         if (j >= kTileHE) break;
         if (!here(q >> 2)) continue;
         const int32_t nl = nx_q[q];
@@ -678,25 +685,31 @@ __device__ __forceinline__ void tile_body(
       for (int h = 0; h < kTileHops && !(r & (kSuccFront | kSuccUnknown)); ++h) r = succ[r];
       bool ok = (r & kSuccFront) != 0, tipped = false;
       const bool landed = ok;
-      int32_t mn = 0, n = 0, x = 0;  // quad indices (the same order as half-edge ids)
+      int32_t mn = 0, n = 0, x = 0;  // quad indices (the same order as half-edge ids, but for sorted tiles)
+      int64_t gmin = INT64_MAX;      // (sorted tiles: the minimum global id)
       if (ok) {
         x = r & kSuccIdx;
         int32_t y = x;
         mn = x;
         do {
           mn = min(mn, y);
+          if (SORTED) gmin = min(gmin, ghe(y));
           ++n;
           y = nx_q[y];
           if (y < 0 || n > kP6MaxLen) { ok = false; tipped = y == -2; break; }  // deferred / barrier-tip / long loop
         } while (y != x);
       }
-      if (ok) {
+      if (ok && SORTED) {  // canonical seed = the minimum global id: its bit set in the global C directly
+        len[gmin] = n;
+        const uint32_t gbit = 1u << (gmin & 31);
+        if (!(atomicOr(&C[gmin >> 5], gbit) & gbit)) atomicAdd(&wlen[gmin >> 5], n);  // first setter only
+      } else if (ok) {
         const int64_t gmn = ghe(mn);  // (the loop minimum: quad and half-edge orders agree)
         mn = j_of(mn);
         len[gmn] = n;
         const uint32_t bit = 1u << (mn & 31);
         if (!(atomicOr(&Cw[mn >> 5], bit) & bit)) {  // first setter only
-          if (GRID) atomicAdd(&wlen[gmn >> 5], n);   // (grid: global words, zeroed before the build)
+          if (SCAT) atomicAdd(&wlen[gmn >> 5], n);   // (grid / sorted: global words, zeroed before the build)
           else atomicAdd(&Wl[mn >> 5], n);
         }
       } else if (!tipped) {
@@ -732,6 +745,29 @@ __device__ __forceinline__ void tile_body(
       put(C, Cw[tid]);
       put(SDB, SDm[tid]);
     }
+  } else if (SORTED) {
+    // each triangle's three bits go to global bits 3f .. 3f+2 (f = perm[...]): one (or
+    // two, across a word boundary) atomicOr per array with any bit set
+    for (int u = tid; u < nt; u += kTileThreads) {
+      const int64_t gb = 3 * gtri(u);
+      const int64_t gw = gb >> 5;
+      const int sh = (int)(gb & 31), lj = 3 * u;
+      auto bits3 = [&](const uint32_t* w) -> uint32_t {  // local bits lj .. lj+2 (may straddle a word)
+        const uint64_t two = (uint64_t)w[lj >> 5] | ((lj >> 5) + 1 < kTileWords ? (uint64_t)w[(lj >> 5) + 1] << 32 : 0);
+        return (uint32_t)(two >> (lj & 31)) & 7u;
+      };
+      auto put = [&](uint32_t* base, uint32_t v) {
+        if (!v) return;
+        atomicOr(base + gw, v << sh);
+        if (sh > 29) atomicOr(base + gw + 1, v >> (32 - sh));
+      };
+      const uint32_t f = bits3(Fw);
+      put(F0, f);
+      put(F0 + bv_stride, f);
+      put(F0 + 2 * bv_stride, bits3(Sw));
+      put(F0 + 3 * bv_stride, bits3(Tw));
+      put(SDB, bits3(SDm));  // (C: set directly by P6)
+    }
   } else if (tid * 32 < nhe) {
     const int64_t w = (e0 >> 5) + tid;
     C[w] = Cw[tid];
@@ -744,7 +780,7 @@ __device__ __forceinline__ void tile_body(
 // One CTA per tile; while it works it prefetches into L2 the triangles and vertex
 // coordinates of the tile that will start when it ends.  Full tiles take the specialised
 // body (constant trip counts, no bounds checks), the ragged last tile the generic one.
-template <bool GRID>
+template <int MODE>
 __global__ void __launch_bounds__(kTileThreads, 2)
     k_tile(const double2* __restrict__ xy, const int32_t* __restrict__ tri, int64_t V, int64_t T,
            int32_t* __restrict__ origin, hid* __restrict__ twin, hid* __restrict__ next,
@@ -753,7 +789,7 @@ __global__ void __launch_bounds__(kTileThreads, 2)
            uint32_t* __restrict__ SDB, int32_t* __restrict__ cnt_ld, DevCounters* ctr,
            int64_t prefetch_dist, int64_t tile_base, const Tiling tl) {
   extern __shared__ __align__(16) unsigned char smem_tile[];
-  const int64_t ntiles = GRID ? tl.ntiles : (T + kTileTris - 1) / kTileTris;
+  const int64_t ntiles = MODE != kTileContig ? tl.ntiles : (T + kTileTris - 1) / kTileTris;
   // tiles [tile_base, tile_base + gridDim.x): all of them, or one chunk of an upload
   // pipeline (polylla_run_host)
   const int64_t tile = tile_base + sched_tile(blockIdx.x, gridDim.x);
@@ -761,17 +797,17 @@ __global__ void __launch_bounds__(kTileThreads, 2)
   // kResident at a time): its data is prefetched into L2, which every SM shares
   const int64_t nxt = tile + prefetch_dist < ntiles ? tile + prefetch_dist : -1;
   bool full;
-  if (GRID) {
+  if (MODE == kTileGrid) {
     const TileGeom g = tile_geom(tl, T, tile);
     full = g.nrows == kGridTH && g.ncols == kGridTW;
   } else {
     full = (tile + 1) * kTileTris <= T;
   }
   if (full)
-    tile_body<true, GRID>(smem_tile, tl, xy, tri, V, T, origin, twin, next, lcode, F0, bv_stride, C, len, wlen,
+    tile_body<true, MODE>(smem_tile, tl, xy, tri, V, T, origin, twin, next, lcode, F0, bv_stride, C, len, wlen,
                           left_key, left_e, def_e, SDB, cnt_ld, ctr, tile, nxt);
   else
-    tile_body<false, GRID>(smem_tile, tl, xy, tri, V, T, origin, twin, next, lcode, F0, bv_stride, C, len, wlen,
+    tile_body<false, MODE>(smem_tile, tl, xy, tri, V, T, origin, twin, next, lcode, F0, bv_stride, C, len, wlen,
                            left_key, left_e, def_e, SDB, cnt_ld, ctr, tile, nxt);
 }
 
@@ -1071,9 +1107,130 @@ __global__ void k_border_next(DevCounters* ctr, int64_t T3, const int32_t* __res
   }
 }
 
-Tiling make_tiling(int64_t T, int64_t R) {
+// ---- the sorted tiling (POLYLLA_BUILD_SORT): a counting sort of the triangles by the
+// Morton cell (8 bits per axis) of their first vertex in the bounding box of the vertices
+// (one coordinate gather per triangle; any point of the triangle groups as well).
+// Only the grouping into tiles depends on it (every output is the same bits for any
+// order), so ties within a cell are left in atomic order.
+__device__ __forceinline__ unsigned long long ord_of(double d) {  // order-preserving uint64 of a double
+  const unsigned long long u = (unsigned long long)__double_as_longlong(d);
+  return (u >> 63) ? ~u : (u | 0x8000000000000000ull);
+}
+__device__ __forceinline__ double of_ord(unsigned long long o) {
+  return __longlong_as_double((long long)((o >> 63) ? (o & 0x7FFFFFFFFFFFFFFFull) : ~o));
+}
+__global__ void k_sort_init(unsigned long long* bbox, uint32_t* hist, int64_t cells) {
+  if (blockIdx.x == 0 && threadIdx.x < 4) bbox[threadIdx.x] = (threadIdx.x & 1) ? 0ull : ~0ull;  // min x, max x, min y, max y
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < cells; i += (int64_t)gridDim.x * blockDim.x)
+    hist[i] = 0;
+}
+__global__ void __launch_bounds__(256) k_sort_bbox(const double2* __restrict__ xy, int64_t V, unsigned long long* bbox) {
+  __shared__ unsigned long long red[4][8];
+  unsigned long long mnx = ~0ull, mxx = 0, mny = ~0ull, mxy = 0;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < V; i += (int64_t)gridDim.x * blockDim.x) {
+    const double2 p = xy[i];
+    const unsigned long long ox = ord_of(p.x), oy = ord_of(p.y);
+    mnx = min(mnx, ox); mxx = max(mxx, ox); mny = min(mny, oy); mxy = max(mxy, oy);
+  }
+#pragma unroll
+  for (int o = 16; o; o >>= 1) {
+    mnx = min(mnx, __shfl_xor_sync(0xffffffffu, mnx, o));
+    mxx = max(mxx, __shfl_xor_sync(0xffffffffu, mxx, o));
+    mny = min(mny, __shfl_xor_sync(0xffffffffu, mny, o));
+    mxy = max(mxy, __shfl_xor_sync(0xffffffffu, mxy, o));
+  }
+  const int w = threadIdx.x >> 5;
+  if ((threadIdx.x & 31) == 0) { red[0][w] = mnx; red[1][w] = mxx; red[2][w] = mny; red[3][w] = mxy; }
+  __syncthreads();
+  if (threadIdx.x == 0) {  // one atomic per block and bound (warp-level atomics serialised on 4 words)
+    for (int k = 1; k < 8; ++k) {
+      mnx = min(mnx, red[0][k]); mxx = max(mxx, red[1][k]); mny = min(mny, red[2][k]); mxy = max(mxy, red[3][k]);
+    }
+    atomicMin(bbox, mnx); atomicMax(bbox + 1, mxx); atomicMin(bbox + 2, mny); atomicMax(bbox + 3, mxy);
+  }
+}
+__device__ __forceinline__ uint32_t spread8(uint32_t v) {  // 8 bits -> every other bit of 16
+  v &= 0xFFu;
+  v = (v | (v << 8)) & 0x00FF00FFu;
+  v = (v | (v << 4)) & 0x0F0F0F0Fu;
+  v = (v | (v << 2)) & 0x33333333u;
+  v = (v | (v << 1)) & 0x55555555u;
+  return v;
+}
+__global__ void k_sort_keys(const double2* __restrict__ xy, const int32_t* __restrict__ tri, int64_t V, int64_t T,
+                            const unsigned long long* __restrict__ bbox, uint32_t* __restrict__ key,
+                            uint32_t* hist) {
+  const double x0 = of_ord(bbox[0]), x1 = of_ord(bbox[1]), y0 = of_ord(bbox[2]), y1 = of_ord(bbox[3]);
+  const double sx = x1 > x0 ? 255.999 / (x1 - x0) : 0.0, sy = y1 > y0 ? 255.999 / (y1 - y0) : 0.0;
+  for (int64_t f = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; f < T; f += (int64_t)gridDim.x * blockDim.x) {
+    const int32_t v = tri[3 * f];
+    // (a dangling index is reported by the build; any cell will do)
+    const double2 p = (uint64_t)v < (uint64_t)V ? __ldg(xy + v) : make_double2(x0, y0);
+    const uint32_t qx = (uint32_t)fmin(fmax((p.x - x0) * sx, 0.0), 255.0);
+    const uint32_t qy = (uint32_t)fmin(fmax((p.y - y0) * sy, 0.0), 255.0);
+    const uint32_t cell = spread8(qx) | (spread8(qy) << 1);
+    key[f] = cell;
+    // (neighbouring triangles share cells: one atomic per distinct cell of the warp)
+    const uint32_t peers = __match_any_sync(__activemask(), cell);
+    if ((int)(threadIdx.x & 31) == __ffs(peers) - 1) atomicAdd(&hist[cell], (uint32_t)__popc(peers));
+  }
+}
+// exclusive scan of the cell counts in place: one block of 1024 threads, warp w owns the
+// 8,192 cells from 8,192 w on, read lane-strided (coalesced), two passes
+__global__ void __launch_bounds__(1024) k_sort_scan(uint32_t* hist) {
+  constexpr int per = (int)(kSortCells / 32);  // cells per warp
+  __shared__ uint32_t wsum[32];
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  uint32_t* h = hist + (int64_t)wid * per;
+  uint32_t sum = 0;
+#pragma unroll 8
+  for (int i = lane; i < per; i += 32) sum += h[i];
+  sum = __reduce_add_sync(0xffffffffu, sum);
+  if (lane == 0) wsum[wid] = sum;
+  __syncthreads();
+  if (wid == 0) {
+    const uint32_t w = wsum[lane];
+    uint32_t iw = w;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t a = __shfl_up_sync(0xffffffffu, iw, o);
+      if (lane >= o) iw += a;
+    }
+    wsum[lane] = iw - w;
+  }
+  __syncthreads();
+  uint32_t carry = wsum[wid];
+  for (int i0 = 0; i0 < per; i0 += 32) {
+    const uint32_t c = h[i0 + lane];
+    uint32_t inc = c;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t a = __shfl_up_sync(0xffffffffu, inc, o);
+      if (lane >= o) inc += a;
+    }
+    h[i0 + lane] = carry + inc - c;
+    carry += __shfl_sync(0xffffffffu, inc, 31);
+  }
+}
+__global__ void k_sort_scatter(int64_t T, const uint32_t* __restrict__ key, uint32_t* cursor, int32_t* __restrict__ perm) {
+  for (int64_t f = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; f < T; f += (int64_t)gridDim.x * blockDim.x) {
+    const uint32_t cell = key[f];
+    const uint32_t m = __activemask(), peers = __match_any_sync(m, cell);
+    const int lane = threadIdx.x & 31, leader = __ffs(peers) - 1;
+    uint32_t base = 0;
+    if (lane == leader) base = atomicAdd(&cursor[cell], (uint32_t)__popc(peers));
+    base = __shfl_sync(peers, base, leader);
+    perm[base + __popc(peers & ((1u << lane) - 1))] = (int32_t)f;
+  }
+}
+
+Tiling make_tiling(int64_t T, int64_t R, bool sorted) {
   Tiling g;
-  if (R > 0 && T % R == 0) {
+  if (sorted) {
+    g.mode = kTileSorted;
+    g.ntiles = (T + kTileTris - 1) / kTileTris;
+  } else if (R > 0 && T % R == 0) {
+    g.mode = kTileGrid;
     g.R = R;
     g.nrows = T / R;
     g.ntc = (R + kGridTW - 1) / kGridTW;
@@ -1096,8 +1253,9 @@ static int device_setup(int* n_sm) {
   if (cudaGetDevice(&dev) != cudaSuccess) return -1;
   std::lock_guard<std::mutex> lk(g_dev_mu);
   if (dev >= 64 || !((g_dev_ready >> dev) & 1)) {
-    if (cudaFuncSetAttribute(k_tile<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kTileSmem) != cudaSuccess ||
-        cudaFuncSetAttribute(k_tile<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kTileSmemGrid) != cudaSuccess)
+    if (cudaFuncSetAttribute(k_tile<kTileContig>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kTileSmem) != cudaSuccess ||
+        cudaFuncSetAttribute(k_tile<kTileGrid>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kTileSmemGrid) != cudaSuccess ||
+        cudaFuncSetAttribute(k_tile<kTileSorted>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kTileSmemGrid) != cudaSuccess)
       return -1;
     int sms = 0;
     if (cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess) return -1;
@@ -1123,12 +1281,22 @@ static int64_t prefetch_distance(int n_sm) {
 // the start of a build: counters zeroed, per-device setup
 int launch_build_begin(Ctx* c, cudaStream_t s) {
   if (cudaMemsetAsync(c->ctr, 0, sizeof(DevCounters), s) != cudaSuccess) return -1;
-  if (c->tiling.R) {  // grid tiles OR their words into the bit-vectors (shared words): zero them
+  if (c->tiling.mode != kTileContig) {  // grid / sorted tiles OR their words into the bit-vectors: zero them
     const size_t wb = (size_t)c->n_words * 4;
     if (cudaMemsetAsync(c->F0, 0, (size_t)(c->TB - c->F0) * 4 + wb, s) != cudaSuccess ||
         cudaMemsetAsync(c->C, 0, wb, s) != cudaSuccess || cudaMemsetAsync(c->SDB, 0, wb, s) != cudaSuccess ||
         cudaMemsetAsync(c->wlen, 0, wb, s) != cudaSuccess || cudaMemsetAsync(c->BB, 0, wb, s) != cudaSuccess)
       return -1;
+  }
+  if (c->tiling.mode == kTileSorted) {  // the triangle order of the sorted tiling
+    const unsigned g = 148 * 8;
+    k_sort_init<<<g, 256, 0, s>>>(c->sort_bbox, c->sort_hist, kSortCells);
+    k_sort_bbox<<<g, 256, 0, s>>>(reinterpret_cast<const double2*>(c->xy), c->V, c->sort_bbox);
+    k_sort_keys<<<g, 256, 0, s>>>(reinterpret_cast<const double2*>(c->xy), c->tri, c->V, c->T, c->sort_bbox,
+                                  c->sort_key, c->sort_hist);
+    k_sort_scan<<<1, 1024, 0, s>>>(c->sort_hist);
+    k_sort_scatter<<<g, 256, 0, s>>>(c->T, c->sort_key, c->sort_hist, const_cast<int32_t*>(c->tiling.perm));
+    if (cudaGetLastError() != cudaSuccess) return -1;
   }
   int n_sm = 0;
   return device_setup(&n_sm);
@@ -1143,8 +1311,9 @@ int launch_build_tiles(Ctx* c, cudaStream_t s, int64_t t0, int64_t t1) {
   const int64_t bv_stride = c->F1 - c->F0;  // F0, F1, S, TB are equally spaced (capi.cu layout)
   if (c->S - c->F1 != bv_stride || c->TB - c->S != bv_stride) return -1;
   prof_mark(s, "k_tile");
-  auto kt = c->tiling.R ? k_tile<true> : k_tile<false>;
-  kt<<<(unsigned)(t1 - t0), kTileThreads, c->tiling.R ? kTileSmemGrid : kTileSmem, s>>>(reinterpret_cast<const double2*>(c->xy), c->tri, c->V, c->T,
+  auto kt = c->tiling.mode == kTileGrid ? k_tile<kTileGrid> : c->tiling.mode == kTileSorted ? k_tile<kTileSorted>
+                                                                                         : k_tile<kTileContig>;
+  kt<<<(unsigned)(t1 - t0), kTileThreads, c->tiling.mode != kTileContig ? kTileSmemGrid : kTileSmem, s>>>(reinterpret_cast<const double2*>(c->xy), c->tri, c->V, c->T,
                                                           c->origin, c->twin, c->next, c->lcode, c->F0, bv_stride, c->C,
                                                           c->len, c->wlen, c->left_key, c->left_e, c->def_e, c->SDB,
                                                           c->cnt_ld, c->ctr, pf_dist, t0, c->tiling);
@@ -1175,7 +1344,7 @@ int launch_build_rest(Ctx* c, cudaStream_t s) {
   const unsigned left_grid = (unsigned)(tiles < 148 * (4096 / POLYLLA_LEFT_THREADS) ? tiles : 148 * (4096 / POLYLLA_LEFT_THREADS));
   k_left_insert<<<left_grid, POLYLLA_LEFT_THREADS, 0, s>>>(c->ctr, tiles, c->T, c->tiling, c->cnt_ld, c->left_key,
                                                            c->left_e, c->twin, ehash);
-  if (c->tiling.R) {  // grid tiles: the border ranking by bit order
+  if (c->tiling.mode != kTileContig) {  // grid / sorted tiles: the border ranking by bit order
     const int64_t nchunks = (c->n_words + kBBChunk - 1) / kBBChunk;
     k_bb_mark<<<seg_grid, kSegThreads, 0, s>>>(c->ctr, tiles, c->T, c->tiling, c->cnt_ld, c->left_e, c->twin, c->BB);
     k_bb_count<<<(unsigned)((nchunks + 7) / 8), 256, 0, s>>>(c->ctr, c->n_words, nchunks, c->BB, c->bcnt);

@@ -27,9 +27,11 @@ struct Layout {
 
 // region order; sizes in bytes.  Hmax = 3T + Bmax (the caller's bound on the border
 // half-edges; 3T covers every mesh); the run_host staging regions only when `staging`.
-static Layout layout(int64_t V, int64_t T, int64_t Bmax, bool staging, int64_t R) {
+static Layout layout(int64_t V, int64_t T, int64_t Bmax, bool staging, int64_t R, bool sorted) {
   const int64_t Hmax = 3 * T + Bmax;
-  const int64_t bt = make_tiling(T, R).ntiles;  // build tiles (grid tilings have more, partial ones)
+  const Tiling tg = make_tiling(T, R, sorted);
+  const int64_t bt = tg.ntiles;  // build tiles (grid tilings have more, partial ones)
+  const bool scat = tg.mode != kTileContig;
   const int64_t ct = (T + 2047) / 2048;          // contiguous tiles (emission, canonical sums)
   const int64_t nw = (3 * T + 31) / 32;
   const int64_t nb = (nw + 2047) / 2048 + 1;
@@ -52,7 +54,7 @@ static Layout layout(int64_t V, int64_t T, int64_t Bmax, bool staging, int64_t R
       0,                      // 14 (unused)
       (size_t)V * 4,          // 15 tips
       (size_t)(2 * V) * 4,    // 16 aff
-      R > 0 ? (size_t)nw * 4 : 0,  // 17 BB: unmatched leftovers (grid tiling)
+      scat ? (size_t)nw * 4 : 0,  // 17 BB: unmatched leftovers (grid / sorted tiling)
       (size_t)nb * 8,         // 18 scan_a
       (size_t)nb * 8,         // 19 scan_b
       (size_t)nb * 8,         // 20 scan_c
@@ -69,6 +71,10 @@ static Layout layout(int64_t V, int64_t T, int64_t Bmax, bool staging, int64_t R
       (size_t)(2 * bt + 2) * 4,  // 31 per-build-tile leftover / deferred counts
       (size_t)(3 * ((T + 2047) / 2048) + 2) * 4,  // 32 per-tile canonical-seed sums
       (size_t)(2 * ((T + 2047) / 2048) + 2) * 4,  // 33 per-tile polygon / loop-entry bases
+      sorted ? (size_t)T * 4 : 0,                 // 34 (sorted tiling) perm
+      sorted ? (size_t)T * 4 : 0,                 // 35 (sorted tiling) Morton cell keys
+      sorted ? (size_t)kSortCells * 4 : 0,        // 36 (sorted tiling) cell counts / cursors
+      sorted ? (size_t)32 : 0,                    // 37 (sorted tiling) bounding box
   };
   Layout L{};
   static_assert(sizeof(sz) / sizeof(sz[0]) <= sizeof(L.off) / sizeof(L.off[0]), "Layout::off too small");
@@ -81,13 +87,14 @@ static Layout layout(int64_t V, int64_t T, int64_t Bmax, bool staging, int64_t R
   return L;
 }
 
-size_t workspace_bytes(int64_t V, int64_t T, int64_t Bmax, bool staging, int64_t R) {
-  return layout(V, T, Bmax, staging, R).total;
+size_t workspace_bytes(int64_t V, int64_t T, int64_t Bmax, bool staging, int64_t R, bool sorted) {
+  return layout(V, T, Bmax, staging, R, sorted).total;
 }
 
 bool carve(Ctx* c, void* ws, size_t bytes) {
-  c->tiling = make_tiling(c->T, c->tiling.R);
-  const Layout L = layout(c->V, c->T, c->Bmax, c->staging, c->tiling.R);
+  const bool sorted = c->tiling.mode == kTileSorted;  // (new_ctx: the requested tiling)
+  c->tiling = make_tiling(c->T, c->tiling.R, sorted);
+  const Layout L = layout(c->V, c->T, c->Bmax, c->staging, c->tiling.R, sorted);
   if (bytes < L.total || (reinterpret_cast<uintptr_t>(ws) & 255)) return false;
   char* b = static_cast<char*>(ws);
   c->Hmax = 3 * c->T + c->Bmax;
@@ -109,7 +116,13 @@ bool carve(Ctx* c, void* ws, size_t bytes) {
   c->tips = reinterpret_cast<hid*>(b + L.off[15]);
   c->aff = reinterpret_cast<hid*>(b + L.off[16]);
   c->mids = nullptr;
-  c->BB = c->tiling.R ? reinterpret_cast<uint32_t*>(b + L.off[17]) : nullptr;
+  c->BB = c->tiling.mode != kTileContig ? reinterpret_cast<uint32_t*>(b + L.off[17]) : nullptr;
+  if (sorted) {
+    c->tiling.perm = reinterpret_cast<int32_t*>(b + L.off[34]);
+    c->sort_key = reinterpret_cast<uint32_t*>(b + L.off[35]);
+    c->sort_hist = reinterpret_cast<uint32_t*>(b + L.off[36]);
+    c->sort_bbox = reinterpret_cast<unsigned long long*>(b + L.off[37]);
+  }
   c->scan_a = reinterpret_cast<long long*>(b + L.off[18]);
   c->scan_b = reinterpret_cast<long long*>(b + L.off[19]);
   c->scan_c = reinterpret_cast<long long*>(b + L.off[20]);
@@ -201,7 +214,8 @@ POLYLLA_API size_t polylla_workspace_bytes(int64_t n_vertices, int64_t n_triangl
 POLYLLA_API size_t polylla_workspace_bytes_ex(int64_t n_vertices, int64_t n_triangles, int64_t max_border,
                                               uint32_t flags, int64_t row_stride) {
   if (n_vertices < 0 || n_triangles < 0 || max_border < 0 || max_border > 3 * n_triangles || row_stride < 0) return 0;
-  return workspace_bytes(n_vertices, n_triangles, max_border, (flags & POLYLLA_WS_STAGING) != 0, row_stride);
+  return workspace_bytes(n_vertices, n_triangles, max_border, (flags & POLYLLA_WS_STAGING) != 0, row_stride,
+                         (flags & POLYLLA_BUILD_SORT) != 0);
 }
 
 // index limits (NEXT-3): vertex ids int32; half-edge ids uint32 with H <= 2^32 - 2
@@ -211,7 +225,8 @@ static bool index_ok(int64_t V, int64_t T, int64_t Bmax) {
 
 // a new ctx over caller memory (no launches): argument checks + workspace carving
 static polylla_status new_ctx(const double* xy, int64_t V, const int32_t* tri, int64_t T, int64_t Bmax,
-                              bool staging, int64_t R, void* workspace, size_t workspace_bytes_, polylla_ctx** out) {
+                              bool staging, int64_t R, void* workspace, size_t workspace_bytes_, polylla_ctx** out,
+                              bool sorted = false) {
   *out = nullptr;
   if (!xy || !tri || !workspace || V < 3 || T < 1 || Bmax < 0 || Bmax > 3 * T || R < 0)
     return POLYLLA_E_INVALID_ARGUMENT;
@@ -227,7 +242,8 @@ static polylla_status new_ctx(const double* xy, int64_t V, const int32_t* tri, i
   c->T = T;
   c->Bmax = Bmax;
   c->staging = staging;
-  c->tiling.R = R;  // (carve() derives the tiling: contiguous unless R divides T)
+  c->tiling.R = R;  // (carve() derives the tiling: sorted if asked, else grid if R divides T, else contiguous)
+  c->tiling.mode = sorted ? kTileSorted : kTileContig;
   if (!carve(c, workspace, workspace_bytes_)) {
     std::free(p);
     return POLYLLA_E_WORKSPACE;
@@ -243,7 +259,7 @@ POLYLLA_API polylla_status polylla_build_halfedges_ex(const double* xy, int64_t 
   if (!ctx_out) return POLYLLA_E_INVALID_ARGUMENT;
   polylla_ctx* p = nullptr;
   const polylla_status st = new_ctx(xy, V, tri, T, max_border, (flags & POLYLLA_WS_STAGING) != 0, row_stride,
-                                    workspace, workspace_bytes_, &p);
+                                    workspace, workspace_bytes_, &p, (flags & POLYLLA_BUILD_SORT) != 0);
   if (st != POLYLLA_OK) return st;
   Ctx* c = &p->c;
   const int n = launch_build(c, S(stream));

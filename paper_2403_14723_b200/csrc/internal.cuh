@@ -63,11 +63,17 @@ struct DevCounters {
 // t = tr * ntc + tc; its local triangle u = 128 r + c is triangle (16 tr + r) R + 128 tc + c.
 // A thin strip of one row cuts a third of all edges; a 16 x 128 patch cuts ~3%.
 constexpr int kGridTW = 128, kGridTH = 16, kGridTWShift = 7;  // kGridTW * kGridTH = 2048 triangles
+// Sorted tiling (POLYLLA_BUILD_SORT, any input order): the build first orders the
+// triangles by the Morton cell of their centroid (a counting sort into ~T/16 cells of the
+// bounding box) and tile t takes triangles perm[2048 t .. 2048 t + 2048).
+enum : int { kTileContig = 0, kTileGrid = 1, kTileSorted = 2 };
 struct Tiling {
-  int64_t R = 0;      // triangles per row (0: contiguous tiles)
-  int64_t nrows = 0;  // T / R
-  int64_t ntc = 0;    // column tiles per band: ceil(R / 128)
+  int mode = kTileContig;
+  int64_t R = 0;      // (grid) triangles per row
+  int64_t nrows = 0;  // (grid) T / R
+  int64_t ntc = 0;    // (grid) column tiles per band: ceil(R / 128)
   int64_t ntiles = 0;
+  const int32_t* perm = nullptr;  // (sorted) triangle order
 };
 struct TileGeom {
   int64_t base;       // global triangle of local triangle 0
@@ -84,7 +90,7 @@ __host__ __device__ __forceinline__ TileGeom contig_geom(int64_t T, int64_t tile
   return r;
 }
 __host__ __device__ __forceinline__ TileGeom tile_geom(const Tiling& g, int64_t T, int64_t tile) {
-  if (!g.R) return contig_geom(T, tile);
+  if (g.mode != kTileGrid) return contig_geom(T, tile);  // (sorted tiles: positions in perm)
   TileGeom r;
   const int64_t tr = tile / g.ntc, tc = tile - tr * g.ntc;
   const int64_t row0 = tr * kGridTH, col0 = tc * kGridTW;
@@ -94,7 +100,7 @@ __host__ __device__ __forceinline__ TileGeom tile_geom(const Tiling& g, int64_t 
   r.seg = 3 * (row0 * g.R + col0 * r.nrows);
   return r;
 }
-Tiling make_tiling(int64_t T, int64_t R);  // R <= 0, or T % R != 0: contiguous
+Tiling make_tiling(int64_t T, int64_t R, bool sorted);  // sorted > grid (R > 0 dividing T) > contiguous
 
 struct Ctx {
   // inputs
@@ -105,7 +111,10 @@ struct Ctx {
   int64_t Bmax;  // border bound of the workspace layout
   bool staging;  // the layout holds run_host's staging regions
   Tiling tiling; // the build tiling (contiguous unless a row stride was given)
-  uint32_t* BB;  // [n_words] unmatched leftovers (grid tiling: the border ranking by bit scan)
+  uint32_t* BB;  // [n_words] unmatched leftovers (grid/sorted tiling: the border ranking by bit scan)
+  uint32_t* sort_key;   // (sorted tiling) [T] Morton cell of each triangle
+  uint32_t* sort_hist;  // (sorted tiling) [kSortCells] cell counts, then cursors
+  unsigned long long* sort_bbox;  // (sorted tiling) [4] order-preserving encodings of min/max x, y
   // workspace views
   int32_t* origin;   // vertex ids
   hid *twin, *next;
@@ -152,7 +161,8 @@ void prof_mark(cudaStream_t s, const char* name);  // start of kernel `name` (en
 void prof_end(cudaStream_t s);
 
 // workspace
-size_t workspace_bytes(int64_t V, int64_t T, int64_t Bmax, bool staging, int64_t R = 0);
+constexpr int64_t kSortCells = int64_t(1) << 16;  // Morton cells (8 bits per axis) for the sorted tiling
+size_t workspace_bytes(int64_t V, int64_t T, int64_t Bmax, bool staging, int64_t R = 0, bool sorted = false);
 bool carve(Ctx* c, void* ws, size_t bytes);  // layout from c->V, c->T, c->Bmax, c->staging
 
 // launchers (each returns the number of kernel launches issued, < 0 on CUDA error)

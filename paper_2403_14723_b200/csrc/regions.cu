@@ -204,7 +204,7 @@ int launch_regions(Ctx* c, int32_t* out, int mode, cudaStream_t s) {
   const uint32_t* F = mode == 1 ? c->F0 : c->F1;
   const unsigned g = 148 * 8;
   prof_mark(s, mode == 1 ? "k_regions_pre" : "k_regions");
-  hid* cross = c->tiling.R ? reinterpret_cast<hid*>(slot + c->T) : nullptr;  // (16T bytes left of the 24T scratch)
+  hid* cross = c->tiling.mode != kTileContig ? reinterpret_cast<hid*>(slot + c->T) : nullptr;  // (16T bytes left of the 24T scratch)
   if (cross) cudaMemsetAsync(&c->ctr->n_cross, 0, 4, s);
   k_uf_local<<<(unsigned)((c->T + kUfTile - 1) / kUfTile), kUfThreads, 0, s>>>(c->T, c->twin, F, parent, slot,
                                                                                  cross, c->ctr);

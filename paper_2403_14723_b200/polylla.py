@@ -34,6 +34,7 @@ EXPORTS = (
 )
 
 WS_STAGING = 1  # POLYLLA_WS_STAGING
+BUILD_SORT = 2  # POLYLLA_BUILD_SORT
 
 
 class PolyllaError(RuntimeError):
@@ -151,40 +152,46 @@ class Context:
             destroy(self)
 
 
+def _flags(staging: bool, sort: bool) -> int:
+    return (WS_STAGING if staging else 0) | (BUILD_SORT if sort else 0)
+
+
 def workspace_bytes(n_vertices: int, n_triangles: int, max_border: int | None = None, staging: bool = True,
-                    row_stride: int = 0) -> int:
+                    row_stride: int = 0, sort: bool = False) -> int:
     """polylla_workspace_bytes, or polylla_workspace_bytes_ex when a border bound, a row
-    stride or staging=False is given (the capacity path; grid tiling)."""
-    if max_border is None and staging and not row_stride:
+    stride, sort=True or staging=False is given (the capacity path; grid or
+    sorted tiling)."""
+    if max_border is None and staging and not row_stride and not sort:
         return int(lib().polylla_workspace_bytes(n_vertices, n_triangles))
     mb = 3 * n_triangles if max_border is None else max_border
-    return int(lib().polylla_workspace_bytes_ex(n_vertices, n_triangles, mb, WS_STAGING if staging else 0,
-                                                row_stride))
+    return int(lib().polylla_workspace_bytes_ex(n_vertices, n_triangles, mb, _flags(staging, sort), row_stride))
 
 
 def alloc_workspace(n_vertices: int, n_triangles: int, device="cuda", max_border: int | None = None,
-                    staging: bool = True, row_stride: int = 0) -> torch.Tensor:
-    return torch.empty(workspace_bytes(n_vertices, n_triangles, max_border, staging, row_stride), dtype=torch.uint8,
-                       device=device)
+                    staging: bool = True, row_stride: int = 0, sort: bool = False) -> torch.Tensor:
+    return torch.empty(workspace_bytes(n_vertices, n_triangles, max_border, staging, row_stride, sort),
+                       dtype=torch.uint8, device=device)
 
 
 def build_halfedges(xy: torch.Tensor, tri: torch.Tensor, workspace: torch.Tensor, stream=None,
-                    max_border: int | None = None, staging: bool = True, row_stride: int = 0) -> Context:
+                    max_border: int | None = None, staging: bool = True, row_stride: int = 0,
+                    sort: bool = False) -> Context:
     """polylla_build_halfedges; with a border bound, a row stride (row-major input: grid
-    tiles) or staging=False polylla_build_halfedges_ex over a workspace from
-    alloc_workspace(..., max_border, staging, row_stride) (the same arguments)."""
+    tiles), sort=True (any input order: tiles over the Morton-sorted triangles) or
+    staging=False polylla_build_halfedges_ex over a workspace from
+    alloc_workspace(..., max_border, staging, row_stride, sort) (the same arguments)."""
     if not (xy.is_cuda and tri.is_cuda and workspace.is_cuda):
         raise ValueError("xy, tri and workspace must be CUDA tensors")
     if xy.dtype != torch.float64 or tri.dtype != torch.int32 or not xy.is_contiguous() or not tri.is_contiguous():
         raise ValueError("xy must be contiguous float64 [V,2], tri contiguous int32 [T,3]")
     h = ctypes.c_void_p()
-    if max_border is None and staging and not row_stride:
+    if max_border is None and staging and not row_stride and not sort:
         rc = lib().polylla_build_halfedges(_ptr(xy), xy.shape[0], _ptr(tri), tri.shape[0], _ptr(workspace),
                                            workspace.numel(), _stream(stream), ctypes.byref(h))
     else:
         mb = 3 * tri.shape[0] if max_border is None else max_border
         rc = lib().polylla_build_halfedges_ex(_ptr(xy), xy.shape[0], _ptr(tri), tri.shape[0], mb,
-                                              WS_STAGING if staging else 0, row_stride, _ptr(workspace),
+                                              _flags(staging, sort), row_stride, _ptr(workspace),
                                               workspace.numel(), _stream(stream), ctypes.byref(h))
     _check(rc, "polylla_build_halfedges")
     return Context(h, xy, tri, workspace)
@@ -288,13 +295,13 @@ def status_string(code: int) -> str:
 # ----------------------------------------------------------------------- conveniences
 
 def run(xy: torch.Tensor, tri: torch.Tensor, stream=None, arrays=True, prev=False, debug=False,
-        regions=False, check=False, paper=False, row_stride=0) -> dict:
+        regions=False, check=False, paper=False, row_stride=0, sort=False) -> dict:
     """build -> label -> generate -> get_counts -> get_polygons on device tensors.
     Returns a dict of torch tensors (offsets, loops, seeds, [origin, twin, next, prev],
     [lcode, frontier0, frontier1, seed_bits, next_pre]) plus the counts."""
     V, T = xy.shape[0], tri.shape[0]
-    ws = alloc_workspace(V, T, xy.device, row_stride=row_stride)
-    ctx = build_halfedges(xy, tri, ws, stream, row_stride=row_stride)
+    ws = alloc_workspace(V, T, xy.device, row_stride=row_stride, sort=sort)
+    ctx = build_halfedges(xy, tri, ws, stream, row_stride=row_stride, sort=sort)
     if check:
         check_manifold(ctx, stream)
     next_pre = None
@@ -386,7 +393,7 @@ class GraphStep:
     The C ABI is called unchanged during capture; its kernels read the mesh size from the
     workspace counters on the device, so a replay recomputes everything."""
 
-    def __init__(self, xy, tri, workspace, offsets, loops, stream=None, paper=False, row_stride=0):
+    def __init__(self, xy, tri, workspace, offsets, loops, stream=None, paper=False, row_stride=0, sort=False):
         self.stream = stream or torch.cuda.Stream(device=xy.device)
 
         def lg(ctx, st):
@@ -398,7 +405,7 @@ class GraphStep:
         self.args = (xy, tri, workspace, offsets, loops)
         # warm once outside capture (lazy CUDA attribute setup inside the library)
         with torch.cuda.stream(self.stream):
-            ctx = build_halfedges(xy, tri, workspace, self.stream, row_stride=row_stride)
+            ctx = build_halfedges(xy, tri, workspace, self.stream, row_stride=row_stride, sort=sort)
             lg(ctx, self.stream)
             get_polygons(ctx, offsets, loops, stream=self.stream)
             self.launches = launch_count(ctx)
@@ -407,7 +414,7 @@ class GraphStep:
         self.graph = torch.cuda.CUDAGraph()
         with torch.cuda.graph(self.graph, stream=self.stream):
             s = torch.cuda.current_stream()
-            ctx = build_halfedges(xy, tri, workspace, s, row_stride=row_stride)
+            ctx = build_halfedges(xy, tri, workspace, s, row_stride=row_stride, sort=sort)
             lg(ctx, s)
             get_polygons(ctx, offsets, loops, stream=s)
             destroy(ctx)

@@ -55,6 +55,14 @@ gr = pp.run(torch.from_numpy(gx).cuda(), torch.from_numpy(gt).cuda(), row_stride
 for k in ("origin", "twin", "next", "prev"):
     assert np.array_equal(gr[k].cpu().numpy(), go[k]), k
 assert np.array_equal(gr["poly_of_tri"].cpu().numpy(), oracle.triangle_polygons(go))
+# sorted tiling (POLYLLA_BUILD_SORT) on a shuffled mesh
+sx, st = synth.random_delaunay(5000, 31)
+st = np.ascontiguousarray(st[np.random.default_rng(2).permutation(st.shape[0])])
+so = oracle.run(sx, st)
+sr = pp.run(torch.from_numpy(sx).cuda(), torch.from_numpy(st).cuda(), sort=True, prev=True, regions=True)
+for k in ("origin", "twin", "next", "prev"):
+    assert np.array_equal(sr[k].cpu().numpy(), so[k]), k
+assert np.array_equal(sr["loops"].cpu().numpy(), so["loops"])
 h = pp.run_host(xy, tri)
 assert np.array_equal(h["loops"].numpy(), o["loops"]) and np.array_equal(h["next"].numpy(), o["next"])
-print("sanitize cases ok", len(cases) + 4)
+print("sanitize cases ok", len(cases) + 5)

@@ -20,13 +20,13 @@ from test_gpu_parity import bits_to_bool
 pytestmark = pytest.mark.gpu
 
 
-def _check(xy, tri, R):
+def _check(xy, tri, R, sort=False):
     from paper_2403_14723_b200 import polylla as pp
     T = tri.shape[0]
-    assert T % R == 0
+    assert sort or T % R == 0
     ref = oracle.run(xy, tri)
     res = pp.run(torch.from_numpy(xy).cuda(), torch.from_numpy(np.ascontiguousarray(tri)).cuda(), row_stride=R,
-                 debug=True, prev=True, regions=True)
+                 debug=True, prev=True, regions=True, sort=sort)
     assert (res["H"], res["P"], res["L"], res["n_tips"]) == (ref["H"], ref["P"], ref["L"], ref["n_tips"])
     for k in ("origin", "twin", "next", "prev", "seeds", "offsets", "loops"):
         np.testing.assert_array_equal(res[k].cpu().numpy(), ref[k], err_msg=k)
@@ -66,3 +66,24 @@ def test_grid_tiles_any_stride(shuffle):
         tri = np.ascontiguousarray(tri[np.random.default_rng(4).permutation(T)])
     R = next(d for d in range(300, T + 1) if T % d == 0)  # a divisor of T unrelated to the mesh
     _check(xy, tri, R)
+
+
+@pytest.mark.parametrize("name", ["shuffled", "random", "grid", "fan", "tie", "holes"])
+def test_sorted_tiles(name):
+    """The sorted tiling (POLYLLA_BUILD_SORT: tiles over the Morton-cell order of the
+    triangle centroids, for any input order), bit-exact vs the oracle."""
+    from test_gpu_parity import _grid_with_holes
+    if name == "shuffled":
+        xy, tri = synth.random_delaunay(40000, 13)
+        tri = np.ascontiguousarray(tri[np.random.default_rng(5).permutation(tri.shape[0])])
+    elif name == "random":
+        xy, tri = synth.random_delaunay(30000, 14)
+    elif name == "grid":
+        xy, tri = synth.grid(120, 0.2, 2)
+    elif name == "holes":
+        xy, tri = _grid_with_holes()
+    else:
+        xy, tri = {"fan": synth.fixture_fan, "tie": synth.fixture_tie_lattice}[name]()
+    res = _check(xy, tri, 0, sort=True)
+    if name == "shuffled":  # the point of it: few leftovers although the input order is random
+        assert res["n_leftover"] < 0.10 * 3 * tri.shape[0]

@@ -11,6 +11,7 @@ python profiles/tools/ncu_traffic.py 3 $O/launches_c3.csv > $O/ncu_traffic.txt 2
 timeout 900 python bench.py > $O/bench_c3.json 2> $O/bench_c3.err
 timeout 900 python bench.py --config 2 > $O/bench_c2.json 2> $O/bench_c2.err
 timeout 900 python bench.py --config 2 --order shuffled --no-cpu-baseline > $O/bench_c2_shuffled.json 2> $O/bench_c2_shuffled.err
+timeout 900 python bench.py --config 2 --order shuffled --sort --no-cpu-baseline --no-e2e > $O/bench_c2_shuffled_sort.json 2> $O/bench_c2_shuffled_sort.err
 timeout 900 python bench.py --config 5 --steps 5 --warmup 3 > $O/bench_c5.json 2> $O/bench_c5.err
 timeout 900 python bench.py --config 4 --steps 3 --warmup 3 --no-e2e --no-cpu-baseline > $O/bench_c4.json 2> $O/bench_c4.err
 timeout 900 python bench.py --config 5 --steps 5 --warmup 3 --no-cpu-baseline --no-e2e --no-row-hint > $O/bench_c5_contiguous.json 2> $O/bench_c5_contiguous.err
