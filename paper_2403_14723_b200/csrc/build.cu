@@ -29,8 +29,17 @@ namespace polylla {
 constexpr int kTileTris = kBuildTileTris;
 constexpr int kTileHE = 3 * kTileTris;   // 6144 half-edges = 192 bit-vector words (e order)
 constexpr int kTileQ = 4 * kTileTris;    // quad slots q = 4t + k (slot 3: copy of vertex 0 / unused)
-constexpr int kTileSlots = 16384;        // pow2 hash slots of 16 bits (load ~0.19: only the lo->hi halves insert)
-constexpr int kSlotBits = 14;            // log2(kTileSlots)
+#ifndef POLYLLA_TILE_SLOTS
+#define POLYLLA_TILE_SLOTS 24000  // (a multiple of 8, >= 4,096; measured 12,288 / 15,360 / 19,456 / 21,504 / 22,528 / 24,000)
+#endif
+// hash slots of 16 bits (only the lo->hi halves insert: 3,072 keys, load 0.13); the table
+// overlays the P3-P6 arrays.  The tile's shared memory also decides the L1 left for the
+// coordinate gathers (the carveout is the smallest that holds two CTAs): 105 KB per CTA
+// (228 KB carveout, 28 KB of L1) -> 90 KB (196 KB, 60 KB of L1) cut k_tile by 11% on
+// config 3; within the 196 KB carveout a larger table then pays (fewer collision losers
+// and probing lookups): 99,200 B per CTA with 24,000 slots, the most that stays inside it.
+constexpr int kTileSlots = POLYLLA_TILE_SLOTS;
+static_assert(kTileSlots % 8 == 0 && kTileSlots >= 2 * kBuildTileTris, "slot count: uint4 clears, load < 1/2");
 #ifndef POLYLLA_TILE_THREADS
 #define POLYLLA_TILE_THREADS 768
 #endif
@@ -53,18 +62,25 @@ __device__ __forceinline__ int q_step(int q) {
 }
 // shared memory (bytes):
 //   tri_q int32[kTileQ]   32768  quad layout (v0, v1, v2, v0): half-edge q runs tri_q[q] -> tri_q[q+1]
-//   tw_s  int16[kTileQ]   16384  twin as a quad index, -1 = outside the tile
-//   slot  u16[kTileSlots] 32768  quad index of a lo->hi half-edge, 0xFFFF empty (dead after
-//                                P2: reused for succ u16[kTileQ])
+//   tw_s  int16[kTileQ]   16384  twin as a quad index, -1 = outside the tile (P2-P4b); then, written
+//                                over it quad by quad in P4b, nx_q: the local next (quad index),
+//                                -1 not walkable, kNxTip | twin for a barrier tip (P4b-P6)
 //   lc_s  u8[kTileTris]    2048
-//   nx_l  int16[kTileQ]  16384 | Sw, Cw, Wl, Lm, Dm, SDm, Fw, Tw u32[192] 6144   (P4-P6; quad-indexed local next;
-//                                Fw, Tw: the frontier / tip words of a grid tile, flushed at the end)
-constexpr size_t kOffTw = kTileQ * 4, kOffSlot = kOffTw + kTileQ * 2, kOffLc = kOffSlot + kTileSlots * 2,
-                 kOffNx = kOffLc + kTileTris,
-                 kNxBytes = kTileQ * 2 + 8 * (kTileHE / 8),                    // P4-P6 arrays (22,528 B)
-                 kTileSmemGrid = kOffNx + kNxBytes,                            // 106,496 B -> 2 CTAs/SM
-                 kTileSmem = kTileSmemGrid - 2 * (kTileHE / 8);               // 104,960 B: contiguous tiles need no Fw/Tw
+//   then one region that changes role after P2c:
+//     P0-P2c: slot u16[kTileSlots]       quad index of a lo->hi half-edge, 0xFFFF empty
+//     P3-P6 : succ u16[kTileQ] 16384 (pointer jumping in place) |
+//             Sw, Cw, Wl, Lm, Dm, SDm, Fw, Tw u32[192] 6144   (Fw, Tw: the frontier / tip
+//             words of a grid tile, flushed at the end)
+constexpr size_t kOffTw = kTileQ * 4, kOffLc = kOffTw + kTileQ * 2, kOffSlot = kOffLc + kTileTris,
+                 kOffWords = kOffSlot + kTileQ * 2,                            // (succ: the first 16 KB of the region)
+                 kWordBytes = 8 * (kTileHE / 8),                               // 6,144 B
+                 kRegion = kTileQ * 2 + kWordBytes > kTileSlots * 2 ? kTileQ * 2 + kWordBytes : kTileSlots * 2,
+                 kTileSmemGrid = kOffSlot + kRegion,                           // 99,200 B -> 2 CTAs/SM in 196 KB
+                 kTileSmem = kTileSmemGrid;
+constexpr int kNxTip = 0x4000;  // nx_q: barrier tip (quad indices are < 0x2000)
 static_assert(2 * (kTileSmemGrid + 1024) <= 228 * 1024, "two tiles per SM");
+static_assert(POLYLLA_TILE_SLOTS != 24000 || 2 * (kTileSmemGrid + 1024) <= 196 * 1024, "the 196 KB carveout");
+static_assert(kOffSlot % 16 == 0, "uint4 clears of the slot table");
 constexpr unsigned long long kLeftDown = 1ull << 63;    // leftover key: set if origin > target
 constexpr unsigned long long kLeftPaired = 1ull << 31;  // leftover key: set once the key's slot holder is paired
 constexpr uint32_t kEmpty16 = 0xFFFFu;             // empty 16-bit slot (quad indices are < 8192)
@@ -151,14 +167,16 @@ __device__ __forceinline__ double2 ld_xy(const double2* ptr, uint64_t pol) {
 __device__ __forceinline__ uint32_t tile_hash(uint32_t lo, uint32_t hi) {
   return ((lo * 0x9E3779B1u) ^ hi) * 0x85EBCA6Bu;
 }
-__device__ __forceinline__ uint32_t tile_pos(uint32_t lo, uint32_t hi) { return tile_hash(lo, hi) >> (32 - kSlotBits); }
+// home slot: the high bits of hash * kTileSlots (a power of two: the top bits of the hash)
+__device__ __forceinline__ uint32_t tile_pos(uint32_t lo, uint32_t hi) { return __umulhi(tile_hash(lo, hi), (uint32_t)kTileSlots); }
+__device__ __forceinline__ uint32_t slot_succ(uint32_t p) { return p + 1 == (uint32_t)kTileSlots ? 0u : p + 1; }
 
 // collision loser of the claim pass: CAS (on the 32-bit word holding the 16-bit slot) +
 // linear probing from its home slot
 __device__ __noinline__ uint32_t tile_insert_probe(uint16_t* slot, const int32_t* tri_q, int32_t q, uint32_t lo,
                                                    uint32_t hi) {
   uint32_t p = tile_pos(lo, hi);
-  for (int probe = 0; probe < kTileSlots; ++probe, p = (p + 1) & (kTileSlots - 1)) {
+  for (int probe = 0; probe < kTileSlots; ++probe, p = slot_succ(p)) {
     uint32_t* wp = reinterpret_cast<uint32_t*>(slot + (p & ~1u));
     const int sh = (int)(p & 1) * 16;
     uint32_t word = ld_relaxed(wp);
@@ -178,7 +196,7 @@ __device__ __noinline__ uint32_t tile_insert_probe(uint16_t* slot, const int32_t
 __device__ __noinline__ int32_t tile_lookup_probe(const uint16_t* slot, const int32_t* tri_q, uint32_t lo, uint32_t hi) {
   uint32_t p = tile_pos(lo, hi);
   for (int probe = 1; probe < kTileSlots; ++probe) {
-    p = (p + 1) & (kTileSlots - 1);
+    p = slot_succ(p);
     const uint32_t w = slot[p];
     if (w == kEmpty16) return -1;
     if ((uint32_t)tri_q[w] == lo && (uint32_t)tri_q[w + 1] == hi) return (int32_t)w;
@@ -237,9 +255,8 @@ __device__ __forceinline__ void tile_body(
   int16_t* tw_s = reinterpret_cast<int16_t*>(smem_tile + kOffTw);
   uint16_t* slot = reinterpret_cast<uint16_t*>(smem_tile + kOffSlot);
   uint8_t* lc_s = smem_tile + kOffLc;
-  int16_t* nx_l = reinterpret_cast<int16_t*>(smem_tile + kOffNx);               // local next (quad), -1: not walkable
   // six word arrays in a row (word wl of array r at Sw + r * kTileWords + wl)
-  uint32_t* Sw = reinterpret_cast<uint32_t*>(smem_tile + kOffNx + kTileQ * 2);   // seed bits (e order)
+  uint32_t* Sw = reinterpret_cast<uint32_t*>(smem_tile + kOffWords);   // seed bits (e order)
   uint32_t* Cw = Sw + kTileWords;                                                // canonical seed bits
   int32_t* Wl = reinterpret_cast<int32_t*>(Cw + kTileWords);                     // loop lengths per C word
   uint32_t* Lm = reinterpret_cast<uint32_t*>(Wl + kTileWords);                   // leftover bits
@@ -408,17 +425,15 @@ __device__ __forceinline__ void tile_body(
         cb[k] = look ? tri_q[w[k] + 1] : -1;
       }
 #pragma unroll
-      for (int k = 0; k < 3; ++k) {
+      for (int k = 0; k < 3; ++k) {  // (flag arithmetic and predicated stores: no divergent branch)
         const int32_t q = 4 * t + k;
-        if (vs[k] < vs[k + 1]) {
-          if (w[k] != (uint32_t)q) pend_ins |= 1u << (4 * i + k);
-        } else if (vs[k] > vs[k + 1] && w[k] != kEmpty16) {
-          if (ca[k] == vs[k + 1] && cb[k] == vs[k]) {
-            tw_s[q] = (int16_t)w[k];
-            tw_s[w[k]] = (int16_t)q;
-          } else {
-            pend_look |= 1u << (4 * i + k);
-          }
+        const bool look = vs[k] > vs[k + 1] && w[k] != kEmpty16;
+        const bool match = ca[k] == vs[k + 1] && cb[k] == vs[k];  // (ca = -1 unless look)
+        pend_ins |= (uint32_t)(vs[k] < vs[k + 1] && w[k] != (uint32_t)q) << (4 * i + k);
+        pend_look |= (uint32_t)(look && !match) << (4 * i + k);
+        if (match) {
+          tw_s[q] = (int16_t)w[k];
+          tw_s[w[k]] = (int16_t)q;
         }
       }
     }
@@ -525,25 +540,24 @@ __device__ __forceinline__ void tile_body(
   __syncthreads();
   PHASE_MARK(3);
 
-  // ---- P4a: pointer jumping, double-buffered between succ and the (still unused) P4-P6
-  // area: each round doubles the resolved chain length; an even number of rounds leaves
-  // the result in succ.  (Slot 3 of a quad holds 0xFFFF: terminal, never a target.)
-  static_assert(kTileJumps % 2 == 0 && kTileJumps <= 4, "result must end in succ");
-  uint16_t* succ_b = reinterpret_cast<uint16_t*>(smem_tile + kOffNx);  // 16 KB <= the P4-P6 area
+  // ---- P4a: pointer jumping in place: each round doubles the resolved chain length.  A
+  // successor read while its owner rewrites it is the old or the new value, both on the
+  // chain and at least as far along as the round before, so after r rounds every entry is
+  // >= 2^r steps ahead (or terminal); further along only moves work from the global fixup
+  // into the tile, which computes the same next.  (Slot 3 of a quad: 0xFFFF, terminal.)
+  static_assert(kTileJumps <= 4, "pointer-jumping rounds");
 #pragma unroll 1
   for (int round = 0; round < kTileJumps; ++round) {
-    const uint16_t* src = (round & 1) ? succ_b : succ;
-    uint16_t* dst = (round & 1) ? succ : succ_b;
 #pragma unroll
     for (int i = 0; i < kTriIters; ++i) {
       const int t = tid + i * kTileThreads;
       if (!tri_here<FULL, GRID>(i, t, nt, g_rows, g_cols)) continue;
-      const uint2 s2 = *reinterpret_cast<const uint2*>(src + 4 * t);
+      const uint2 s2 = *reinterpret_cast<const uint2*>(succ + 4 * t);  // (own quad: only this thread writes it)
       const uint32_t sc[3] = {s2.x & 0xFFFFu, s2.x >> 16, s2.y & 0xFFFFu};
       uint32_t d[3];
 #pragma unroll
-      for (int k = 0; k < 3; ++k) d[k] = (sc[k] & (kSuccFront | kSuccUnknown)) ? sc[k] : src[sc[k]];
-      *reinterpret_cast<uint2*>(dst + 4 * t) = make_uint2(d[0] | (d[1] << 16), d[2] | 0xFFFF0000u);
+      for (int k = 0; k < 3; ++k) d[k] = (sc[k] & (kSuccFront | kSuccUnknown)) ? sc[k] : ld_relaxed16(succ + sc[k]);
+      *reinterpret_cast<uint2*>(succ + 4 * t) = make_uint2(d[0] | (d[1] << 16), d[2] | 0xFFFF0000u);
     }
     __syncthreads();
   }
@@ -552,7 +566,7 @@ __device__ __forceinline__ void tile_body(
   // ---- P4b: per triangle: next (Alg. 11) of its three half-edges, F words (Alg. 8), tips
   // (next == twin, R4), deferred half-edges; the local next in quad indices (nx_q; the
   // global origin/twin/next are written from the quad arrays in half-edge order in P5)
-  int16_t* nx_q = nx_l;  // quad-indexed local next: -1 not walkable, -2 barrier tip
+  int16_t* nx_q = tw_s;  // quad-indexed local next over the twins (each thread reads its quad's twins first)
 #pragma unroll
   for (int i = 0; i < kTriIters; ++i) {
     if (!(i < kTriIters - 1 || tid < kTileTris - (kTriIters - 1) * kTileThreads)) continue;
@@ -582,7 +596,7 @@ __device__ __forceinline__ void tile_body(
             fr = false;  // the fixup sets every bit of a deferred half-edge
           }
         }
-        nl[k] = deferred ? -1 : tip ? -2 : nx;  // -2: a barrier tip (the loop will be split by the repair)
+        nl[k] = deferred ? -1 : tip ? (kNxTip | tq[k]) : nx;  // a barrier tip (its loop is split by the repair)
         packed |= ((uint32_t)fr << k) | ((uint32_t)tip << (4 + k)) | ((uint32_t)deferred << (8 + k));
       }
       *reinterpret_cast<uint2*>(nx_q + 4 * t) =
@@ -658,18 +672,18 @@ __device__ __forceinline__ void tile_body(
         if (j >= kTileHE) break;
         if (!here(q >> 2)) continue;
         const int32_t nl = nx_q[q];
-        if (nl != -1) __stcs(next + ghe(q), (hid)ghe(nl == -2 ? tw_s[q] : nl));
+        if (nl != -1) __stcs(next + ghe(q), (hid)ghe(nl & ~kNxTip));
         continue;
       }
       if ((!FULL || kHePartial) && j >= nhe) break;
       const int32_t nl = nx_q[q];
-      if (nl != -1) __stcs(next + e0 + j, (hid)(e0 + j_of(nl == -2 ? tw_s[q] : nl)));
+      if (nl != -1) __stcs(next + e0 + j, (hid)(e0 + j_of(nl & ~kNxTip)));
     }
   }
 
   // ---- P6: seeds whose polygon closes inside the tile (Alg. 12 + Overwrite seeds,
   // PAPER.md L778-849): land on a frontier half-edge by rotation (the resolved successor
-  // chain), walk the loop on nx_l, keep the minimum id and the length.  Loops that touch
+  // chain), walk the loop on nx_q, keep the minimum id and the length.  Loops that touch
   // a deferred half-edge or a barrier tip (repaired later) are handed to the global
   // seed walk (bit-vector SDB).  kSeedLanes threads per word take its seeds in turn.
   {
@@ -696,7 +710,11 @@ __device__ __forceinline__ void tile_body(
           if (SORTED) gmin = min(gmin, ghe(y));
           ++n;
           y = nx_q[y];
-          if (y < 0 || n > kP6MaxLen) { ok = false; tipped = y == -2; break; }  // deferred / barrier-tip / long loop
+          if ((uint32_t)y >= (uint32_t)kNxTip || n > kP6MaxLen) {  // deferred (-1) / barrier tip / long loop
+            ok = false;
+            tipped = y >= 0 && (y & kNxTip);
+            break;
+          }
         } while (y != x);
       }
       if (ok && SORTED) {  // canonical seed = the minimum global id: its bit set in the global C directly

@@ -220,7 +220,10 @@ __device__ __forceinline__ int64_t sched_tile(int64_t i, int64_t ntiles) {
 // entries); each full (or final) queue is handed to f(e, valid) in warp-uniform rounds of
 // 32 (all lanes present, so f may use warp collectives; valid is false on the padding
 // lanes of the last round; e is then kNoHe).  Returns the number of set bits this warp saw.
-constexpr int kBitQueue = 128;  // small: the walks that follow live on L1 hits (shared memory shrinks L1)
+#ifndef POLYLLA_BIT_QUEUE
+#define POLYLLA_BIT_QUEUE 128
+#endif
+constexpr int kBitQueue = POLYLLA_BIT_QUEUE;  // small: the walks that follow live on L1 hits (shared memory shrinks L1)
 #ifndef POLYLLA_BIT_CHUNK
 #define POLYLLA_BIT_CHUNK 32
 #endif

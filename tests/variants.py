@@ -7,7 +7,8 @@ paper_2403_14723_b200/variants/libpolylla_<name>.so (rebuilt when a source is ne
 
   rev       tiles run in reverse block order (k_tile, leftover match, border ranking,
             label fixup, emission); 4 pointer-jumping rounds in k_tile
-  threads   other block sizes for every global kernel, 4-word bit chunks
+  threads   other block sizes for every global kernel, 4-word bit chunks; a k_tile hash
+            of 4,104 slots (load 0.75: long probe runs, wrap-around at the table's end)
   tile384   k_tile with 384 threads (6 triangle iterations per thread), no pointer
             jumping (rotation chains resolved by hops only)
   fallback  a 64-entry k_emit queue (every tile takes the dense-tile branch) and an
@@ -27,7 +28,7 @@ VARIANTS = {
     "rev": ["-DPOLYLLA_REVERSE_TILES", "-DPOLYLLA_TILE_JUMPS=4"],
     "threads": ["-DPOLYLLA_FIX_THREADS=128", "-DPOLYLLA_SEED_THREADS=128", "-DPOLYLLA_EMIT_THREADS=256",
                 "-DPOLYLLA_REPAIR_THREADS=256", "-DPOLYLLA_LEFT_THREADS=128", "-DPOLYLLA_BIT_CHUNK=4",
-                "-DPOLYLLA_UF_THREADS=256"],
+                "-DPOLYLLA_UF_THREADS=256", "-DPOLYLLA_TILE_SLOTS=4104"],
     "tile384": ["-DPOLYLLA_TILE_THREADS=384", "-DPOLYLLA_TILE_JUMPS=0"],
     "fallback": ["-DPOLYLLA_EMIT_Q=64", "-DPOLYLLA_P6_MAXLEN=3"],
 }
