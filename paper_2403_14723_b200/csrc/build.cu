@@ -914,6 +914,7 @@ __global__ void k_left_insert(DevCounters* ctr, int64_t ntiles, int64_t T, const
           const hid es = left_e[s];
           twin[ei] = es;
           twin[es] = ei;
+          left_key[i] = kd | kLeftPaired;  // (own entry, never in the hash): both halves flagged for the ranking
           break;
         }
         h = (h + 1) & mask;
@@ -926,8 +927,11 @@ __global__ void k_left_insert(DevCounters* ctr, int64_t ntiles, int64_t T, const
 // b = 3T + rank(e) over the unmatched interior half-edges in ascending order.  Each tile
 // segment is in ascending e order, so the rank is (border half-edges of the earlier
 // tiles) + (rank inside the segment):
-//   k_border_rank  one block per tile segment: the unmatched leftovers in segment order
-//                  -> blist (the dead leftover-key storage), their count -> bcnt[tile]
+//   k_border_rank  one block per tile segment: the unmatched leftovers (no kLeftPaired
+//                  flag: the segment's keys are read coalesced instead of a random twin
+//                  per leftover) in segment order -> blist, written over the segment's own
+//                  dead keys (4-byte entry 2 * base + rank <= the chunk being read), their
+//                  count -> bcnt[tile]
 //   k_border_scan  one block: exclusive prefix of bcnt over the tiles, B = the total
 //   k_border_emit  one block per tile segment: b = 3T + base + rank; twin/origin of b and
 //                  vmap[origin(b)] = b (written only at border vertices: never cleared;
@@ -936,7 +940,7 @@ constexpr int kSegThreads = 256;
 
 __global__ void __launch_bounds__(kSegThreads)
     k_border_rank(DevCounters* ctr, int64_t ntiles, const int32_t* __restrict__ cnt_ld,
-                  const hid* __restrict__ left_e, const hid* __restrict__ twin, hid* __restrict__ blist,
+                  const hid* __restrict__ left_e, const unsigned long long* left_key, hid* blist,
                   uint32_t* __restrict__ bcnt) {
   __shared__ int32_t wtot[kSegThreads / 32];
   if (ctr->status) return;
@@ -948,8 +952,8 @@ __global__ void __launch_bounds__(kSegThreads)
     int carry = 0;
     for (int32_t k0 = 0; k0 < n; k0 += kSegThreads) {  // block-uniform trip count
       const int32_t k = k0 + threadIdx.x;
-      const hid e = k < n ? left_e[base + k] : kNoHe;
-      const bool un = e != kNoHe && twin[e] == kNoHe;
+      const bool un = k < n && !(left_key[base + k] & kLeftPaired);
+      const hid e = un ? left_e[base + k] : kNoHe;
       const uint32_t m = __ballot_sync(0xffffffffu, un);
       if (lane == 0) wtot[wid] = __popc(m);
       __syncthreads();
@@ -958,7 +962,7 @@ __global__ void __launch_bounds__(kSegThreads)
         if (w < wid) pre += wtot[w];
         tot += wtot[w];
       }
-      if (un) blist[base + pre + __popc(m & ((1u << lane) - 1))] = e;  // segment-local rank order
+      if (un) blist[2 * base + pre + __popc(m & ((1u << lane) - 1))] = e;  // segment-local rank order
       carry += tot;
       __syncthreads();
     }
@@ -1023,7 +1027,7 @@ __global__ void __launch_bounds__(kSegThreads)
     const int32_t n = (int32_t)((tile + 1 < ntiles ? bbase[tile + 1] : nb) - b0);
     const int64_t base = 3 * kTileTris * tile;
     for (int32_t k = threadIdx.x; k < n; k += kSegThreads) {
-      const hid e = blist[base + k];
+      const hid e = blist[2 * base + k];
       const hid b = (hid)(T3 + b0 + k);
       const int32_t v = origin[next_in(e)];  // origin(b) = target(e)
       twin[e] = b;
@@ -1040,14 +1044,15 @@ __global__ void __launch_bounds__(kSegThreads)
 // chunks' exclusive prefix (k_border_scan), then each chunk's bits in order (k_bb_emit).
 __global__ void k_bb_mark(DevCounters* ctr, int64_t ntiles, int64_t T, const Tiling tl,
                           const int32_t* __restrict__ cnt_ld, const hid* __restrict__ left_e,
-                          const hid* __restrict__ twin, uint32_t* BB) {
+                          const unsigned long long* __restrict__ left_key, uint32_t* BB) {
   if (ctr->status) return;
   for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
     const int32_t n = cnt_ld[2 * tile];
     const int64_t base = tile_geom(tl, T, tile).seg;
     for (int32_t k = threadIdx.x; k < n; k += blockDim.x) {
+      if (left_key[base + k] & kLeftPaired) continue;  // (paired: flagged by k_left_insert)
       const hid e = left_e[base + k];
-      if (twin[e] == kNoHe) atomicOr(&BB[e >> 5], 1u << (e & 31));
+      atomicOr(&BB[e >> 5], 1u << (e & 31));
     }
   }
 }
@@ -1364,7 +1369,7 @@ int launch_build_rest(Ctx* c, cudaStream_t s) {
                                                            c->left_e, c->twin, ehash);
   if (c->tiling.mode != kTileContig) {  // grid / sorted tiles: the border ranking by bit order
     const int64_t nchunks = (c->n_words + kBBChunk - 1) / kBBChunk;
-    k_bb_mark<<<seg_grid, kSegThreads, 0, s>>>(c->ctr, tiles, c->T, c->tiling, c->cnt_ld, c->left_e, c->twin, c->BB);
+    k_bb_mark<<<seg_grid, kSegThreads, 0, s>>>(c->ctr, tiles, c->T, c->tiling, c->cnt_ld, c->left_e, c->left_key, c->BB);
     k_bb_count<<<(unsigned)((nchunks + 7) / 8), 256, 0, s>>>(c->ctr, c->n_words, nchunks, c->BB, c->bcnt);
     n += 3;
     prof_mark(s, "k_border_scan");
@@ -1374,7 +1379,7 @@ int launch_build_rest(Ctx* c, cudaStream_t s) {
     n += 2;
   } else {
     hid* blist = reinterpret_cast<hid*>(c->left_key);  // dead after k_left_insert
-    k_border_rank<<<seg_grid, kSegThreads, 0, s>>>(c->ctr, tiles, c->cnt_ld, c->left_e, c->twin, blist, c->bcnt);
+    k_border_rank<<<seg_grid, kSegThreads, 0, s>>>(c->ctr, tiles, c->cnt_ld, c->left_e, c->left_key, blist, c->bcnt);
     n += 3;
     prof_mark(s, "k_border_scan");
     k_border_scan<<<1, kBorderScanThreads, 0, s>>>(c->ctr, tiles, 3 * c->T, c->Bmax, c->bcnt);

@@ -221,7 +221,7 @@ __device__ __forceinline__ int64_t sched_tile(int64_t i, int64_t ntiles) {
 // 32 (all lanes present, so f may use warp collectives; valid is false on the padding
 // lanes of the last round; e is then kNoHe).  Returns the number of set bits this warp saw.
 #ifndef POLYLLA_BIT_QUEUE
-#define POLYLLA_BIT_QUEUE 128
+#define POLYLLA_BIT_QUEUE 256  // (64 / 128 / 256 / 512 measured: 256 best for k_seed_walk on config 3)
 #endif
 constexpr int kBitQueue = POLYLLA_BIT_QUEUE;  // small: the walks that follow live on L1 hits (shared memory shrinks L1)
 #ifndef POLYLLA_BIT_CHUNK
