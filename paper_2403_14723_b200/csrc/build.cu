@@ -247,7 +247,7 @@ __device__ __forceinline__ void tile_body(
     unsigned char* smem_tile, const Tiling tl, const double2* __restrict__ xy, const int32_t* __restrict__ tri, int64_t V, int64_t T,
     int32_t* __restrict__ origin, hid* __restrict__ twin, hid* __restrict__ next, uint8_t* __restrict__ lcode,
     uint32_t* __restrict__ F0, int64_t bv_stride, uint32_t* __restrict__ C,
-    int32_t* __restrict__ len, int32_t* __restrict__ wlen, unsigned long long* __restrict__ left_key,
+    uint8_t* __restrict__ len, int32_t* __restrict__ wlen, unsigned long long* __restrict__ left_key,
     hid* __restrict__ left_e, hid* __restrict__ def_e, uint32_t* __restrict__ SDB,
     int32_t* __restrict__ cnt_ld, DevCounters* ctr, int64_t tile, int64_t tile_next) {
   int32_t* tri_q = reinterpret_cast<int32_t*>(smem_tile);
@@ -718,13 +718,13 @@ __device__ __forceinline__ void tile_body(
         } while (y != x);
       }
       if (ok && SORTED) {  // canonical seed = the minimum global id: its bit set in the global C directly
-        len[gmin] = n;
+        len[gmin] = len_code(n);
         const uint32_t gbit = 1u << (gmin & 31);
         if (!(atomicOr(&C[gmin >> 5], gbit) & gbit)) atomicAdd(&wlen[gmin >> 5], n);  // first setter only
       } else if (ok) {
         const int64_t gmn = ghe(mn);  // (the loop minimum: quad and half-edge orders agree)
         mn = j_of(mn);
-        len[gmn] = n;
+        len[gmn] = len_code(n);
         const uint32_t bit = 1u << (mn & 31);
         if (!(atomicOr(&Cw[mn >> 5], bit) & bit)) {  // first setter only
           if (SCAT) atomicAdd(&wlen[gmn >> 5], n);   // (grid / sorted: global words, zeroed before the build)
@@ -802,7 +802,7 @@ template <int MODE>
 __global__ void __launch_bounds__(kTileThreads, 2)
     k_tile(const double2* __restrict__ xy, const int32_t* __restrict__ tri, int64_t V, int64_t T,
            int32_t* __restrict__ origin, hid* __restrict__ twin, hid* __restrict__ next,
-           uint8_t* __restrict__ lcode, uint32_t* __restrict__ F0, int64_t bv_stride, uint32_t* __restrict__ C, int32_t* __restrict__ len, int32_t* __restrict__ wlen,
+           uint8_t* __restrict__ lcode, uint32_t* __restrict__ F0, int64_t bv_stride, uint32_t* __restrict__ C, uint8_t* __restrict__ len, int32_t* __restrict__ wlen,
            unsigned long long* __restrict__ left_key, hid* __restrict__ left_e, hid* __restrict__ def_e,
            uint32_t* __restrict__ SDB, int32_t* __restrict__ cnt_ld, DevCounters* ctr,
            int64_t prefetch_dist, int64_t tile_base, const Tiling tl) {

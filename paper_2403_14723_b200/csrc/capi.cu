@@ -46,7 +46,7 @@ static Layout layout(int64_t V, int64_t T, int64_t Bmax, bool staging, int64_t R
       (size_t)nw * 4,         // 6 S
       (size_t)nw * 4,         // 7 TB: barrier tips (F0, F1, S, TB equally spaced: k_tile stores them by offset)
       (size_t)((bt > ct ? bt : ct) + 1) * 4,  // 8 per-tile (or per-chunk) border counts / bases
-      (size_t)(3 * T) * 4,    // 9 len
+      (size_t)(3 * T),        // 9 len (bytes)
       (size_t)(3 * T) * 8,    // 10 left_key
       (size_t)(3 * T) * 4,    // 11 left_e
       (size_t)cap * 4,        // 12 ehash
@@ -107,7 +107,7 @@ bool carve(Ctx* c, void* ws, size_t bytes) {
   c->S = reinterpret_cast<uint32_t*>(b + L.off[6]);
   c->TB = reinterpret_cast<uint32_t*>(b + L.off[7]);
   c->bcnt = reinterpret_cast<uint32_t*>(b + L.off[8]);
-  c->len = reinterpret_cast<int32_t*>(b + L.off[9]);
+  c->len = reinterpret_cast<uint8_t*>(b + L.off[9]);
   c->left_key = reinterpret_cast<unsigned long long*>(b + L.off[10]);
   c->left_e = reinterpret_cast<hid*>(b + L.off[11]);
   c->ehash = b + L.off[12];

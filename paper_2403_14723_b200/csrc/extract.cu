@@ -26,8 +26,19 @@ constexpr int kEmitThreads = POLYLLA_EMIT_THREADS;
 #endif
 constexpr int kEmitQ = POLYLLA_EMIT_Q;  // queue capacity (polygons per tile; a tile with more walks per word)
 
+// loop length of canonical seed e: len[e], or counted along next when it is the escape
+// (a loop of >= kLenEsc entries)
+__device__ __forceinline__ uint32_t loop_len(const uint8_t* __restrict__ len, const hid* __restrict__ next, hid e) {
+  uint32_t n = len[e];
+  if (n == kLenEsc) {
+    n = 1;
+    for (hid x = next[e]; x != e; x = next[x]) ++n;  // (the loop closed when its seed was set)
+  }
+  return n;
+}
+
 __global__ void __launch_bounds__(kEmitThreads)
-    k_emit(int64_t T, int64_t n_words, const uint32_t* __restrict__ C, const int32_t* __restrict__ len,
+    k_emit(int64_t T, int64_t n_words, const uint32_t* __restrict__ C, const uint8_t* __restrict__ len,
            const uint32_t* __restrict__ tb, const int32_t* __restrict__ origin, const hid* __restrict__ next,
            hid* __restrict__ seeds, uint32_t* __restrict__ offsets, int64_t offsets_cap, int32_t* __restrict__ loops,
            int64_t loops_cap, DevCounters* ctr) {
@@ -77,11 +88,11 @@ __global__ void __launch_bounds__(kEmitThreads)
       // offset of the word's first polygon: tile base + lengths of the earlier polygons
       uint32_t o = obase;
       for (int64_t ww = wt; ww < wt + wl; ++ww)
-        for (uint32_t b = C[ww]; b; b &= b - 1) o += len[ww * 32 + __ffs(b) - 1];
+        for (uint32_t b = C[ww]; b; b &= b - 1) o += loop_len(len, next, (hid)(ww * 32 + __ffs(b) - 1));
       uint32_t r = rbase + wbase[wl];
       for (uint32_t b = C[wt + wl]; b; b &= b - 1, ++r) {
         const hid e = (hid)((wt + wl) * 32 + __ffs(b) - 1);
-        const int32_t n = len[e];
+        const int32_t n = (int32_t)loop_len(len, next, e);
         seeds[r] = e;
         offsets[r] = o;
         hid x = e;
@@ -98,7 +109,7 @@ __global__ void __launch_bounds__(kEmitThreads)
       for (uint32_t b = C[wt + wl]; b; b &= b - 1, ++p) qe[p] = (hid)((wt + wl) * 32 + __ffs(b) - 1);
     }
     __syncthreads();
-    for (int i = tid; i < np; i += kEmitThreads) qo[i] = (uint32_t)len[qe[i]];
+    for (int i = tid; i < np; i += kEmitThreads) qo[i] = loop_len(len, next, qe[i]);
     __syncthreads();
     // exclusive scan of the lengths: thread t owns queue entries [t*per, (t+1)*per)
     const int per = (np + kEmitThreads - 1) / kEmitThreads;

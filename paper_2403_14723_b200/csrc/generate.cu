@@ -148,7 +148,7 @@ constexpr int kSeedThreads = POLYLLA_SEED_THREADS;
 
 __device__ __forceinline__ void process_seed(hid s, int64_t T3, int64_t H, const hid* __restrict__ twin,
                                              const hid* __restrict__ next, const uint32_t* __restrict__ F1,
-                                             uint32_t* C, int32_t* len, int32_t* wlen, DevCounters* ctr) {
+                                             uint32_t* C, uint8_t* len, int32_t* wlen, DevCounters* ctr) {
   hid x = s;
   int64_t steps = 0;
   while (!f1_of(F1, T3, x)) {  // Alg. 12: rotate (sweep_out) to a frontier half-edge (<= deg <= 3T steps)
@@ -162,7 +162,7 @@ __device__ __forceinline__ void process_seed(hid s, int64_t T3, int64_t H, const
     y = next[y];
     if (++n > H) { raise_status(ctr, ST_WALK); return; }
   } while (y != x);
-  len[mn] = (int32_t)n;
+  len[mn] = len_code(n);
   const uint32_t bit = 1u << (mn & 31);
   if (!(atomicOr(&C[mn >> 5], bit) & bit)) atomicAdd(&wlen[mn >> 5], (int32_t)n);  // first setter only
 }
@@ -172,7 +172,7 @@ __device__ __forceinline__ void process_seed(hid s, int64_t T3, int64_t H, const
 // over warps (warp_foreach_bit), one seed per lane.
 __global__ void __launch_bounds__(kSeedThreads)
     k_seed_walk(int64_t T, int64_t n_words, const uint32_t* __restrict__ SDB, const hid* __restrict__ twin,
-                const hid* __restrict__ next, const uint32_t* __restrict__ F1, uint32_t* C, int32_t* len,
+                const hid* __restrict__ next, const uint32_t* __restrict__ F1, uint32_t* C, uint8_t* len,
                 int32_t* wlen, DevCounters* ctr) {
   __shared__ hid queue[kSeedThreads / 32][kBitQueue];
   if (ctr->status) return;

@@ -120,7 +120,8 @@ struct Ctx {
   hid *twin, *next;
   uint8_t* lcode;
   uint32_t *F0, *F1, *S, *C;
-  int32_t* len;     // [3T] loop length, at canonical seeds
+  uint8_t* len;     // [3T] loop length at canonical seeds, min(n, kLenEsc) (bytes: its sparse reads and
+                    // writes touch a quarter of the sectors of an int32 array)
   int32_t* wlen;    // [n_words] sum of loop lengths of the canonical seeds of each C word
   unsigned long long* left_key;
   hid* left_e;
@@ -202,6 +203,8 @@ __device__ __forceinline__ uint32_t mix32(uint32_t a, uint32_t b) {
 }
 
 constexpr uint32_t kEmpty = 0xFFFFFFFFu;   // empty hash slot
+constexpr uint32_t kLenEsc = 255;          // len[]: a loop of >= 255 entries (its length is counted by walking it)
+__device__ __forceinline__ uint8_t len_code(int64_t n) { return (uint8_t)(n < (int64_t)kLenEsc ? n : kLenEsc); }
 constexpr int kBuildTileTris = 2048;     // triangles per k_tile tile (list segments are 3 * 2048 wide)
 
 // Block -> tile schedule of the per-tile kernels.  POLYLLA_REVERSE_TILES (a test variant,

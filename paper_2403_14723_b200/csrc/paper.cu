@@ -185,7 +185,7 @@ __global__ void k_p_sfk(int64_t T, const int32_t* __restrict__ twin, const uint3
 
 // Overwrite seeds (OSK): one thread per seed: walk the polygon, its minimum id becomes
 // its seed; the loop length goes with it for the compaction
-__global__ void k_p_osk(int64_t T, const int32_t* __restrict__ next, uint32_t* S, uint32_t* C, int32_t* len,
+__global__ void k_p_osk(int64_t T, const int32_t* __restrict__ next, uint32_t* S, uint32_t* C, uint8_t* len,
                         int32_t* wlen, int64_t n_words, DevCounters* ctr) {
   if (ctr->status) return;
   const int64_t H = 3 * T + ctr->n_border;
@@ -201,7 +201,7 @@ __global__ void k_p_osk(int64_t T, const int32_t* __restrict__ next, uint32_t* S
       }
       if (mn != init) atomicAnd(&S[init >> 5], ~(1u << (init & 31)));
       atomicOr(&S[mn >> 5], 1u << (mn & 31));
-      len[mn] = (int32_t)n;
+      len[mn] = len_code(n);
       const uint32_t bit = 1u << (mn & 31);
       if (!(atomicOr(&C[mn >> 5], bit) & bit)) atomicAdd(&wlen[mn >> 5], (int32_t)n);
     }

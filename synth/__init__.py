@@ -117,6 +117,23 @@ def fixture_fan():
     return np.array(xy, dtype=np.float64), np.array(tri, dtype=np.int32)
 
 
+def fixture_long_fan(n: int, span_deg: float = 300.0):
+    """F6: an open fan of n triangles around a hub with slowly growing radii, which is ONE
+    polygon of n + 2 vertices: hub h = (0, 0), rim p_i = r_i (cos t_i, sin t_i) with
+    r_i = 1 + 1e-4 i and t_i = span * i / n (i = 0..n); triangles (h, p_i, p_{i+1}).  The
+    rim chords are short, so the longest edge of triangle i is its spoke h-p_{i+1}, which
+    is not the longest edge of triangle i + 1: every interior spoke is non-frontier, the
+    Lepp chain runs 0 -> n - 1 and ends at the border spoke h-p_n.  Loops of >= 255
+    entries (the emission's escaped length) and > 1024 (the in-tile walk bound)."""
+    i = np.arange(n + 1, dtype=np.float64)
+    r = 1.0 + 1e-4 * i
+    t = np.radians(span_deg) * i / n
+    xy = np.concatenate([[[0.0, 0.0]], np.stack([r * np.cos(t), r * np.sin(t)], axis=1)]).astype(np.float64)
+    k = np.arange(n, dtype=np.int32)
+    tri = np.stack([np.zeros(n, dtype=np.int32), k + 1, k + 2], axis=1).astype(np.int32)
+    return np.ascontiguousarray(xy), np.ascontiguousarray(tri)
+
+
 def fixture_tie_lattice(m: int = 9):
     """F5: lattice with every triangle's longest side tied (sqrt10, sqrt10, 2).
 

@@ -80,6 +80,20 @@ def test_tie_lattice():
     assert res["P"] == 8
 
 
+@pytest.mark.parametrize("n", [252, 253, 300, 1100, 2040])
+def test_long_fan_one_polygon(n):
+    """One polygon of n + 2 vertices (synth.fixture_long_fan): loop lengths around the
+    byte code's escape (>= 255: counted by walking at emission) and past the in-tile walk
+    bound (> 1024: the global seed walk), alone and next to a random mesh in other tiles."""
+    xy, tri = synth.fixture_long_fan(n)
+    res, _ = assert_parity(xy, tri)
+    assert res["P"] == 1 and int(res["offsets"][1]) == n + 2
+    xr, tr = synth.random_delaunay(20000, 11)
+    xy2 = np.concatenate([xr, xy + np.array([3.0, 0.5])])
+    tri2 = np.concatenate([tr, tri + xr.shape[0]]).astype(np.int32)
+    assert_parity(xy2, tri2, stages=False)
+
+
 @pytest.mark.parametrize("s", [2, 3, 10, 33, 64, 200])
 def test_regular_grid(s):
     res, _ = assert_parity(*synth.grid(s))

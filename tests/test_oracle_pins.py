@@ -116,6 +116,22 @@ def test_fan_barrier_tip_repair():
     check_output(xy, tri, o, o["frontier1"])
 
 
+# ----------------------------------------------------------------- F6: long open fan
+@pytest.mark.parametrize("n", [12, 40, 300])
+def test_long_fan_closed_form(n):
+    """synth.fixture_long_fan: the longest edge of triangle i is its spoke h-p_{i+1} (the
+    rim chords are shorter, r grows with i), so Lcode = 2 for every triangle (half-edge
+    3i + 2 runs p_{i+1} -> h), every interior spoke is non-frontier and the whole fan is
+    one terminal region whose terminal edge is the border spoke h-p_n (Def. 2): one polygon,
+    the loop h, p_0, ..., p_n (vertex ids 0..n+1), no barrier tip."""
+    xy, tri = synth.fixture_long_fan(n)
+    o = oracle.run(xy, tri)
+    assert o["lcode"].tolist() == [2] * n
+    assert o["P"] == 1 and o["n_tips"] == 0 and o["B"] == n + 2
+    assert o["loops"].tolist() == list(range(n + 2))
+    check_output(xy, tri, o, o["frontier1"])
+
+
 # ----------------------------------------------------------------- F5: tie lattice
 def test_tie_lattice_matches_bruteforce_lepp():
     """Every triangle has two tied longest sides; the tie-break (first max, R7)
