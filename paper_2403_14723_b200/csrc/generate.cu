@@ -31,7 +31,13 @@ __device__ __forceinline__ bool f1_of(const uint32_t* __restrict__ F1, int64_t T
 #define POLYLLA_REPAIR_THREADS 128
 #endif
 constexpr int kRepairThreads = POLYLLA_REPAIR_THREADS;
-constexpr int kRotMax = 32;  // rotations up to this degree are walked once and kept (local array)
+#ifndef POLYLLA_ROT_MAX
+#define POLYLLA_ROT_MAX 16
+#endif
+// rotations up to this degree are walked once and kept in shared memory (the rewire; a
+// per-thread local array of 32 had 128-B stack frames spilling to L2: 2048 threads x 128 B
+// per SM)
+constexpr int kRotMax = POLYLLA_ROT_MAX;
 __global__ void __launch_bounds__(kRepairThreads)
     k_repair_mid(int64_t T, int64_t n_words, const uint32_t* __restrict__ TB, const hid* __restrict__ twin,
                  uint32_t* F1, uint32_t* SDB, hid* __restrict__ tips, hid* __restrict__ aff, DevCounters* ctr) {
@@ -49,9 +55,7 @@ __global__ void __launch_bounds__(kRepairThreads)
     hid x = e0;
     int64_t d = 0;
     bool ok = true;
-    hid rot[kRotMax];  // the rotation, recorded for the middle-edge step below (deg <= kRotMax)
     do {  // degree(v): rotation closure about v (an interior vertex); deg(v) <= 3T
-      if (d < kRotMax) rot[d] = x;
       const hid tx = twin[x];
       if (tx >= T3 || ++d > T3) { ok = false; break; }
       x = next_in(tx);
@@ -62,10 +66,8 @@ __global__ void __launch_bounds__(kRepairThreads)
       aff[2 * i] = aff[2 * i + 1] = e0;
       return;
     }
-    hid m = e0;
-    if (d <= kRotMax) m = rot[(d - 1) / 2];  // floor((d-1)/2) CWvertexEdge steps (R1, R5)
-    else
-      for (int64_t k = 0; k < (d - 1) / 2; ++k) m = next_in(twin[m]);
+    hid m = e0;  // floor((d-1)/2) CWvertexEdge steps (R1, R5), again along the walked rotation (L1 hits)
+    for (int64_t k = 0; k < (d - 1) / 2; ++k) m = next_in(twin[m]);
     const hid tm = twin[m];
     atomicOr(&F1[m >> 5], 1u << (m & 31));
     atomicOr(&F1[tm >> 5], 1u << (tm & 31));
@@ -76,8 +78,10 @@ __global__ void __launch_bounds__(kRepairThreads)
   });
 }
 
-__global__ void k_repair_rewire(int64_t T, const hid* __restrict__ twin, const uint32_t* __restrict__ F1,
-                                const hid* __restrict__ aff, hid* next, DevCounters* ctr) {
+__global__ void __launch_bounds__(kRepairThreads)
+    k_repair_rewire(int64_t T, const hid* __restrict__ twin, const uint32_t* __restrict__ F1,
+                    const hid* __restrict__ aff, hid* next, DevCounters* ctr) {
+  __shared__ hid rot_s[kRotMax][kRepairThreads];  // (entry k of this thread's rotation: rot_s[k][tid])
   if (ctr->status) return;
   const int64_t T3 = 3 * T;
   const int64_t H = T3 + ctr->n_border;  // walk bound (a rotation about w has <= deg(w) <= H steps)
@@ -87,14 +91,14 @@ __global__ void k_repair_rewire(int64_t T, const hid* __restrict__ twin, const u
     // one walk around w collects its outgoing half-edges in sweep order (R1; the border
     // chain at the hull); the next F1 half-edge after each incoming p = prev_in(y_i) is
     // then the first frontier y_m, m >= i cyclically -- what a rotation from y_i finds
-    hid rot[kRotMax];
+    hid* const rot = &rot_s[0][threadIdx.x];  // rot[i * kRepairThreads]
     int d = 0;
     bool fits = true, ok = true;
     {
       hid y = o;
       int64_t guard = 0;
       do {
-        if (d < kRotMax) rot[d] = y; else fits = false;
+        if (d < kRotMax) rot[d * kRepairThreads] = y; else fits = false;
         ++d;
         const hid ty = twin[y];
         y = ty >= T3 ? next[ty] : next_in(ty);
@@ -105,15 +109,16 @@ __global__ void k_repair_rewire(int64_t T, const hid* __restrict__ twin, const u
     if (fits) {
       uint32_t fo = 0, fi = 0;  // bit i: y_i frontier (F1 or border) / p_i = prev_in(y_i) an interior F1 half-edge
       for (int i = 0; i < d; ++i) {
-        fo |= (uint32_t)f1_of(F1, T3, rot[i]) << i;
-        if (rot[i] < T3) fi |= (uint32_t)f1_of(F1, T3, prev_in(rot[i])) << i;
+        const hid y = rot[i * kRepairThreads];
+        fo |= (uint32_t)f1_of(F1, T3, y) << i;
+        if (y < T3) fi |= (uint32_t)f1_of(F1, T3, prev_in(y)) << i;
       }
       if (fi && !fo) { raise_status(ctr, ST_WALK); return; }  // (a rotation without a frontier half-edge)
       for (uint32_t b = fi; b; b &= b - 1) {
         const int i = __ffs(b) - 1;
         const uint32_t ahead = fo >> i;  // (i < 32)
         const int m = ahead ? i + __ffs(ahead) - 1 : __ffs(fo) - 1;
-        next[prev_in(rot[i])] = rot[m];
+        next[prev_in(rot[i * kRepairThreads])] = rot[m * kRepairThreads];
       }
       continue;
     }

@@ -119,7 +119,7 @@ def fixture_fan():
 
 def fixture_long_fan(n: int, span_deg: float = 300.0):
     """F6: an open fan of n triangles around a hub with slowly growing radii, which is ONE
-    polygon of n + 2 vertices: hub h = (0, 0), rim p_i = r_i (cos t_i, sin t_i) with
+    polygon of n + 2 vertices (n >= 8: rim chords shorter than spokes): hub h = (0, 0), rim p_i = r_i (cos t_i, sin t_i) with
     r_i = 1 + 1e-4 i and t_i = span * i / n (i = 0..n); triangles (h, p_i, p_{i+1}).  The
     rim chords are short, so the longest edge of triangle i is its spoke h-p_{i+1}, which
     is not the longest edge of triangle i + 1: every interior spoke is non-frontier, the

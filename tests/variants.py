@@ -12,7 +12,8 @@ paper_2403_14723_b200/variants/libpolylla_<name>.so (rebuilt when a source is ne
   tile384   k_tile with 384 threads (6 triangle iterations per thread), no pointer
             jumping (rotation chains resolved by hops only)
   fallback  a 64-entry k_emit queue (every tile takes the dense-tile branch) and an
-            in-tile loop-walk bound of 3 (almost every seed goes to the global walk)
+            in-tile loop-walk bound of 3 (almost every seed goes to the global walk); repair
+            rotations above degree 4 walked per incoming frontier half-edge
 """
 from __future__ import annotations
 
@@ -30,7 +31,7 @@ VARIANTS = {
                 "-DPOLYLLA_REPAIR_THREADS=256", "-DPOLYLLA_LEFT_THREADS=128", "-DPOLYLLA_BIT_CHUNK=4",
                 "-DPOLYLLA_UF_THREADS=256", "-DPOLYLLA_TILE_SLOTS=4104"],
     "tile384": ["-DPOLYLLA_TILE_THREADS=384", "-DPOLYLLA_TILE_JUMPS=0"],
-    "fallback": ["-DPOLYLLA_EMIT_Q=64", "-DPOLYLLA_P6_MAXLEN=3"],
+    "fallback": ["-DPOLYLLA_EMIT_Q=64", "-DPOLYLLA_P6_MAXLEN=3", "-DPOLYLLA_ROT_MAX=4"],
 }
 
 
