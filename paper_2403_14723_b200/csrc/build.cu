@@ -806,6 +806,7 @@ __global__ void __launch_bounds__(kTileThreads, 2)
            unsigned long long* __restrict__ left_key, hid* __restrict__ left_e, hid* __restrict__ def_e,
            uint32_t* __restrict__ SDB, int32_t* __restrict__ cnt_ld, DevCounters* ctr,
            int64_t prefetch_dist, int64_t tile_base, const Tiling tl) {
+  pdl_enter();
   extern __shared__ __align__(16) unsigned char smem_tile[];
   const int64_t ntiles = MODE != kTileContig ? tl.ntiles : (T + kTileTris - 1) / kTileTris;
   // tiles [tile_base, tile_base + gridDim.x): all of them, or one chunk of an upload
@@ -847,6 +848,7 @@ __device__ __forceinline__ uint64_t hash_cap_for(uint32_t n) {
 }
 
 __global__ void k_hash_clear(DevCounters* ctr, uint32_t* ehash, int64_t cap_max, int64_t V, int64_t T) {
+  pdl_enter();
   const uint64_t cap = hash_cap_for(ctr->n_left);
   if ((int64_t)cap > cap_max) {
     if (blockIdx.x == 0 && threadIdx.x == 0) raise_status(ctr, ST_INTERNAL);
@@ -883,6 +885,7 @@ __device__ __forceinline__ uint32_t left_home(uint32_t lo, uint32_t hi, unsigned
 __global__ void k_left_insert(DevCounters* ctr, int64_t ntiles, int64_t T, const Tiling tl,
                               const int32_t* __restrict__ cnt_ld, unsigned long long* left_key,
                               const hid* __restrict__ left_e, hid* twin, uint32_t* ehash) {
+  pdl_enter();
   if (ctr->status) return;
   const uint32_t mask = (uint32_t)ctr->hash_cap - 1;
   const unsigned long long scale = ctr->hash_scale;
@@ -942,6 +945,7 @@ __global__ void __launch_bounds__(kSegThreads)
     k_border_rank(DevCounters* ctr, int64_t ntiles, const int32_t* __restrict__ cnt_ld,
                   const hid* __restrict__ left_e, const unsigned long long* left_key, hid* blist,
                   uint32_t* __restrict__ bcnt) {
+  pdl_enter();
   __shared__ int32_t wtot[kSegThreads / 32];
   if (ctr->status) return;
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
@@ -973,6 +977,7 @@ __global__ void __launch_bounds__(kSegThreads)
 constexpr int kBorderScanThreads = 1024;
 __global__ void __launch_bounds__(kBorderScanThreads)
     k_border_scan(DevCounters* ctr, int64_t ntiles, int64_t T3, int64_t Bmax, uint32_t* bcnt) {
+  pdl_enter();
   constexpr int NW = kBorderScanThreads / 32;
   __shared__ long long wsum[NW];
   if (ctr->status) return;
@@ -1019,6 +1024,7 @@ __global__ void __launch_bounds__(kBorderScanThreads)
 __global__ void __launch_bounds__(kSegThreads)
     k_border_emit(DevCounters* ctr, int64_t ntiles, int64_t T3, const hid* __restrict__ blist,
                   const uint32_t* __restrict__ bbase, int32_t* origin, hid* twin, hid* vmap) {
+  pdl_enter();
   if (ctr->status) return;
   const uint32_t nb = ctr->n_border;
   for (int64_t it = blockIdx.x; it < ntiles; it += gridDim.x) {
@@ -1045,6 +1051,7 @@ __global__ void __launch_bounds__(kSegThreads)
 __global__ void k_bb_mark(DevCounters* ctr, int64_t ntiles, int64_t T, const Tiling tl,
                           const int32_t* __restrict__ cnt_ld, const hid* __restrict__ left_e,
                           const unsigned long long* __restrict__ left_key, uint32_t* BB) {
+  pdl_enter();
   if (ctr->status) return;
   for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
     const int32_t n = cnt_ld[2 * tile];
@@ -1060,6 +1067,7 @@ __global__ void k_bb_mark(DevCounters* ctr, int64_t ntiles, int64_t T, const Til
 constexpr int kBBChunk = 192;  // words per chunk (6 per lane)
 __global__ void k_bb_count(DevCounters* ctr, int64_t n_words, int64_t nchunks, const uint32_t* __restrict__ BB,
                            uint32_t* __restrict__ bcnt) {
+  pdl_enter();
   if (ctr->status) return;
   const int lane = threadIdx.x & 31;
   const int64_t nw = (int64_t)gridDim.x * (blockDim.x >> 5);
@@ -1077,6 +1085,7 @@ __global__ void k_bb_count(DevCounters* ctr, int64_t n_words, int64_t nchunks, c
 __global__ void k_bb_emit(DevCounters* ctr, int64_t n_words, int64_t nchunks, int64_t T3,
                           const uint32_t* __restrict__ BB, const uint32_t* __restrict__ bbase, int32_t* origin,
                           hid* twin, hid* vmap) {
+  pdl_enter();
   if (ctr->status) return;
   const int lane = threadIdx.x & 31;
   constexpr int kWPL = kBBChunk / 32;
@@ -1118,6 +1127,7 @@ __global__ void k_bb_emit(DevCounters* ctr, int64_t n_words, int64_t nchunks, in
 // the vmap[origin(b)] == b check (NON_MANIFOLD_VERTEX).
 __global__ void k_border_next(DevCounters* ctr, int64_t T3, const int32_t* __restrict__ origin,
                               const hid* __restrict__ twin, const hid* __restrict__ vmap, hid* next) {
+  pdl_enter();
   if (ctr->status) return;
   const uint32_t nb = ctr->n_border;
   for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < nb; i += gridDim.x * blockDim.x) {
@@ -1143,11 +1153,13 @@ __device__ __forceinline__ double of_ord(unsigned long long o) {
   return __longlong_as_double((long long)((o >> 63) ? (o & 0x7FFFFFFFFFFFFFFFull) : ~o));
 }
 __global__ void k_sort_init(unsigned long long* bbox, uint32_t* hist, int64_t cells) {
+  pdl_enter();
   if (blockIdx.x == 0 && threadIdx.x < 4) bbox[threadIdx.x] = (threadIdx.x & 1) ? 0ull : ~0ull;  // min x, max x, min y, max y
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < cells; i += (int64_t)gridDim.x * blockDim.x)
     hist[i] = 0;
 }
 __global__ void __launch_bounds__(256) k_sort_bbox(const double2* __restrict__ xy, int64_t V, unsigned long long* bbox) {
+  pdl_enter();
   __shared__ unsigned long long red[4][8];
   unsigned long long mnx = ~0ull, mxx = 0, mny = ~0ull, mxy = 0;
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < V; i += (int64_t)gridDim.x * blockDim.x) {
@@ -1183,6 +1195,7 @@ __device__ __forceinline__ uint32_t spread8(uint32_t v) {  // 8 bits -> every ot
 __global__ void k_sort_keys(const double2* __restrict__ xy, const int32_t* __restrict__ tri, int64_t V, int64_t T,
                             const unsigned long long* __restrict__ bbox, uint32_t* __restrict__ key,
                             uint32_t* hist) {
+  pdl_enter();
   const double x0 = of_ord(bbox[0]), x1 = of_ord(bbox[1]), y0 = of_ord(bbox[2]), y1 = of_ord(bbox[3]);
   const double sx = x1 > x0 ? 255.999 / (x1 - x0) : 0.0, sy = y1 > y0 ? 255.999 / (y1 - y0) : 0.0;
   for (int64_t f = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; f < T; f += (int64_t)gridDim.x * blockDim.x) {
@@ -1201,6 +1214,7 @@ __global__ void k_sort_keys(const double2* __restrict__ xy, const int32_t* __res
 // exclusive scan of the cell counts in place: one block of 1024 threads, warp w owns the
 // 8,192 cells from 8,192 w on, read lane-strided (coalesced), two passes
 __global__ void __launch_bounds__(1024) k_sort_scan(uint32_t* hist) {
+  pdl_enter();
   constexpr int per = (int)(kSortCells / 32);  // cells per warp
   __shared__ uint32_t wsum[32];
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
@@ -1236,6 +1250,7 @@ __global__ void __launch_bounds__(1024) k_sort_scan(uint32_t* hist) {
   }
 }
 __global__ void k_sort_scatter(int64_t T, const uint32_t* __restrict__ key, uint32_t* cursor, int32_t* __restrict__ perm) {
+  pdl_enter();
   for (int64_t f = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; f < T; f += (int64_t)gridDim.x * blockDim.x) {
     const uint32_t cell = key[f];
     const uint32_t m = __activemask(), peers = __match_any_sync(m, cell);
@@ -1313,12 +1328,12 @@ int launch_build_begin(Ctx* c, cudaStream_t s) {
   }
   if (c->tiling.mode == kTileSorted) {  // the triangle order of the sorted tiling
     const unsigned g = 148 * 8;
-    k_sort_init<<<g, 256, 0, s>>>(c->sort_bbox, c->sort_hist, kSortCells);
-    k_sort_bbox<<<g, 256, 0, s>>>(reinterpret_cast<const double2*>(c->xy), c->V, c->sort_bbox);
-    k_sort_keys<<<g, 256, 0, s>>>(reinterpret_cast<const double2*>(c->xy), c->tri, c->V, c->T, c->sort_bbox,
+    launch_k(k_sort_init, g, 256, 0, s, c->sort_bbox, c->sort_hist, kSortCells);
+    launch_k(k_sort_bbox, g, 256, 0, s, reinterpret_cast<const double2*>(c->xy), c->V, c->sort_bbox);
+    launch_k(k_sort_keys, g, 256, 0, s, reinterpret_cast<const double2*>(c->xy), c->tri, c->V, c->T, c->sort_bbox,
                                   c->sort_key, c->sort_hist);
-    k_sort_scan<<<1, 1024, 0, s>>>(c->sort_hist);
-    k_sort_scatter<<<g, 256, 0, s>>>(c->T, c->sort_key, c->sort_hist, const_cast<int32_t*>(c->tiling.perm));
+    launch_k(k_sort_scan, 1, 1024, 0, s, c->sort_hist);
+    launch_k(k_sort_scatter, g, 256, 0, s, c->T, c->sort_key, c->sort_hist, const_cast<int32_t*>(c->tiling.perm));
     if (cudaGetLastError() != cudaSuccess) return -1;
   }
   int n_sm = 0;
@@ -1336,7 +1351,7 @@ int launch_build_tiles(Ctx* c, cudaStream_t s, int64_t t0, int64_t t1) {
   prof_mark(s, "k_tile");
   auto kt = c->tiling.mode == kTileGrid ? k_tile<kTileGrid> : c->tiling.mode == kTileSorted ? k_tile<kTileSorted>
                                                                                          : k_tile<kTileContig>;
-  kt<<<(unsigned)(t1 - t0), kTileThreads, c->tiling.mode != kTileContig ? kTileSmemGrid : kTileSmem, s>>>(reinterpret_cast<const double2*>(c->xy), c->tri, c->V, c->T,
+  launch_k(kt, (unsigned)(t1 - t0), kTileThreads, c->tiling.mode != kTileContig ? kTileSmemGrid : kTileSmem, s, reinterpret_cast<const double2*>(c->xy), c->tri, c->V, c->T,
                                                           c->origin, c->twin, c->next, c->lcode, c->F0, bv_stride, c->C,
                                                           c->len, c->wlen, c->left_key, c->left_e, c->def_e, c->SDB,
                                                           c->cnt_ld, c->ctr, pf_dist, t0, c->tiling);
@@ -1359,36 +1374,36 @@ int launch_build_rest(Ctx* c, cudaStream_t s) {
   const int grid = 148 * 32;  // enough threads for ~1 leftover each on 10M-vertex meshes (latency-bound)
   prof_mark(s, "k_left_match");
   uint32_t* ehash = static_cast<uint32_t*>(c->ehash);
-  k_hash_clear<<<grid, 256, 0, s>>>(c->ctr, ehash, c->hash_cap_max, c->V, c->T);
+  launch_k(k_hash_clear, grid, 256, 0, s, c->ctr, ehash, c->hash_cap_max, c->V, c->T);
 #ifndef POLYLLA_LEFT_THREADS
 #define POLYLLA_LEFT_THREADS 256  // 128 / 256 / 384 / 512 measured: 128-256 best
 #endif
   const unsigned seg_grid = (unsigned)(tiles < 148 * 16 ? tiles : 148 * 16);
   const unsigned left_grid = (unsigned)(tiles < 148 * (4096 / POLYLLA_LEFT_THREADS) ? tiles : 148 * (4096 / POLYLLA_LEFT_THREADS));
-  k_left_insert<<<left_grid, POLYLLA_LEFT_THREADS, 0, s>>>(c->ctr, tiles, c->T, c->tiling, c->cnt_ld, c->left_key,
+  launch_k(k_left_insert, left_grid, POLYLLA_LEFT_THREADS, 0, s, c->ctr, tiles, c->T, c->tiling, c->cnt_ld, c->left_key,
                                                            c->left_e, c->twin, ehash);
   if (c->tiling.mode != kTileContig) {  // grid / sorted tiles: the border ranking by bit order
     const int64_t nchunks = (c->n_words + kBBChunk - 1) / kBBChunk;
-    k_bb_mark<<<seg_grid, kSegThreads, 0, s>>>(c->ctr, tiles, c->T, c->tiling, c->cnt_ld, c->left_e, c->left_key, c->BB);
-    k_bb_count<<<(unsigned)((nchunks + 7) / 8), 256, 0, s>>>(c->ctr, c->n_words, nchunks, c->BB, c->bcnt);
+    launch_k(k_bb_mark, seg_grid, kSegThreads, 0, s, c->ctr, tiles, c->T, c->tiling, c->cnt_ld, c->left_e, c->left_key, c->BB);
+    launch_k(k_bb_count, (unsigned)((nchunks + 7) / 8), 256, 0, s, c->ctr, c->n_words, nchunks, c->BB, c->bcnt);
     n += 3;
     prof_mark(s, "k_border_scan");
-    k_border_scan<<<1, kBorderScanThreads, 0, s>>>(c->ctr, nchunks, 3 * c->T, c->Bmax, c->bcnt);
-    k_bb_emit<<<(unsigned)((nchunks + 7) / 8), 256, 0, s>>>(c->ctr, c->n_words, nchunks, 3 * c->T, c->BB, c->bcnt,
+    launch_k(k_border_scan, 1, kBorderScanThreads, 0, s, c->ctr, nchunks, 3 * c->T, c->Bmax, c->bcnt);
+    launch_k(k_bb_emit, (unsigned)((nchunks + 7) / 8), 256, 0, s, c->ctr, c->n_words, nchunks, 3 * c->T, c->BB, c->bcnt,
                                                              c->origin, c->twin, c->vmap);
     n += 2;
   } else {
     hid* blist = reinterpret_cast<hid*>(c->left_key);  // dead after k_left_insert
-    k_border_rank<<<seg_grid, kSegThreads, 0, s>>>(c->ctr, tiles, c->cnt_ld, c->left_e, c->left_key, blist, c->bcnt);
+    launch_k(k_border_rank, seg_grid, kSegThreads, 0, s, c->ctr, tiles, c->cnt_ld, c->left_e, c->left_key, blist, c->bcnt);
     n += 3;
     prof_mark(s, "k_border_scan");
-    k_border_scan<<<1, kBorderScanThreads, 0, s>>>(c->ctr, tiles, 3 * c->T, c->Bmax, c->bcnt);
-    k_border_emit<<<seg_grid, kSegThreads, 0, s>>>(c->ctr, tiles, 3 * c->T, blist, c->bcnt, c->origin, c->twin,
+    launch_k(k_border_scan, 1, kBorderScanThreads, 0, s, c->ctr, tiles, 3 * c->T, c->Bmax, c->bcnt);
+    launch_k(k_border_emit, seg_grid, kSegThreads, 0, s, c->ctr, tiles, 3 * c->T, blist, c->bcnt, c->origin, c->twin,
                                                    c->vmap);
     n += 2;
   }
   prof_mark(s, "k_border_next");
-  k_border_next<<<grid, 256, 0, s>>>(c->ctr, 3 * c->T, c->origin, c->twin, c->vmap, c->next);
+  launch_k(k_border_next, grid, 256, 0, s, c->ctr, 3 * c->T, c->origin, c->twin, c->vmap, c->next);
   ++n;
   prof_end(s);
   return cudaGetLastError() == cudaSuccess ? n : -1;

@@ -42,6 +42,7 @@ __global__ void __launch_bounds__(kEmitThreads)
            const uint32_t* __restrict__ tb, const int32_t* __restrict__ origin, const hid* __restrict__ next,
            hid* __restrict__ seeds, uint32_t* __restrict__ offsets, int64_t offsets_cap, int32_t* __restrict__ loops,
            int64_t loops_cap, DevCounters* ctr) {
+  pdl_enter();
   __shared__ hid qe[kEmitQ];
   __shared__ uint32_t qo[kEmitQ];
   __shared__ int32_t wbase[kEmitWords];
@@ -152,6 +153,7 @@ __global__ void __launch_bounds__(kEmitThreads)
 
 __global__ void k_prev(int64_t T, const hid* __restrict__ next, const uint32_t* __restrict__ F1,
                        hid* __restrict__ prev, DevCounters* ctr) {
+  pdl_enter();
   if (ctr->status) return;
   const int64_t T3 = 3 * T;
   const int64_t H = T3 + ctr->n_border;
@@ -168,13 +170,13 @@ int launch_extract(Ctx* c, uint32_t* offsets, int64_t offsets_cap, int32_t* loop
   prof_mark(s, "k_extract");
   if (loops) {
     const int64_t tiles = (c->T + kBuildTileTris - 1) / kBuildTileTris;
-    k_emit<<<(unsigned)tiles, kEmitThreads, 0, s>>>(c->T, c->n_words, c->C, c->len, c->tbase, c->origin, c->next,
+    launch_k(k_emit, (unsigned)tiles, kEmitThreads, 0, s, c->T, c->n_words, c->C, c->len, c->tbase, c->origin, c->next,
                                                    c->seeds, offsets ? offsets : c->offsets,
                                                    offsets ? offsets_cap : c->T + 1, loops, loops_cap, c->ctr);
     ++n;
   }
   if (prev) {
-    k_prev<<<148 * 16, 256, 0, s>>>(c->T, c->next, c->F1, prev, c->ctr);
+    launch_k(k_prev, 148 * 16, 256, 0, s, c->T, c->next, c->F1, prev, c->ctr);
     ++n;
   }
   prof_end(s);

@@ -41,6 +41,7 @@ constexpr int kRotMax = POLYLLA_ROT_MAX;
 __global__ void __launch_bounds__(kRepairThreads)
     k_repair_mid(int64_t T, int64_t n_words, const uint32_t* __restrict__ TB, const hid* __restrict__ twin,
                  uint32_t* F1, uint32_t* SDB, hid* __restrict__ tips, hid* __restrict__ aff, DevCounters* ctr) {
+  pdl_enter();
   __shared__ hid queue[kRepairThreads / 32][kBitQueue];
   if (ctr->status) return;
   const int64_t T3 = 3 * T;
@@ -81,6 +82,7 @@ __global__ void __launch_bounds__(kRepairThreads)
 __global__ void __launch_bounds__(kRepairThreads)
     k_repair_rewire(int64_t T, const hid* __restrict__ twin, const uint32_t* __restrict__ F1,
                     const hid* __restrict__ aff, hid* next, DevCounters* ctr) {
+  pdl_enter();
   __shared__ hid rot_s[kRotMax][kRepairThreads];  // (entry k of this thread's rotation: rot_s[k][tid])
   if (ctr->status) return;
   const int64_t T3 = 3 * T;
@@ -179,6 +181,7 @@ __global__ void __launch_bounds__(kSeedThreads)
     k_seed_walk(int64_t T, int64_t n_words, const uint32_t* __restrict__ SDB, const hid* __restrict__ twin,
                 const hid* __restrict__ next, const uint32_t* __restrict__ F1, uint32_t* C, uint8_t* len,
                 int32_t* wlen, DevCounters* ctr) {
+  pdl_enter();
   __shared__ hid queue[kSeedThreads / 32][kBitQueue];
   if (ctr->status) return;
   const int64_t T3 = 3 * T;
@@ -198,6 +201,7 @@ constexpr int kTileWordsG = 3 * kBuildTileTris / 32;  // 192
 __global__ void k_canon_tiles(int64_t n_words, int64_t ntiles, const uint32_t* __restrict__ C,
                               const int32_t* __restrict__ wlen, const uint32_t* __restrict__ F1, int32_t* __restrict__ ts,
                               DevCounters* ctr) {
+  pdl_enter();
   if (ctr->status) return;
   const int lane = threadIdx.x & 31;
   const int64_t nwarps = (int64_t)gridDim.x * (blockDim.x >> 5);
@@ -230,6 +234,7 @@ constexpr int kTopThreads = 1024;
 __global__ void __launch_bounds__(kTopThreads)
     k_tiles_scan(int64_t ntiles, const int32_t* __restrict__ ts, uint32_t* __restrict__ tb, uint32_t* __restrict__ offsets,
                  DevCounters* ctr) {
+  pdl_enter();
   constexpr int NW = kTopThreads / 32;
   __shared__ long long wsum[3][NW];
   if (ctr->status) return;
@@ -291,11 +296,11 @@ int launch_generate(Ctx* c, cudaStream_t s) {
   int n = 0;
   if (c->next_pre) cudaMemcpyAsync(c->next_pre, c->next, (size_t)c->Hmax * 4, cudaMemcpyDeviceToDevice, s);
   prof_mark(s, "k_repair");
-  k_repair_mid<<<148 * (1536 / kRepairThreads), kRepairThreads, 0, s>>>(c->T, c->n_words, c->TB, c->twin, c->F1, c->SDB, c->tips, c->aff, c->ctr);
-  k_repair_rewire<<<148 * (4096 / kRepairThreads), kRepairThreads, 0, s>>>(c->T, c->twin, c->F1, c->aff, c->next, c->ctr);
+  launch_k(k_repair_mid, 148 * (1536 / kRepairThreads), kRepairThreads, 0, s, c->T, c->n_words, c->TB, c->twin, c->F1, c->SDB, c->tips, c->aff, c->ctr);
+  launch_k(k_repair_rewire, 148 * (4096 / kRepairThreads), kRepairThreads, 0, s, c->T, c->twin, c->F1, c->aff, c->next, c->ctr);
   prof_mark(s, "k_seed_walk");
   // (the canonical bit-vector C was written in full by k_tile; global walks OR into it)
-  k_seed_walk<<<148 * (2048 / kSeedThreads), kSeedThreads, 0, s>>>(c->T, c->n_words, c->SDB, c->twin, c->next, c->F1, c->C, c->len,
+  launch_k(k_seed_walk, 148 * (2048 / kSeedThreads), kSeedThreads, 0, s, c->T, c->n_words, c->SDB, c->twin, c->next, c->F1, c->C, c->len,
                                                c->wlen, c->ctr);
   n += 3;
   const int m = launch_canon_scan(c, s);
@@ -307,8 +312,8 @@ int launch_generate(Ctx* c, cudaStream_t s) {
 int launch_canon_scan(Ctx* c, cudaStream_t s) {
   prof_mark(s, "k_canon_scan");
   const int64_t tiles = (c->T + kBuildTileTris - 1) / kBuildTileTris;
-  k_canon_tiles<<<(unsigned)((tiles + 7) / 8), 256, 0, s>>>(c->n_words, tiles, c->C, c->wlen, c->F1, c->tsum, c->ctr);
-  k_tiles_scan<<<1, kTopThreads, 0, s>>>(tiles, c->tsum, c->tbase, c->offsets, c->ctr);
+  launch_k(k_canon_tiles, (unsigned)((tiles + 7) / 8), 256, 0, s, c->n_words, tiles, c->C, c->wlen, c->F1, c->tsum, c->ctr);
+  launch_k(k_tiles_scan, 1, kTopThreads, 0, s, tiles, c->tsum, c->tbase, c->offsets, c->ctr);
   prof_end(s);
   return cudaGetLastError() == cudaSuccess ? 2 : -1;
 }

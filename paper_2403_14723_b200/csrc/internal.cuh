@@ -179,6 +179,39 @@ int launch_regions(Ctx* c, int32_t* out, int mode, cudaStream_t s);  // mode 0: 
 int launch_check_manifold(Ctx* c, cudaStream_t s);
 int launch_paper(Ctx* c, cudaStream_t s);  // the paper's LLK..OSK + Scan sequence (NEXT-2 ablation)
 
+// Programmatic dependent launch (PDL): the hot-path kernels are launched with
+// programmatic stream serialisation, so a kernel's CTAs are scheduled while its
+// predecessor's last wave still runs; each kernel waits (griddepcontrol.wait: the
+// predecessor grid complete and its writes visible) before touching any memory, then
+// lets its own successor launch.  POLYLLA_PDL=0 builds plain launches (A/B).
+#ifndef POLYLLA_PDL
+#define POLYLLA_PDL 1
+#endif
+__device__ __forceinline__ void pdl_enter() {
+#if POLYLLA_PDL
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+#endif
+}
+template <typename... KP, typename... A>
+inline void launch_k(void (*k)(KP...), dim3 grid, dim3 block, size_t smem, cudaStream_t s, A... a) {
+#if POLYLLA_PDL
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  cudaLaunchKernelEx(&cfg, k, static_cast<KP>(a)...);  // (errors: cudaGetLastError at the launcher's end)
+#else
+  k<<<grid, block, smem, s>>>(static_cast<KP>(a)...);
+#endif
+}
+
 // ------------------------------------------------------------------ device helpers
 __device__ __forceinline__ hid next_in(hid e) {  // 3f + (k+1)%3
   const hid k = e % 3u;

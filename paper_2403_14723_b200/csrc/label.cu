@@ -34,6 +34,7 @@ __global__ void __launch_bounds__(kLabelThreads)
                   const hid* __restrict__ twin, const uint8_t* __restrict__ lcode, hid* __restrict__ next,
                   uint32_t* __restrict__ F0, uint32_t* __restrict__ F1, uint32_t* __restrict__ S,
                   uint32_t* __restrict__ TB, uint32_t* __restrict__ SDB, DevCounters* ctr) {
+  pdl_enter();
   if (ctr->status) return;
   const int64_t T3 = 3 * T;
   const int lane = threadIdx.x & 31;
@@ -91,7 +92,7 @@ constexpr int kFixBlocksPerSM = 4096 / kLabelThreads;  // a grid of 2 resident w
 int launch_label(Ctx* c, cudaStream_t s) {
   const int64_t tiles = c->tiling.ntiles;
   prof_mark(s, "k_label_fixup");
-  k_label_fixup<<<(unsigned)(tiles < 148 * kFixBlocksPerSM ? tiles : 148 * kFixBlocksPerSM), kLabelThreads, 0, s>>>(
+  launch_k(k_label_fixup, (unsigned)(tiles < 148 * kFixBlocksPerSM ? tiles : 148 * kFixBlocksPerSM), kLabelThreads, 0, s, 
       c->T, tiles, c->tiling, c->cnt_ld, c->def_e, c->twin, c->lcode, c->next, c->F0, c->F1, c->S, c->TB, c->SDB, c->ctr);
   prof_end(s);
   return cudaGetLastError() == cudaSuccess ? 1 : -1;
