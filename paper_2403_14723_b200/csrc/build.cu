@@ -493,7 +493,14 @@ __device__ __forceinline__ void tile_body(
   nm = 0;
   for (int i = tid; i < kTileTris; i += kTileThreads) succ[4 * i + 3] = 0xFFFFu;
   {
-    uint32_t* const s_dst = lane == 0 ? Sw : Lm;
+    // the two ballot words of every iteration are kept by one lane each and stored after
+    // the loop (one store per lane instead of a divergent store branch per iteration)
+    constexpr bool kBatchWords = kHeIters <= 8;
+    const int keep_i = lane & 7;
+    const bool keep_l = (lane >> 3) == 1;
+    uint32_t kept = 0;
+    (void)keep_i; (void)keep_l; (void)kept;
+    uint32_t* const s_dst = kBatchWords ? (lane < 8 ? Sw : Lm) : (lane == 0 ? Sw : Lm);
     int q = q_of(tid);
 #pragma unroll 4
     for (int i = 0; i < kHeIters; ++i, q = q_step(q)) {
@@ -526,12 +533,23 @@ __device__ __forceinline__ void tile_body(
         left = tq < 0;
       }
       const uint32_t sw = __ballot_sync(0xffffffffu, sd), lw = __ballot_sync(0xffffffffu, left);
-      const int wl = (j - lane) >> 5;  // tile-local word of this warp
-      // lane 0: Sw, lane 1: Lm (shared); lane 2: the global S
-      if (lane < 2) {
-        s_dst[wl] = lane == 0 ? sw : lw;
-      } else if (!SCAT && lane == 2 && (FULL || j - lane < nhe)) {  // (grid / sorted tiles: flushed at the end)
-        F0[2 * bv_stride + (e0 >> 5) + wl] = sw;
+      if constexpr (kBatchWords) {
+        if (i == keep_i) kept = keep_l ? lw : sw;  // (stored once, after the loop)
+      } else {
+        const int wl = (j - lane) >> 5;  // tile-local word of this warp
+        // lane 0: Sw, lane 1: Lm (shared); lane 2: the global S
+        if (lane < 2) {
+          s_dst[wl] = lane == 0 ? sw : lw;
+        } else if (!SCAT && lane == 2 && (FULL || j - lane < nhe)) {  // (grid / sorted tiles: flushed at the end)
+          F0[2 * bv_stride + (e0 >> 5) + wl] = sw;
+        }
+      }
+    }
+    if constexpr (kBatchWords) {  // lanes 0-7: Sw, 8-15: Lm (shared), 16-23: the global S of iteration lane % 8
+      const int wl = (tid >> 5) + keep_i * (kTileThreads / 32);
+      if (lane < 24 && keep_i < kHeIters && wl < kTileWords) {
+        if (lane < 16) s_dst[wl] = kept;
+        else if (!SCAT && (FULL || 32 * wl < nhe)) F0[2 * bv_stride + (e0 >> 5) + wl] = kept;
       }
     }
   }
