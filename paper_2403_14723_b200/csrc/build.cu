@@ -87,10 +87,11 @@ constexpr uint32_t kEmpty16 = 0xFFFFu;             // empty 16-bit slot (quad in
 // rotation successors (P3/P4): quad index in the low 13 bits, terminal flags above
 constexpr uint16_t kSuccIdx = 0x1FFF, kSuccFront = 0x4000, kSuccUnknown = 0x8000;
 #ifndef POLYLLA_TILE_JUMPS
-#define POLYLLA_TILE_JUMPS 2  // measured 0 (walks) / 2 / 4 on configs 3 and 5
+#define POLYLLA_TILE_JUMPS 1  // measured 0 / 2 / 4 (round 2), 1 / 2 / 3 with the in-place jumping: 1 best
 #endif
-// pointer-jumping rounds (even: the result ends in succ); each use of a successor then
-// follows up to kTileHops more jumped pointers, so chains up to 16 steps resolve in-tile
+// pointer-jumping rounds (in place: after r rounds a successor is >= 2^r steps ahead); each
+// use of a successor then follows up to kTileHops more jumped pointers, so chains up to 16
+// steps resolve in-tile
 constexpr int kTileJumps = POLYLLA_TILE_JUMPS;
 constexpr int kTileHops = (16 >> kTileJumps) - 1;
 #ifndef POLYLLA_P6_MAXLEN
@@ -173,7 +174,12 @@ __device__ __forceinline__ uint32_t slot_succ(uint32_t p) { return p + 1 == (uin
 
 // collision loser of the claim pass: CAS (on the 32-bit word holding the 16-bit slot) +
 // linear probing from its home slot
-__device__ __noinline__ uint32_t tile_insert_probe(uint16_t* slot, const int32_t* tri_q, int32_t q, uint32_t lo,
+#ifdef POLYLLA_PROBE_NOINLINE  // (inlined: k_tile -1% with the 24,000-slot table)
+#define POLYLLA_PROBE_ATTR __noinline__
+#else
+#define POLYLLA_PROBE_ATTR __forceinline__
+#endif
+__device__ POLYLLA_PROBE_ATTR uint32_t tile_insert_probe(uint16_t* slot, const int32_t* tri_q, int32_t q, uint32_t lo,
                                                    uint32_t hi) {
   uint32_t p = tile_pos(lo, hi);
   for (int probe = 0; probe < kTileSlots; ++probe, p = slot_succ(p)) {
@@ -193,7 +199,7 @@ __device__ __noinline__ uint32_t tile_insert_probe(uint16_t* slot, const int32_t
 }
 
 // the quad holding key lo -> hi, probing from the slot after its home (the home missed), or -1
-__device__ __noinline__ int32_t tile_lookup_probe(const uint16_t* slot, const int32_t* tri_q, uint32_t lo, uint32_t hi) {
+__device__ POLYLLA_PROBE_ATTR int32_t tile_lookup_probe(const uint16_t* slot, const int32_t* tri_q, uint32_t lo, uint32_t hi) {
   uint32_t p = tile_pos(lo, hi);
   for (int probe = 1; probe < kTileSlots; ++probe) {
     p = slot_succ(p);
@@ -232,8 +238,8 @@ __device__ __forceinline__ bool tri_here(int i, int t, int nt, int nrows, int nc
 //  P3 origin/twin written back coalesced; rotation successor of every half-edge: itself if it
 //     is a frontier edge (Alg. 8), else next_in(twin) (sweep_out, R1); a third copy of
 //     an edge breaks the twin involution
-//  P4 the unlink rewire (Alg. 11) by pointer jumping on the successors (2 lock-step
-//     rounds, then up to 3 jumped hops at each use: chains <= 16 steps); frontier / seed bits (Alg. 8-9); tips (next == twin);
+//  P4 the unlink rewire (Alg. 11) by pointer jumping on the successors (kTileJumps
+//     rounds in place, then up to kTileHops jumped hops at each use: chains <= 16 steps); frontier / seed bits (Alg. 8-9); tips (next == twin);
 //     half-edges needing a twin outside the tile (or a longer rotation) are deferred
 //     to k_label_fixup (label phase)
 //  P5 the leftover and deferred lists as per-tile segments (each word ranked by its warp)
