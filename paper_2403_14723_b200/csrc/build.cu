@@ -301,6 +301,10 @@ __device__ __forceinline__ void tile_body(
   const int32_t* raw = tri + e0;  // (contiguous tiles)
   for (int i = tid; i < kTileSlots / 8; i += kTileThreads)
     reinterpret_cast<uint4*>(slot)[i] = make_uint4(0xFFFFFFFFu, 0xFFFFFFFFu, 0xFFFFFFFFu, 0xFFFFFFFFu);
+  // (32-bit stores: with 16-byte ones here ptxas 12.9 scheduled the slot clear above's
+  // single predicated STS.128 of a partial tile before three of its four source registers
+  // were set whenever the table had < 768 uint4s -- garbage slots, caught by the 4,104-slot
+  // test variant; the 32-bit form is correct in every variant)
   for (int i = tid; i < kTileQ / 2; i += kTileThreads) reinterpret_cast<uint32_t*>(tw_s)[i] = 0xFFFFFFFFu;
   const TileGeom tn_ = tile_next < 0 ? TileGeom{0, 0, 0, 0} : GRID ? tile_geom(tl, T, tile_next) : contig_geom(T, tile_next);
   const int64_t f0n = tn_.base;  // this CTA's next tile (prefetched), if tile_next >= 0
@@ -591,6 +595,22 @@ __device__ __forceinline__ void tile_body(
   // (next == twin, R4), deferred half-edges; the local next in quad indices (nx_q; the
   // global origin/twin/next are written from the quad arrays in half-edge order in P5)
   int16_t* nx_q = tw_s;  // quad-indexed local next over the twins (each thread reads its quad's twins first)
+  // the 9 words of iteration i (3 words x frontier / tip / deferred) are kept by lanes
+  // 9i .. 9i + 8 and stored once after the loop (POLYLLA_P4B_BATCH)
+#ifndef POLYLLA_P4B_BATCH
+#define POLYLLA_P4B_BATCH 1
+#endif
+  constexpr bool kBatch4 = POLYLLA_P4B_BATCH && 9 * kTriIters <= 32;
+  const int my_it = lane / 9, my_f = (lane % 9) / 3;
+  uint32_t kept4 = 0;
+  (void)my_it; (void)my_f; (void)kept4;
+  if constexpr (kBatch4) {  // (Cw, Wl, SDm: zero before P6's atomics)
+    for (int w = tid; w < kTileWords; w += kTileThreads) {
+      Sw[kTileWords + w] = 0u;
+      Sw[2 * kTileWords + w] = 0u;
+      Sw[5 * kTileWords + w] = 0u;
+    }
+  }
 #pragma unroll
   for (int i = 0; i < kTriIters; ++i) {
     if (!(i < kTriIters - 1 || tid < kTileTris - (kTriIters - 1) * kTileThreads)) continue;
@@ -630,6 +650,11 @@ __device__ __forceinline__ void tile_body(
     const uint32_t f0w = word_bits(packed, 0, 0), f1w = word_bits(packed, 1, 0), f2w = word_bits(packed, 2, 0);
     const uint32_t t0w = word_bits(packed, 0, 1), t1w = word_bits(packed, 1, 1), t2w = word_bits(packed, 2, 1);
     const uint32_t d0w = word_bits(packed, 0, 2), d1w = word_bits(packed, 1, 2), d2w = word_bits(packed, 2, 2);
+    if constexpr (kBatch4) {
+      if (my_it == i)
+        kept4 = my_f == 0 ? pick_m(f0w, f1w, f2w) : my_f == 1 ? pick_m(t0w, t1w, t2w) : pick_m(d0w, d1w, d2w);
+      continue;
+    }
     // lanes 0-11: shared Cw (0), Wl (0), Dm, SDm (0); lanes 12-20: global F0, F1, TB
     if (lane < 12) {
       const int r = lane_ty == 0 ? 1 : lane_ty == 1 ? 2 : lane_ty == 2 ? 4 : 5;  // Cw, Wl, Dm, SDm
@@ -640,6 +665,21 @@ __device__ __forceinline__ void tile_body(
     } else if (lane < 21 && (FULL || 32 * (wl0 + lane_m) < nhe)) {
       const int g = lane_ty == 4 ? 0 : lane_ty == 5 ? 1 : 3;  // F0, F1, TB
       F0[g * bv_stride + (e0 >> 5) + wl0 + lane_m] = lane_ty == 6 ? pick_m(t0w, t1w, t2w) : pick_m(f0w, f1w, f2w);
+    }
+  }
+  if constexpr (kBatch4) {
+    const int wl = (3 * kTileThreads / 32) * my_it + wl_warp + lane_m;
+    if (lane < 9 * kTriIters && wl < kTileWords) {
+      if (my_f == 2) Dm[wl] = kept4;
+      else if (SCAT) (my_f == 0 ? Fw : Tw)[wl] = kept4;  // (flushed at the end)
+      else if (FULL || 32 * wl < nhe) {
+        if (my_f == 0) {
+          F0[(e0 >> 5) + wl] = kept4;
+          F0[bv_stride + (e0 >> 5) + wl] = kept4;
+        } else {
+          F0[3 * bv_stride + (e0 >> 5) + wl] = kept4;
+        }
+      }
     }
   }
   __syncthreads();
