@@ -16,13 +16,23 @@ namespace polylla {
 // walks one polygon: offsets/seeds at the polygon's rank, the loop's vertex ids from
 // its canonical seed (the tile's next/origin lines stay in L1 across the CTA's walks).
 // Polygons come out in ascending canonical-seed order.
-constexpr int kEmitWords = 3 * kBuildTileTris / 32;  // 192
+constexpr int kEmitTileWords = 3 * kBuildTileTris / 32;  // 192
+// each build tile is emitted by kEmitSub CTAs, one per run of kEmitWords words: a CTA
+// holds its shared memory and registers until its longest loop walk ends, so smaller
+// parts free them sooner (a part's bases: the tile's, plus the popcounts / per-word length
+// sums of the tile's earlier words)
+#ifndef POLYLLA_EMIT_SUB
+#define POLYLLA_EMIT_SUB 3  // (parts per tile: 1 / 2 / 3 / 6 measured on configs 3 and 5; 3 best, 6 equal)
+#endif
+constexpr int kEmitSub = POLYLLA_EMIT_SUB;
+constexpr int kEmitWords = kEmitTileWords / kEmitSub;
+static_assert(kEmitTileWords % kEmitSub == 0 && kEmitWords % 32 == 0, "emission parts of whole lanes of words");
 #ifndef POLYLLA_EMIT_THREADS
-#define POLYLLA_EMIT_THREADS 384  // measured 256/384/512 on configs 3 and 5
+#define POLYLLA_EMIT_THREADS (384 / POLYLLA_EMIT_SUB)  // (one part per tile: 256/384/512 measured, 384 best; two: 192 / 256)
 #endif
 constexpr int kEmitThreads = POLYLLA_EMIT_THREADS;
 #ifndef POLYLLA_EMIT_Q
-#define POLYLLA_EMIT_Q 2048  // (a test variant sets it tiny to force the dense-tile branch)
+#define POLYLLA_EMIT_Q (2048 / POLYLLA_EMIT_SUB)  // (a test variant sets it tiny to force the dense-tile branch)
 #endif
 constexpr int kEmitQ = POLYLLA_EMIT_Q;  // queue capacity (polygons per tile; a tile with more walks per word)
 
@@ -39,7 +49,8 @@ __device__ __forceinline__ uint32_t loop_len(const uint8_t* __restrict__ len, co
 
 __global__ void __launch_bounds__(kEmitThreads)
     k_emit(int64_t T, int64_t n_words, const uint32_t* __restrict__ C, const uint8_t* __restrict__ len,
-           const uint32_t* __restrict__ tb, const int32_t* __restrict__ origin, const hid* __restrict__ next,
+           const uint32_t* __restrict__ tb, const int32_t* __restrict__ wlen, const int32_t* __restrict__ origin,
+           const hid* __restrict__ next,
            hid* __restrict__ seeds, uint32_t* __restrict__ offsets, int64_t offsets_cap, int32_t* __restrict__ loops,
            int64_t loops_cap, DevCounters* ctr) {
   pdl_enter();
@@ -48,6 +59,7 @@ __global__ void __launch_bounds__(kEmitThreads)
   __shared__ int32_t wbase[kEmitWords];
   __shared__ int32_t chunk[kEmitThreads / 32 + 1];
   __shared__ int32_t npoly;
+  __shared__ uint32_t pbase[2];
   if (ctr->status) return;
   const int32_t P = ctr->P;
   const uint32_t L = ctr->L;
@@ -55,11 +67,29 @@ __global__ void __launch_bounds__(kEmitThreads)
     if (blockIdx.x == 0 && threadIdx.x == 0) raise_status(ctr, ST_CAPACITY);
     return;
   }
-  const int64_t tile = sched_tile(blockIdx.x, gridDim.x);
-  const int64_t wt = tile * kEmitWords;  // first word of the tile
+  const int64_t blk = sched_tile(blockIdx.x, gridDim.x);
+  const int64_t tile = blk / kEmitSub;
+  const int part = (int)(blk - tile * kEmitSub);
+  const int64_t wt = tile * kEmitTileWords + (int64_t)part * kEmitWords;  // first word of the part
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  if (warp == 0) {  // the part's bases: the tile's + the tile's earlier words (polygons, loop entries)
+    int pc = 0, lc = 0;
+    for (int k = lane; k < part * kEmitWords; k += 32) {
+      const int64_t ww = tile * kEmitTileWords + k;
+      if (ww < n_words) {
+        pc += __popc(C[ww]);
+        lc += wlen[ww];
+      }
+    }
+    pc = __reduce_add_sync(0xffffffffu, pc);
+    lc = __reduce_add_sync(0xffffffffu, lc);
+    if (lane == 0) {
+      pbase[0] = tb[2 * tile] + (uint32_t)pc;
+      pbase[1] = tb[2 * tile + 1] + (uint32_t)lc;
+    }
+  }
   if (warp == 0) {  // per-word exclusive prefix of the canonical-seed count
-    constexpr int kWPL = kEmitWords / 32;  // 6
+    constexpr int kWPL = kEmitWords / 32;  // 3
     int cp[kWPL], sp = 0;
 #pragma unroll
     for (int k = 0; k < kWPL; ++k) {
@@ -83,7 +113,7 @@ __global__ void __launch_bounds__(kEmitThreads)
   }
   __syncthreads();
   const int np = npoly;
-  const uint32_t rbase = tb[2 * tile], obase = tb[2 * tile + 1];
+  const uint32_t rbase = pbase[0], obase = pbase[1];
   if (np > kEmitQ) {  // (dense tile) one thread per word walks its polygons in order
     for (int wl = tid; wl < kEmitWords && wt + wl < n_words; wl += kEmitThreads) {
       // offset of the word's first polygon: tile base + lengths of the earlier polygons
@@ -170,7 +200,8 @@ int launch_extract(Ctx* c, uint32_t* offsets, int64_t offsets_cap, int32_t* loop
   prof_mark(s, "k_extract");
   if (loops) {
     const int64_t tiles = (c->T + kBuildTileTris - 1) / kBuildTileTris;
-    launch_k(k_emit, (unsigned)tiles, kEmitThreads, 0, s, c->T, c->n_words, c->C, c->len, c->tbase, c->origin, c->next,
+    launch_k(k_emit, (unsigned)(tiles * kEmitSub), kEmitThreads, 0, s, c->T, c->n_words, c->C, c->len, c->tbase, c->wlen,
+             c->origin, c->next,
                                                    c->seeds, offsets ? offsets : c->offsets,
                                                    offsets ? offsets_cap : c->T + 1, loops, loops_cap, c->ctr);
     ++n;
