@@ -178,7 +178,7 @@ __global__ void __launch_bounds__(kEmitThreads)
       for (int32_t k = 0; k < n; ++k, x = next[x]) dst[k] = origin[x];
     }
   }
-  if (tile == (int64_t)gridDim.x - 1 && tid == 0) offsets[P] = L;
+  if (blk == (int64_t)gridDim.x - 1 && tid == 0) offsets[P] = L;  // (the last part of the last tile)
 }
 
 __global__ void k_prev(int64_t T, const hid* __restrict__ next, const uint32_t* __restrict__ F1,
