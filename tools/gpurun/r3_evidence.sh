@@ -1,7 +1,7 @@
 # round 2 session 4 evidence (profiles/r02s4): host, full GPU suite, smoke, ncu launch list -> ncu_traffic.json
 # (this source hash), bench lines (c3 default, c2, c2 shuffled, c5, c4, reference arm),
 # per-kernel medians, ncu --set full of the top kernels
-O=gpurun_out/ev4; mkdir -p $O
+O=gpurun_out/ev5; mkdir -p $O
 (nproc; lscpu | grep -E "Model name|^CPU\(s\)"; free -g; nvidia-smi --query-gpu=name,memory.total,clocks.max.sm --format=csv) > $O/host.txt 2>&1
 timeout 2400 python -m pytest tests -m gpu -q -p no:cacheprovider > $O/pytest_gpu.txt 2>&1; tail -2 $O/pytest_gpu.txt
 timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > $O/smoke.txt 2>&1; tail -2 $O/smoke.txt
