@@ -74,7 +74,9 @@ __device__ __forceinline__ int q_step(int q) {
 constexpr size_t kOffTw = kTileQ * 4, kOffLc = kOffTw + kTileQ * 2, kOffSlot = kOffLc + kTileTris,
                  kOffWords = kOffSlot + kTileQ * 2,                            // (succ: the first 16 KB of the region)
                  kWordBytes = 8 * (kTileHE / 8),                               // 6,144 B
-                 kRegion = kTileQ * 2 + kWordBytes > kTileSlots * 2 ? kTileQ * 2 + kWordBytes : kTileSlots * 2,
+                 kSeedListBytes = 16 + 2 * (kTileHE / 2),                     // (P6 list: count + u16 seeds)
+                 kP3Bytes = kTileQ * 2 + kWordBytes + kSeedListBytes,
+                 kRegion = kP3Bytes > kTileSlots * 2 ? kP3Bytes : kTileSlots * 2,
                  kTileSmemGrid = kOffSlot + kRegion,                           // 99,200 B -> 2 CTAs/SM in 196 KB
                  kTileSmem = kTileSmemGrid;
 constexpr int kNxTip = 0x4000;  // nx_q: barrier tip (quad indices are < 0x2000)
@@ -97,7 +99,10 @@ constexpr int kTileHops = (16 >> kTileJumps) - 1;
 #ifndef POLYLLA_P6_MAXLEN
 #define POLYLLA_P6_MAXLEN 1024  // (a test variant sets it tiny to force the global seed walk)
 #endif
-constexpr int kP6MaxLen = POLYLLA_P6_MAXLEN;  // in-tile loop walks longer than this go to k_seed_walk
+constexpr int kP6MaxLen = POLYLLA_P6_MAXLEN;
+#ifndef POLYLLA_P6_LIST
+#define POLYLLA_P6_LIST 1  // P6 takes the tile's seeds from a list, one per thread (0: kSeedLanes per word)
+#endif  // in-tile loop walks longer than this go to k_seed_walk
 
 #ifdef POLYLLA_PHASE_TIMING
 __device__ unsigned long long g_phase_cycles[16];
@@ -565,6 +570,9 @@ __device__ __forceinline__ void tile_body(
   }
   if (kTriIters > 2) pf_issue();
   if (nm) raise_status(ctr, nm);
+  uint32_t* const seed_n = reinterpret_cast<uint32_t*>(smem_tile + kOffWords + kWordBytes);  // (dead table space)
+  uint16_t* const seed_list = reinterpret_cast<uint16_t*>(seed_n + 4);
+  if (POLYLLA_P6_LIST && tid == 0) *seed_n = 0;
   __syncthreads();
   PHASE_MARK(3);
 
@@ -601,6 +609,22 @@ __device__ __forceinline__ void tile_body(
 #define POLYLLA_P4B_BATCH 1
 #endif
   constexpr bool kBatch4 = POLYLLA_P4B_BATCH && 9 * kTriIters <= 32;
+#if POLYLLA_P6_LIST
+  if (tid < kTileWords) {  // the tile's seeds (S bits, final since P3) listed for P6 (one seed per thread there)
+    uint32_t sb = Sw[tid];
+    const int c = __popc(sb);
+    int incl = c;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int a = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += a;
+    }
+    uint32_t base = 0;
+    if (lane == 31) base = atomicAdd(seed_n, (uint32_t)incl);
+    base = __shfl_sync(0xffffffffu, base, 31) + (uint32_t)(incl - c);
+    for (; sb; sb &= sb - 1) seed_list[base++] = (uint16_t)(tid * 32 + __ffs(sb) - 1);
+  }
+#endif
   const int my_it = lane / 9, my_f = (lane % 9) / 3;
   uint32_t kept4 = 0;
   (void)my_it; (void)my_f; (void)kept4;
@@ -751,6 +775,11 @@ __device__ __forceinline__ void tile_body(
   // a deferred half-edge or a barrier tip (repaired later) are handed to the global
   // seed walk (bit-vector SDB).  kSeedLanes threads per word take its seeds in turn.
   {
+#if POLYLLA_P6_LIST
+    const int n_seeds = (int)*seed_n;  // one listed seed per thread (the walks fill whole warps)
+    for (int si = tid; si < n_seeds; si += kTileThreads) {
+      const int32_t sj = seed_list[si];
+#else
     constexpr int kSeedLanes = kTileThreads / kTileWords;  // 4 (the threads past kSeedLanes * 192 idle)
     static_assert(kSeedLanes >= 1, "threads per word");
     const int wsd = tid / kSeedLanes, sub = tid % kSeedLanes;
@@ -759,6 +788,7 @@ __device__ __forceinline__ void tile_body(
     while (sb) {
       const int32_t sj = wsd * 32 + __ffs(sb) - 1;
       for (int k = 0; k < kSeedLanes && sb; ++k) sb &= sb - 1;
+#endif
       uint16_t r = succ[q_of(sj)];  // the frontier half-edge the rotation reaches, if resolved
       for (int h = 0; h < kTileHops && !(r & (kSuccFront | kSuccUnknown)); ++h) r = succ[r];
       bool ok = (r & kSuccFront) != 0, tipped = false;
