@@ -776,8 +776,10 @@ __device__ __forceinline__ void tile_body(
   // seed walk (bit-vector SDB).  kSeedLanes threads per word take its seeds in turn.
   {
 #if POLYLLA_P6_LIST
-    const int n_seeds = (int)*seed_n;  // one listed seed per thread (the walks fill whole warps)
-    for (int si = tid; si < n_seeds; si += kTileThreads) {
+    const int n_seeds = (int)*seed_n;  // one listed seed per thread (the walks fill whole warps),
+    // the first ones to the threads past warps 0-5, which are still writing P5's lists
+    const int s0 = tid >= kTileWords ? tid - kTileWords : tid + (kTileThreads - kTileWords);
+    for (int si = s0; si < n_seeds; si += kTileThreads) {
       const int32_t sj = seed_list[si];
 #else
     constexpr int kSeedLanes = kTileThreads / kTileWords;  // 4 (the threads past kSeedLanes * 192 idle)
