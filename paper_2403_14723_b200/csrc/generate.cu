@@ -152,6 +152,13 @@ __global__ void __launch_bounds__(kRepairThreads)
 #define POLYLLA_SEED_THREADS 256
 #endif
 constexpr int kSeedThreads = POLYLLA_SEED_THREADS;
+#ifndef POLYLLA_SEED_DYN
+#define POLYLLA_SEED_DYN 1
+#endif
+#ifndef POLYLLA_SEED_BURST
+#define POLYLLA_SEED_BURST 4
+#endif
+constexpr int kSeedBurst = POLYLLA_SEED_BURST;
 
 __device__ __forceinline__ void process_seed(hid s, int64_t T3, int64_t H, const hid* __restrict__ twin,
                                              const hid* __restrict__ next, const uint32_t* __restrict__ F1,
@@ -186,9 +193,56 @@ __global__ void __launch_bounds__(kSeedThreads)
   if (ctr->status) return;
   const int64_t T3 = 3 * T;
   const int64_t H = T3 + ctr->n_border;
+#if POLYLLA_SEED_DYN
+  // a lane that closes its loop takes the next seed of the warp's queue (ballot of the idle
+  // lanes, ranks by popcount) instead of waiting for the round's longest walk; walks
+  // advance kSeedBurst steps between refills
+  const int lane = threadIdx.x & 31;
+  const int n = warp_foreach_bit<true>(SDB, n_words, queue[threadIdx.x >> 5], [&](const hid* q, int fill) {
+    int head = 0;
+    bool active = false;
+    hid x = 0, y = 0, mn = 0;
+    int64_t cnt = 0;
+    while (true) {
+      const uint32_t idle = __ballot_sync(0xffffffffu, !active);
+      if (head < fill && idle) {
+        const int my = head + __popc(idle & ((1u << lane) - 1));
+        head += __popc(idle);
+        if (!active && my < fill) {
+          const hid s = q[my];
+          hid xx = s;
+          int64_t steps = 0;
+          bool ok = true;
+          while (!f1_of(F1, T3, xx)) {  // Alg. 12: rotate (sweep_out) to a frontier half-edge
+            xx = next_in(twin[xx]);
+            if (++steps > T3 || xx == s) { raise_status(ctr, ST_WALK); ok = false; break; }
+          }
+          if (ok) { active = true; x = y = mn = xx; cnt = 0; }
+        }
+      }
+      if (!__any_sync(0xffffffffu, active)) {
+        if (head >= fill) break;
+        continue;
+      }
+#pragma unroll 1
+      for (int k = 0; k < kSeedBurst && active; ++k) {  // Overwrite seeds: walk the polygon, keep the minimum
+        mn = min(mn, y);
+        y = next[y];
+        if (++cnt > H) { raise_status(ctr, ST_WALK); active = false; break; }
+        if (y == x) {
+          len[mn] = len_code(cnt);
+          const uint32_t bit = 1u << (mn & 31);
+          if (!(atomicOr(&C[mn >> 5], bit) & bit)) atomicAdd(&wlen[mn >> 5], (int32_t)cnt);  // first setter only
+          active = false;
+        }
+      }
+    }
+  });
+#else
   const int n = warp_foreach_bit(SDB, n_words, queue[threadIdx.x >> 5], [&](hid s, bool valid) {
     if (valid) process_seed(s, T3, H, twin, next, F1, C, len, wlen, ctr);
   });
+#endif
   if ((threadIdx.x & 31) == 0 && n) atomicAdd(&ctr->n_sdef, (uint32_t)n);
 }
 

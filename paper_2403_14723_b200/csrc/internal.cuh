@@ -265,7 +265,8 @@ constexpr int kBitQueue = POLYLLA_BIT_QUEUE;  // small: the walks that follow li
 #endif
 constexpr int kBitChunk = POLYLLA_BIT_CHUNK;  // words per warp chunk (<= 32; 8 and 4 measured slower)
 static_assert(kBitChunk >= 1 && kBitChunk <= 32, "one word per lane");
-template <class F>
+// (WHOLE: each full or final queue is handed to f(q, fill) at once, all lanes present)
+template <bool WHOLE = false, class F>
 __device__ __forceinline__ int warp_foreach_bit(const uint32_t* __restrict__ bv, int64_t n_words, hid* q, F f) {
   const int lane = threadIdx.x & 31;
   const int64_t nwarps = (int64_t)gridDim.x * (blockDim.x >> 5);
@@ -273,7 +274,11 @@ __device__ __forceinline__ int warp_foreach_bit(const uint32_t* __restrict__ bv,
   int fill = 0, seen = 0;
   auto flush = [&]() {
     __syncwarp();
-    for (int base = 0; base < fill; base += 32) f(base + lane < fill ? q[base + lane] : kNoHe, base + lane < fill);
+    if constexpr (WHOLE) {
+      f(q, fill);
+    } else {
+      for (int base = 0; base < fill; base += 32) f(base + lane < fill ? q[base + lane] : kNoHe, base + lane < fill);
+    }
     __syncwarp();
     fill = 0;
   };
