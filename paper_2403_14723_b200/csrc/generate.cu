@@ -31,6 +31,13 @@ __device__ __forceinline__ bool f1_of(const uint32_t* __restrict__ F1, int64_t T
 #define POLYLLA_REPAIR_THREADS 128
 #endif
 constexpr int kRepairThreads = POLYLLA_REPAIR_THREADS;
+#ifndef POLYLLA_REPAIR_DYN
+#define POLYLLA_REPAIR_DYN 1
+#endif
+#ifndef POLYLLA_SEED_BURST
+#define POLYLLA_SEED_BURST 4
+#endif
+constexpr int kSeedBurst = POLYLLA_SEED_BURST;  // walk steps between per-lane refills (k_repair_mid, k_seed_walk)
 #ifndef POLYLLA_ROT_MAX
 #define POLYLLA_ROT_MAX 16
 #endif
@@ -46,6 +53,73 @@ __global__ void __launch_bounds__(kRepairThreads)
   if (ctr->status) return;
   const int64_t T3 = 3 * T;
   const int lane = threadIdx.x & 31;
+#if POLYLLA_REPAIR_DYN
+  // per-lane refill (as in k_seed_walk): a lane done with its tip takes the queue's next one;
+  // the degree walk and the middle-edge walk are the same step (x <- next_in(twin x))
+  warp_foreach_bit<true>(TB, n_words, queue[threadIdx.x >> 5], [&](const hid* q, int fill) {
+    int base = 0;
+    if (lane == 0) base = atomicAdd(&ctr->n_tips, fill);
+    base = __shfl_sync(0xffffffffu, base, 0);
+    int head = 0, idx = 0;
+    bool active = false, second = false;
+    hid e0 = 0, x = 0;
+    int64_t d = 0, st = 0, target = 0;
+    while (true) {
+      const uint32_t idle = __ballot_sync(0xffffffffu, !active);
+      if (head < fill && idle) {
+        const int my = head + __popc(idle & ((1u << lane) - 1));
+        head += __popc(idle);
+        if (!active && my < fill) {
+          const hid e = q[my];
+          idx = base + my;
+          tips[idx] = e;
+          e0 = twin[e];  // the tip's only outgoing frontier half-edge
+          x = e0;
+          d = 0;
+          second = false;
+          active = true;
+        }
+      }
+      if (!__any_sync(0xffffffffu, active)) {
+        if (head >= fill) break;
+        continue;
+      }
+#pragma unroll 1
+      for (int k = 0; k < kSeedBurst && active; ++k) {
+        bool done = false;
+        if (!second) {  // degree(v): rotation closure about v (an interior vertex); deg(v) <= 3T
+          const hid tx = twin[x];
+          if (tx >= T3 || ++d > T3) {
+            raise_status(ctr, ST_WALK);
+            aff[2 * idx] = aff[2 * idx + 1] = e0;
+            active = false;
+            break;
+          }
+          x = next_in(tx);
+          if (x == e0) {  // floor((d-1)/2) CWvertexEdge steps (R1, R5) from e0
+            second = true;
+            target = (d - 1) / 2;
+            st = 0;
+            done = target == 0;
+          }
+        } else {
+          x = next_in(twin[x]);
+          done = ++st == target;
+        }
+        if (done) {
+          const hid m = x, tm = twin[m];
+          atomicOr(&F1[m >> 5], 1u << (m & 31));
+          atomicOr(&F1[tm >> 5], 1u << (tm & 31));
+          atomicOr(&SDB[m >> 5], 1u << (m & 31));  // both halves seed the split polygons
+          atomicOr(&SDB[tm >> 5], 1u << (tm & 31));
+          aff[2 * idx] = e0;      // outgoing from v
+          aff[2 * idx + 1] = tm;  // outgoing from u = target(m)
+          active = false;
+        }
+      }
+    }
+  });
+#else
   warp_foreach_bit(TB, n_words, queue[threadIdx.x >> 5], [&](hid e, bool valid) {
     const uint32_t m32 = __ballot_sync(0xffffffffu, valid);
     int base = 0;
@@ -77,6 +151,7 @@ __global__ void __launch_bounds__(kRepairThreads)
     aff[2 * i] = e0;     // outgoing from v
     aff[2 * i + 1] = tm; // outgoing from u = target(m)
   });
+#endif
 }
 
 __global__ void __launch_bounds__(kRepairThreads)
@@ -155,10 +230,7 @@ constexpr int kSeedThreads = POLYLLA_SEED_THREADS;
 #ifndef POLYLLA_SEED_DYN
 #define POLYLLA_SEED_DYN 1
 #endif
-#ifndef POLYLLA_SEED_BURST
-#define POLYLLA_SEED_BURST 4
-#endif
-constexpr int kSeedBurst = POLYLLA_SEED_BURST;
+
 
 __device__ __forceinline__ void process_seed(hid s, int64_t T3, int64_t H, const hid* __restrict__ twin,
                                              const hid* __restrict__ next, const uint32_t* __restrict__ F1,
